@@ -1,0 +1,194 @@
+/*
+ * commtrace_b200 — C ABI of the B200-native trace → communication-matrix path.
+ *
+ * This is the drop-in boundary for the reference's analysis entry point
+ *   analyze_events(events, d=None, config=ModelConfig())   pkg/src/commtrace/matrix.py:316-347
+ * and its siblings split_by_primitive (matrix.py:261), summarize (matrix.py:279),
+ * group_collectives (grouping.py:82) and match_p2p (decompose.py:342).  The
+ * reference has no FFI of its own (it is pure Python); INTEGRATION.md shows the
+ * ctypes stub a maintainer adds to matrix.py to call this library instead.
+ *
+ * Plain C types only: no torch, no CUDA types in signatures (streams are void*).
+ * Every entry point returns a ct_status; CT_ERR_* codes map 1:1 onto the
+ * reference's exception classes (errors.py:9-56 plus OverflowError).
+ */
+#ifndef COMMTRACE_B200_H
+#define COMMTRACE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CT_ABI_VERSION 1
+
+/* ---------------------------------------------------------------- records
+ * One trace record (one JSONL line of the reference wire format,
+ * events.py:8-24), packed to 32 bytes.  The record size is the roofline unit.
+ */
+typedef struct ct_record {
+  uint64_t count;   /* collective/p2p element count; copy byte count          */
+  uint64_t seq;     /* per-(comm, rank) sequence counter                       */
+  uint32_t comm;    /* interned communicator id                                */
+  uint16_t nranks;  /* communicator size N                                     */
+  uint16_t rank;    /* caller rank                                             */
+  uint16_t dev;     /* caller GPU                                              */
+  uint16_t aux;     /* root (bcast/reduce) | peer (send/recv) | copy src GPU    */
+  uint16_t aux2;    /* copy dst GPU                                            */
+  uint8_t kc;       /* kind[0:3] | coll[3:6] | has_root[6]                     */
+  uint8_t ad;       /* algo[0:2] | dtype[2:6] | ckind[6:8]                     */
+} ct_record;
+
+enum { CT_KIND_COLLECTIVE = 0, CT_KIND_SEND = 1, CT_KIND_RECV = 2,
+       CT_KIND_MEMCPY = 3, CT_KIND_UM = 4, CT_KIND_ZEROCOPY = 5 };
+enum { CT_COLL_ALLREDUCE = 0, CT_COLL_BROADCAST = 1, CT_COLL_REDUCE = 2,
+       CT_COLL_REDUCESCATTER = 3, CT_COLL_ALLGATHER = 4 };
+enum { CT_ALGO_RING = 0, CT_ALGO_TREE = 1, CT_ALGO_COLLNET = 2, CT_ALGO_AUTO = 3 };
+enum { CT_CKIND_H2D = 0, CT_CKIND_D2H = 1, CT_CKIND_D2D = 2 };
+
+/* matrix/statistics type keys, in the reference's ALL_TYPES order (matrix.py:39-44) */
+enum { CT_T_ALLREDUCE = 0, CT_T_BROADCAST, CT_T_REDUCE, CT_T_REDUCESCATTER, CT_T_ALLGATHER,
+       CT_T_SENDRECV, CT_T_EXPLICIT, CT_T_UNIFIED, CT_T_ZEROCOPY, CT_NTYPES };
+
+/* diagnostic reasons (grouping.py:64-65) */
+enum { CT_DIAG_INCOMPLETE = 0, CT_DIAG_INCOMPATIBLE, CT_DIAG_DUPLICATE_DEVICE,
+       CT_DIAG_UNMATCHED_SEND, CT_DIAG_UNMATCHED_RECV, CT_DIAG_MISMATCHED_P2P, CT_NDIAG };
+
+/* ---------------------------------------------------------------- status */
+typedef enum ct_status {
+  CT_OK = 0,
+  CT_ERR_INVARIANT = 1,       /* InvariantViolation: nranks disagreement / duplicate seq */
+  CT_ERR_INVALID_CONFIG = 2,  /* InvalidConfig: ring order is not a permutation          */
+  CT_ERR_ENDPOINT_RANGE = 3,  /* EndpointOutOfRange: transfer GPU >= d                    */
+  CT_ERR_OVERFLOW = 4,        /* OverflowError: a matrix cell exceeds 2^63-1              */
+  CT_ERR_WRONG_ALGORITHM = 5, /* WrongAlgorithm                                           */
+  CT_ERR_MISSING_ROOT = 6,    /* MissingRoot                                              */
+  CT_ERR_ARGUMENT = 20,       /* bad argument to this API                                 */
+  CT_ERR_CUDA = 21,           /* CUDA runtime failure (message via ct_last_error)         */
+  CT_ERR_NOT_CANONICAL = 22,  /* force_path=FAST on a trace the fast path cannot take      */
+  CT_ERR_CAPACITY = 23        /* a fixed-capacity table overflowed (see ct_last_error)     */
+} ct_status;
+
+/* ---------------------------------------------------------------- config
+ * Mirrors ModelConfig (matrix.py:207-222) plus the analyze_events ``d`` argument.
+ */
+typedef struct ct_config {
+  int64_t d;                  /* matrix GPU count; -1 = infer (matrix.py:250-258)      */
+  uint64_t tree_threshold;    /* AUTO allreduce: tree below, ring at/above (decompose.py:44) */
+  int32_t ring_len;           /* 0 = identity rings; else ring applies where N == ring_len */
+  int32_t force_path;         /* 0 auto, 1 fast (canonical layout only), 2 exact       */
+  const uint16_t *ring_order; /* host pointer, ring_len entries (need not be a permutation:
+                                 an invalid order raises InvalidConfig only when used)  */
+  int32_t dev_hint;           /* >0: caller's bound on (max GPU id + 1); sizes histograms */
+  int32_t n_comms;            /* number of interned communicator ids (max comm + 1)     */
+} ct_config;
+
+/* ---------------------------------------------------------------- summary
+ * Everything except the cells.  Cells are fetched with ct_result_cells in the
+ * internal index layout: [type][src][dst] with g2 = g_cap + 2 and endpoint index
+ * host = 0, net = 1, gpu g = g + 2 (the host-side wrapper remaps to the reference's
+ * host = 0, gpu g = g + 1, net = d + 1 layout, matrix.py:82-102).
+ */
+typedef struct ct_summary {
+  int32_t status;
+  int32_t path;               /* 1 = fast (canonical), 2 = exact (sort-based join)      */
+  int64_t d;
+  int32_t g_cap;              /* GPUs covered by the cell arrays                        */
+  int32_t net_used;           /* bit t set: type t received a collnet transfer          */
+  uint64_t calls[CT_NTYPES];
+  uint64_t payload_lo[CT_NTYPES];
+  uint64_t payload_hi[CT_NTYPES];
+  uint64_t diag[CT_NDIAG];
+  uint64_t type_first[CT_NTYPES]; /* position of type t in the per_primitive dict order
+                                     (matrix.py:334-335); ~0 when the type is absent */
+  uint64_t n_records;
+  /* error detail (valid when status != CT_OK) */
+  uint64_t err_index;         /* record index involved (global numbering)               */
+  uint64_t err_aux[4];
+  /* timing of the last call, device-measured */
+  float ms_total;
+  float ms_kernel;            /* the fused expand+accumulate kernel alone               */
+  uint32_t n_launches;        /* kernels launched by this call                          */
+  uint32_t reserved;
+} ct_summary;
+
+typedef struct ct_context ct_context;
+
+/* Create a context bound to CUDA device ``device``; owns scratch and the stream. */
+int ct_context_create(int device, ct_context **out);
+int ct_context_destroy(ct_context *ctx);
+const char *ct_last_error(ct_context *ctx);
+
+/* Analyze n records.  ``recs`` is device memory when on_device != 0, else host
+ * memory (copied in inside the call).  ``stream`` may be NULL (context stream).
+ * Synchronous: returns when the summary is filled.
+ * Replaces analyze_events (matrix.py:316-347) on a packed trace. */
+int ct_analyze(ct_context *ctx, const ct_record *recs, uint64_t n, int on_device,
+               const ct_config *cfg, ct_summary *out, void *stream);
+
+/* Copy the last result's cells: bytes and freq, each CT_NTYPES*g2*g2 uint64
+ * (g2 = out->g_cap + 2).  Host pointers. */
+int ct_result_cells(ct_context *ctx, uint64_t *bytes, uint64_t *freq, uint64_t n_cells);
+
+/* Materialise the grouping of the last analyzed trace for the Python-object lists
+ * AnalysisResult.instances / .diagnostics (group_collectives, grouping.py:82-183, and
+ * match_p2p, decompose.py:342-394), computed by the exact join on the device.
+ * ct_result_groups: rows of 5 uint64 {comm, ordinal, status, n_members, member_off} in
+ *   reference order (comm first-seen, ordinal); status 0 = instance, else CT_DIAG_*+1;
+ *   members = original record indices (rank order), rows concatenated.
+ * ct_result_p2p_diags: rows of 7 uint64 {reason, comm, src, dst, k, send_idx, recv_idx}
+ *   (~0 for a missing side), per channel in (comm id, src, dst) order.
+ * Call with null buffers to query the sizes. */
+int ct_result_groups(ct_context *ctx, uint64_t *rows, uint64_t row_cap, uint64_t *members,
+                     uint64_t member_cap, uint64_t *n_rows, uint64_t *n_members);
+int ct_result_p2p_diags(ct_context *ctx, uint64_t *rows, uint64_t row_cap, uint64_t *n_rows);
+/* Run the materialising join on ``recs`` (instead of the last analyzed trace).  Fatal
+ * grouping errors (duplicate seq, nranks disagreement) are reported in ``out`` exactly
+ * as ct_analyze reports them. */
+int ct_materialize(ct_context *ctx, const ct_record *recs, uint64_t n, int on_device, int32_t n_comms,
+                   ct_summary *out);
+
+/* infer_device_count (matrix.py:250-258): max(dev, copy GPU endpoint) + 1 over all records. */
+int ct_infer_device_count(ct_context *ctx, const ct_record *recs, uint64_t n, int on_device, int64_t *d);
+
+/* Emit mode: per-record transfers of canonical instance blocks (decompose_instance,
+ * decompose.py:292-406).  Records must form canonical blocks (ranks 0..n-1
+ * consecutive; a send directly followed by its recv).  Output rows of 7 int64
+ * {block/record index, src endpoint, dst endpoint, bytes_lo, bytes_hi, src rank, sub}
+ * (endpoint: gpu id, -1 = net, -2 = host; sub = destination rank of a collective
+ * edge, 0/1 for collnet dev->net / net->dev).  Rows are grouped per record; callers
+ * order them per instance. */
+int ct_emit_transfers(ct_context *ctx, const ct_record *recs, uint64_t n, int on_device,
+                      const ct_config *cfg, int64_t *rows, uint64_t row_cap, uint64_t *n_rows);
+
+/* Synthetic workload generators writing packed records on the
+ * device: kind 2 = C2 mixed collectives, 3 = C3 mixed with p2p/copies,
+ * 4 = C4 bucketed gradient allreduce, 5 = C5 ring/tree sweep.  Records
+ * [first, first + n) of the infinite seeded stream are written to dev_out. */
+int ct_generate(ct_context *ctx, int kind, uint64_t seed, uint64_t first, uint64_t n,
+                ct_record *dev_out, void *stream);
+/* Shape of the C4 (ResNet-50, 25 MiB buckets) generator: tensor and bucket counts and
+ * the bucket byte sizes (bucket_bytes may be NULL; else room for 64 entries). */
+void ct_c4_shape(uint64_t *n_tensors, uint64_t *n_buckets, uint64_t *bucket_bytes);
+/* Record index of the first element boundary (block head / send / copy) at or
+ * after ``at`` for generator ``kind`` — shard cut points for multi-GPU runs. */
+uint64_t ct_generate_boundary(int kind, uint64_t at);
+
+/* Multi-GPU (one process per GPU): each rank analyzes its shard,
+ * exports a fixed-size uint64 partial (device memory) that the host all-gathers
+ * over NCCL, then merges the ``world`` gathered partials (rank order == shard
+ * order) into the final result.  Sums are exact: cells are < 2^63 per shard and
+ * are re-checked against the 63-bit bound after merging (matrix.py:164-178);
+ * shard-boundary chains (seq order across shards) are re-validated from the
+ * boundary records carried in each partial.  All ranks must use the same g_cap
+ * (set ct_config.d or dev_hint). */
+int ct_partial_size(ct_context *ctx, uint64_t *words);
+int ct_partial_export(ct_context *ctx, uint64_t *dev_out, uint64_t words, void *stream);
+int ct_partial_merge(ct_context *ctx, const uint64_t *dev_in, int world, uint64_t words,
+                     ct_summary *out, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,957 @@
+// C ABI (include/commtrace_b200.h): context, path dispatch, finalisation.
+//
+// ct_analyze runs the fast kernel on the trace as given; if its layout preconditions
+// fail it canonicalises the trace with the exact sort-based join (ct_exact.cu) and runs
+// the fast kernel on the canonical stream.  There is no host fallback: every record is
+// classified, joined, expanded and accumulated on the device; the host only reads back
+// a few kilobytes of counters and maps flags to the reference's exception classes.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "ct_exact.cuh"
+#include "ct_fast.cuh"
+
+namespace ct {
+__global__ void fast_kernel(FastParams P);
+__global__ void chain_sort_check_kernel(const ct_record* recs, uint64_t n, const ChainEntry* chain,
+                                        GlobalState* st);
+__global__ void chain_check_kernel(const ct_record* recs, uint64_t n, const ChainEntry* chain,
+                                   const uint32_t* order, uint32_t count, GlobalState* st);
+int generate(int kind, uint64_t seed, uint64_t first, uint64_t n, ct_record* out, cudaStream_t st);
+uint64_t generate_boundary(int kind, uint64_t at);
+void launch_emit(const ct_record* recs, uint64_t n, const ExpandParams& ex, uint32_t* counts,
+                 const uint64_t* offsets, int64_t* rows, int pass, unsigned int* flags, cudaStream_t st);
+}  // namespace ct
+
+using namespace ct;
+
+struct ct_context {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int num_sms = 148;
+  std::string err;
+  ct_record* in_buf = nullptr;
+  uint64_t in_cap = 0;
+  GlobalState* st = nullptr;
+  unsigned long long* cells = nullptr;  // bytes then freq
+  size_t cells_cap = 0;                 // entries per array
+  unsigned long long* tcf = nullptr;    // [5][n_comms] type_comm_first, then [n_comms] comm_first
+  size_t tcf_cap = 0;
+  ChainEntry* chain = nullptr;
+  uint32_t chain_cap = 0;
+  uint16_t* ring = nullptr;  // order then inverse
+  int ring_cap = 0;
+  cudaEvent_t ev[4];
+  // last result
+  ct_summary last{};
+  int last_g2 = 0;
+  GlobalState last_state{};
+  const ct_record* last_input = nullptr;  // device pointer of last analysed array
+  uint64_t last_n = 0;
+  uint32_t last_comms = 0;
+  bool mat_valid = false;
+  ExactResult mat;
+  ct_record* canon_keep = nullptr;  // exact-path canonical stream of the last call
+  bool last_explicit = false;
+  uint64_t canon_n = 0;
+};
+
+namespace {
+
+int fail(ct_context* c, int code, const std::string& msg) {
+  if (c) c->err = msg;
+  return code;
+}
+
+int cuda_fail(ct_context* c, cudaError_t e, const char* where) {
+  return fail(c, CT_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CTX_TRY(c, x)                                        \
+  do {                                                       \
+    cudaError_t e_ = (x);                                    \
+    if (e_ != cudaSuccess) return cuda_fail(c, e_, #x);      \
+  } while (0)
+
+template <typename T>
+int ensure(ct_context* c, T*& p, size_t& cap, size_t need) {
+  if (need <= cap && p) return 0;
+  if (p) cudaFree(p);
+  p = nullptr;
+  size_t n = std::max(need, (size_t)1);
+  cudaError_t e = cudaMalloc(&p, n * sizeof(T));
+  if (e != cudaSuccess) { cap = 0; return cuda_fail(c, e, "cudaMalloc"); }
+  cap = n;
+  return 0;
+}
+
+struct RunOut {
+  GlobalState gs;
+  float ms_kernel;
+  uint32_t launches;
+};
+
+// One pass of the fast kernel (+ cross-CTA chain check) over ``recs``.
+int run_fast(ct_context* c, const ct_record* recs, uint64_t n, int gcap, bool explicit_d,
+             const ExpandParams& ex, uint32_t n_comms, cudaStream_t st, RunOut* out) {
+  const int g2 = gcap + 2;
+  const size_t ncell = (size_t)kTypes * g2 * g2;
+  if (ensure(c, c->cells, c->cells_cap, 2 * ncell)) return CT_ERR_CUDA;
+  size_t tcf_need = 6 * (size_t)std::max<uint32_t>(n_comms, 1);
+  if (ensure(c, c->tcf, c->tcf_cap, tcf_need)) return CT_ERR_CUDA;
+  const uint64_t n_subs = (n + kSub - 1) / kSub;
+  uint32_t grid = (uint32_t)std::min<uint64_t>(n_subs, (uint64_t)c->num_sms);
+  if (grid == 0) grid = 1;
+  uint32_t per = (uint32_t)((n_subs + grid - 1) / grid);
+  if (per == 0) per = 1;
+  grid = (uint32_t)((n_subs + per - 1) / per);
+  if (grid == 0) grid = 1;
+  // chain list capacity: every warp table of every CTA could be full
+  size_t cc = c->chain_cap;
+  if (ensure(c, c->chain, cc, (size_t)grid * kWarps * kChainW)) return CT_ERR_CUDA;
+  c->chain_cap = (uint32_t)cc;
+
+  CTX_TRY(c, cudaMemsetAsync(c->st, 0, sizeof(GlobalState), st));
+  CTX_TRY(c, cudaMemsetAsync(c->cells, 0, 2 * ncell * sizeof(unsigned long long), st));
+  CTX_TRY(c, cudaMemsetAsync(c->tcf, 0xFF, tcf_need * sizeof(unsigned long long), st));
+  {
+    GlobalState init{};
+    init.max_dev = -1;
+    for (int k = 0; k < 3; k++) init.copy_first[k] = ~0ull;
+    init.oor_key = ~0ull;
+    init.of_cell = ~0ull;
+    CTX_TRY(c, cudaMemcpyAsync(c->st, &init, sizeof init, cudaMemcpyHostToDevice, st));
+  }
+  FastParams P{};
+  P.recs = recs;
+  P.n = n;
+  P.base = 0;
+  P.gcap = gcap;
+  P.g2 = g2;
+  P.explicit_d = explicit_d;
+  P.ex = ex;
+  P.n_comms = n_comms;
+  const size_t smem_full = fast_smem_bytes(g2, 1);
+  P.smem_hist = smem_full <= 227 * 1024 ? 1 : 0;
+  const size_t smem = fast_smem_bytes(g2, P.smem_hist);
+  P.st = c->st;
+  P.cells = c->cells;
+  P.freq = c->cells + ncell;
+  P.type_comm_first = c->tcf;
+  P.comm_first = c->tcf + 5 * (size_t)std::max<uint32_t>(n_comms, 1);
+  P.chain = c->chain;
+  P.chain_cap = c->chain_cap;
+  P.subs_per_cta = per;
+  P.n_subs = (uint32_t)n_subs;
+  uint32_t launches = 0;  // kernels launched (cudaMemset/Memcpy are copy-engine work)
+  out->ms_kernel = 0;
+  if (n) {
+    CTX_TRY(c, cudaFuncSetAttribute(fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CTX_TRY(c, cudaEventRecord(c->ev[0], st));
+    fast_kernel<<<grid, kThreads, smem, st>>>(P);
+    CTX_TRY(c, cudaGetLastError());
+    CTX_TRY(c, cudaEventRecord(c->ev[1], st));
+    const int csm = (int)(kChainSortMax * (8 + 8 + 4));
+    CTX_TRY(c, cudaFuncSetAttribute(chain_sort_check_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, csm));
+    chain_sort_check_kernel<<<1, 1024, csm, st>>>(recs, n, c->chain, c->st);
+    CTX_TRY(c, cudaGetLastError());
+    launches += 2;
+  }
+  CTX_TRY(c, cudaMemcpyAsync(&out->gs, c->st, sizeof(GlobalState), cudaMemcpyDeviceToHost, st));
+  CTX_TRY(c, cudaStreamSynchronize(st));
+  if (n) CTX_TRY(c, cudaEventElapsedTime(&out->ms_kernel, c->ev[0], c->ev[1]));
+  const uint32_t E = std::min(out->gs.n_chain, c->chain_cap);
+  if (E > 1 && (out->gs.flags & F_CHAIN_BIG) && !(out->gs.flags & F_NONCANON)) {
+    // order entries by (key, first) with two stable radix passes, then check neighbours
+    uint64_t *k1, *k2;
+    uint32_t *v1, *v2;
+    CTX_TRY(c, cudaMallocAsync(&k1, E * 8, st));
+    CTX_TRY(c, cudaMallocAsync(&k2, E * 8, st));
+    CTX_TRY(c, cudaMallocAsync(&v1, E * 4, st));
+    CTX_TRY(c, cudaMallocAsync(&v2, E * 4, st));
+    std::vector<ChainEntry> h(E);
+    CTX_TRY(c, cudaMemcpyAsync(h.data(), c->chain, E * sizeof(ChainEntry), cudaMemcpyDeviceToHost, st));
+    CTX_TRY(c, cudaStreamSynchronize(st));
+    std::vector<uint64_t> hk(E), hf(E);
+    std::vector<uint32_t> hv(E);
+    for (uint32_t i = 0; i < E; i++) { hk[i] = h[i].key; hf[i] = h[i].first; hv[i] = i; }
+    CTX_TRY(c, cudaMemcpyAsync(k1, hf.data(), E * 8, cudaMemcpyHostToDevice, st));
+    CTX_TRY(c, cudaMemcpyAsync(v1, hv.data(), E * 4, cudaMemcpyHostToDevice, st));
+    size_t tmp = 0;
+    void* t = nullptr;
+    CTX_TRY(c, cub::DeviceRadixSort::SortPairs(nullptr, tmp, k1, k2, v1, v2, E, 0, 64, st));
+    CTX_TRY(c, cudaMallocAsync(&t, tmp, st));
+    CTX_TRY(c, cub::DeviceRadixSort::SortPairs(t, tmp, k1, k2, v1, v2, E, 0, 64, st));
+    // second pass keys: chain key of the sorted entries
+    std::vector<uint32_t> hv2(E);
+    CTX_TRY(c, cudaMemcpyAsync(hv2.data(), v2, E * 4, cudaMemcpyDeviceToHost, st));
+    CTX_TRY(c, cudaStreamSynchronize(st));
+    for (uint32_t i = 0; i < E; i++) hk[i] = h[hv2[i]].key;
+    CTX_TRY(c, cudaMemcpyAsync(k1, hk.data(), E * 8, cudaMemcpyHostToDevice, st));
+    CTX_TRY(c, cub::DeviceRadixSort::SortPairs(t, tmp, k1, k2, v2, v1, E, 0, 64, st));
+    chain_check_kernel<<<(E + 255) / 256, 256, 0, st>>>(recs, n, c->chain, v1, E, c->st);
+    CTX_TRY(c, cudaGetLastError());
+    CTX_TRY(c, cudaMemcpyAsync(&out->gs.flags, &c->st->flags, 4, cudaMemcpyDeviceToHost, st));
+    CTX_TRY(c, cudaStreamSynchronize(st));
+    cudaFreeAsync(t, st);
+    cudaFreeAsync(k1, st);
+    cudaFreeAsync(k2, st);
+    cudaFreeAsync(v1, st);
+    cudaFreeAsync(v2, st);
+    launches += 3;
+  }
+  out->launches = launches;
+  return 0;
+}
+
+__global__ void k_max_dev(const ct_record* recs, uint64_t n, int* out) {
+  int m = -1;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const ct_record& r = recs[i];
+    m = max(m, (int)r.dev);
+    if ((r.kc & 7) >= CT_KIND_MEMCPY) {
+      const int ck = (r.ad >> 6) & 3;
+      if (ck != CT_CKIND_H2D) m = max(m, (int)r.aux);
+      if (ck != CT_CKIND_D2H) m = max(m, (int)r.aux2);
+    }
+  }
+  atomicMax(out, m);
+}
+
+int host_dev_of(ct_context* c, const ct_record* recs, uint64_t i, cudaStream_t st, ct_record* out) {
+  CTX_TRY(c, cudaMemcpyAsync(out, recs + i, sizeof(ct_record), cudaMemcpyDeviceToHost, st));
+  CTX_TRY(c, cudaStreamSynchronize(st));
+  return 0;
+}
+
+// Summary from a (possibly merged) GlobalState plus the cells / first-index tables in
+// the context: dict order, net flags, the combined 63-bit bound and the reference's
+// status precedence (decomposition errors before accumulation errors).
+int summarize_state(ct_context* c, const GlobalState& gs, int gcap, int64_t d, int path,
+                    const uint64_t extra_diag[3], const ct_record* arr, uint32_t n_comms,
+                    cudaStream_t st, ct_summary* out) {
+  const int g2 = gcap + 2;
+  const size_t ncell = (size_t)kTypes * g2 * g2;
+  c->last_state = gs;
+  c->last_g2 = g2;
+  out->path = path;
+  out->d = d;
+  out->g_cap = gcap;
+  for (int t = 0; t < kTypes; t++) {
+    out->calls[t] = gs.calls[t];
+    out->payload_lo[t] = gs.pay_lo[t];
+    out->payload_hi[t] = gs.pay_hi[t];
+  }
+  for (int k = 0; k < CT_NDIAG; k++) out->diag[k] = gs.diag[k];
+  out->diag[CT_DIAG_INCOMPLETE] += extra_diag[0];
+  out->diag[CT_DIAG_UNMATCHED_SEND] += extra_diag[1];
+  out->diag[CT_DIAG_UNMATCHED_RECV] += extra_diag[2];
+  // per_primitive dict order (matrix.py:334-335): collectives by (comm first-seen,
+  // first valid instance), then sendrecv, then copies by first event
+  {
+    std::vector<unsigned long long> tcf(6 * (size_t)n_comms);
+    CTX_TRY(c, cudaMemcpyAsync(tcf.data(), c->tcf, tcf.size() * 8, cudaMemcpyDeviceToHost, st));
+    CTX_TRY(c, cudaStreamSynchronize(st));
+    const unsigned long long* cf = tcf.data() + 5 * (size_t)n_comms;
+    std::vector<std::pair<std::pair<uint64_t, uint64_t>, int>> order;
+    for (int t = 0; t < 5; t++) {
+      uint64_t best_c = ~0ull, best_i = ~0ull;
+      for (uint32_t cm = 0; cm < n_comms; cm++) {
+        const uint64_t v = tcf[(size_t)t * n_comms + cm];
+        if (v == ~0ull) continue;
+        if (cf[cm] < best_c || (cf[cm] == best_c && v < best_i)) { best_c = cf[cm]; best_i = v; }
+      }
+      order.push_back({{best_c, best_i}, t});
+    }
+    std::sort(order.begin(), order.end());
+    for (int k = 0; k < 5; k++)
+      out->type_first[order[k].second] = order[k].first.first == ~0ull ? ~0ull : (uint64_t)k;
+    out->type_first[CT_T_SENDRECV] = gs.calls[CT_T_SENDRECV] ? 5 : ~0ull;
+    std::vector<std::pair<uint64_t, int>> copies;
+    for (int k = 0; k < 3; k++) copies.push_back({gs.copy_first[k], k});
+    std::sort(copies.begin(), copies.end());
+    for (int k = 0; k < 3; k++)
+      out->type_first[CT_T_EXPLICIT + copies[k].second] = copies[k].first == ~0ull ? ~0ull : (uint64_t)(6 + k);
+  }
+  // cells, net flags, combined 63-bit bound (matrix.py:110-113)
+  std::vector<unsigned long long> h(2 * ncell);
+  CTX_TRY(c, cudaMemcpyAsync(h.data(), c->cells, 2 * ncell * 8, cudaMemcpyDeviceToHost, st));
+  CTX_TRY(c, cudaStreamSynchronize(st));
+  bool overflow = (gs.flags & F_OVERFLOW) != 0;
+  uint64_t of_cell = ~0ull;
+  int net_used = 0;
+  for (int t = 0; t < kTypes; t++)
+    for (int a = 0; a < g2; a++)
+      if (h[ncell + ((size_t)t * g2 + a) * g2 + kNet] || h[ncell + ((size_t)t * g2 + kNet) * g2 + a])
+        net_used |= 1 << t;
+  for (int a = 0; a < g2; a++)
+    for (int b = 0; b < g2; b++) {
+      unsigned __int128 sum = 0;
+      for (int t = 0; t < kTypes; t++) sum += h[((size_t)t * g2 + a) * g2 + b];
+      if (sum > (unsigned __int128)INT64_MAX) {
+        overflow = true;
+        if (of_cell == ~0ull) of_cell = ((uint64_t)a << 32) | (uint64_t)b;
+      }
+    }
+  if (overflow && of_cell == ~0ull && gs.of_cell != ~0ull) {  // a per-type sum wrapped past 2^64
+    const uint64_t a = (gs.of_cell / g2) % g2, b = gs.of_cell % g2;
+    of_cell = (a << 32) | b;
+  }
+  out->net_used = net_used;
+  if (gs.flags & F_COMM_RANGE) return fail(c, CT_ERR_ARGUMENT, "record comm id >= n_comms");
+  if (gs.flags & F_BAD_RING) out->status = CT_ERR_INVALID_CONFIG;
+  else if (gs.flags & F_WRONG_ALGO) out->status = CT_ERR_WRONG_ALGORITHM;
+  else if (gs.flags & F_MISSING_ROOT) out->status = CT_ERR_MISSING_ROOT;
+  else if (gs.flags & F_OOR) {
+    out->status = CT_ERR_ENDPOINT_RANGE;
+    const uint64_t k = gs.oor_key;
+    const uint64_t cls = k >> 62, elem = (k >> 21) & ((1ull << 41) - 1);
+    const uint64_t a = (k >> 11) & 1023, sub = (k >> 1) & 1023, which = k & 1;
+    ct_record r{};
+    uint64_t gpu = 0;
+    if (!arr) {
+      gpu = gs.err_index;  // merged partials carry the offending GPU id
+    } else if (cls == 0) {
+      ct_record head{};
+      if (host_dev_of(c, arr, elem, st, &head)) return CT_ERR_CUDA;
+      const bool collnet = (head.ad & 3) == CT_ALGO_COLLNET && ((head.kc >> 3) & 7) == CT_COLL_ALLREDUCE;
+      const uint64_t rank = which == 0 || collnet ? a : sub;
+      if (host_dev_of(c, arr, elem + rank, st, &r)) return CT_ERR_CUDA;
+      gpu = r.dev;
+    } else if (cls == 1) {
+      if (host_dev_of(c, arr, elem + which, st, &r)) return CT_ERR_CUDA;
+      gpu = r.dev;
+    } else {
+      if (host_dev_of(c, arr, elem, st, &r)) return CT_ERR_CUDA;
+      gpu = which ? r.aux2 : r.aux;
+    }
+    out->err_aux[0] = gpu;
+    out->err_aux[1] = (uint64_t)d;
+  } else if (overflow) {
+    out->status = CT_ERR_OVERFLOW;
+    out->err_aux[0] = of_cell;
+  }
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ct_context_create(int device, ct_context** out) {
+  if (!out) return CT_ERR_ARGUMENT;
+  ct_context* c = new ct_context();
+  c->device = device;
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+  for (int k = 0; k < 4 && e == cudaSuccess; k++) e = cudaEventCreate(&c->ev[k]);
+  if (e == cudaSuccess) e = cudaMalloc(&c->st, sizeof(GlobalState));
+  if (e != cudaSuccess) {
+    delete c;
+    return CT_ERR_CUDA;
+  }
+  *out = c;
+  return CT_OK;
+}
+
+int ct_context_destroy(ct_context* c) {
+  if (!c) return CT_ERR_ARGUMENT;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  cudaFree(c->in_buf);
+  cudaFree(c->st);
+  cudaFree(c->cells);
+  cudaFree(c->tcf);
+  cudaFree(c->chain);
+  cudaFree(c->ring);
+  if (c->canon_keep) cudaFree(c->canon_keep);
+  for (int k = 0; k < 4; k++) cudaEventDestroy(c->ev[k]);
+  cudaStreamDestroy(c->stream);
+  delete c;
+  return CT_OK;
+}
+
+const char* ct_last_error(ct_context* c) { return c ? c->err.c_str() : "null context"; }
+
+int ct_analyze(ct_context* c, const ct_record* recs, uint64_t n, int on_device, const ct_config* cfg,
+               ct_summary* out, void* stream) {
+  if (!c || !cfg || !out || (n && !recs)) return fail(c, CT_ERR_ARGUMENT, "null argument");
+  CTX_TRY(c, cudaSetDevice(c->device));
+  cudaStream_t st = stream ? (cudaStream_t)stream : c->stream;
+  memset(out, 0, sizeof *out);
+  out->n_records = n;
+  c->mat_valid = false;
+  if (c->canon_keep) { cudaFree(c->canon_keep); c->canon_keep = nullptr; c->canon_n = 0; }
+  CTX_TRY(c, cudaEventRecord(c->ev[2], st));
+  const ct_record* d_recs = recs;
+  if (!on_device && n) {
+    size_t cap = c->in_cap;
+    if (ensure(c, c->in_buf, cap, n)) return CT_ERR_CUDA;
+    c->in_cap = cap;
+    CTX_TRY(c, cudaMemcpyAsync(c->in_buf, recs, n * sizeof(ct_record), cudaMemcpyHostToDevice, st));
+    d_recs = c->in_buf;
+  }
+  c->last_input = d_recs;
+  c->last_n = n;
+  const uint32_t n_comms = (uint32_t)std::max(cfg->n_comms, 1);
+  c->last_comms = n_comms;
+  if (n_comms >= (1u << 31)) return fail(c, CT_ERR_ARGUMENT, "more than 2^31 communicators");
+
+  // ring order: validity is decided here, raising happens only when a ring instance uses it
+  ExpandParams ex{};
+  ex.tree_threshold = cfg->tree_threshold;
+  ex.ring_len = cfg->ring_len > 0 ? cfg->ring_len : -1;
+  ex.ring_valid = 1;
+  if (cfg->ring_len > 0) {
+    const int L = cfg->ring_len;
+    std::vector<uint16_t> h(2 * (size_t)L, 0);
+    std::vector<int> seen(L, 0);
+    for (int k = 0; k < L; k++) {
+      uint16_t v = cfg->ring_order[k];
+      h[k] = v;
+      if (v >= L || seen[v]) ex.ring_valid = 0;
+      else { seen[v] = 1; h[L + v] = (uint16_t)k; }
+    }
+    size_t cap = (size_t)c->ring_cap;
+    if (ensure(c, c->ring, cap, 2 * (size_t)L)) return CT_ERR_CUDA;
+    c->ring_cap = (int)cap;
+    CTX_TRY(c, cudaMemcpyAsync(c->ring, h.data(), 2 * (size_t)L * 2, cudaMemcpyHostToDevice, st));
+    ex.ring_order = c->ring;
+    ex.ring_inv = c->ring + L;
+  }
+
+  const bool explicit_d = cfg->d >= 0;
+  c->last_explicit = explicit_d;
+  if (explicit_d && cfg->d > 65536) return fail(c, CT_ERR_ARGUMENT, "d exceeds the 16-bit device range");
+  int gcap = explicit_d ? (int)cfg->d : (cfg->dev_hint > 0 ? cfg->dev_hint : 16);
+
+  RunOut ro{};
+  uint32_t launches = 0;
+  int path = 1;
+  int max_dev = -1;
+  const ct_record* arr = d_recs;
+  uint64_t arr_n = n;
+  ExactResult ex_res;
+  bool ran_exact = false;
+  auto do_exact = [&]() -> int {
+    int e = exact_canonicalize(d_recs, n, n_comms, st, false, &ex_res);
+    if (e) return cuda_fail(c, (cudaError_t)e, "exact path");
+    launches += ex_res.launches;
+    ran_exact = true;
+    path = 2;
+    return 0;
+  };
+
+  if (cfg->force_path == 2) {
+    if (int e = do_exact()) return e;
+  } else {
+    if (int e = run_fast(c, d_recs, n, gcap, explicit_d, ex, n_comms, st, &ro)) return e;
+    launches += ro.launches;
+    max_dev = ro.gs.max_dev;
+    if (ro.gs.flags & F_NONCANON) {
+      if (cfg->force_path == 1) return fail(c, CT_ERR_NOT_CANONICAL, "trace is not in the canonical layout");
+      if (int e = do_exact()) return e;
+    }
+  }
+  if (ran_exact) {
+    if (ex_res.fatal) {
+      out->status = ex_res.fatal;
+      out->path = 2;
+      out->err_index = ex_res.err_index;
+      memcpy(out->err_aux, ex_res.err_aux, sizeof out->err_aux);
+      out->err_aux[3] = (uint64_t)ex_res.fatal_kind;
+      if (ex_res.canon) cudaFreeAsync(ex_res.canon, st);
+      c->last = *out;
+      return out->status;
+    }
+    if (max_dev < 0 && n) {  // the fast pass did not run: infer d over all records
+      int* d_m;
+      CTX_TRY(c, cudaMallocAsync(&d_m, 4, st));
+      int init = -1;
+      CTX_TRY(c, cudaMemcpyAsync(d_m, &init, 4, cudaMemcpyHostToDevice, st));
+      k_max_dev<<<std::min<uint64_t>((n + 255) / 256, 4096), 256, 0, st>>>(d_recs, n, d_m);
+      CTX_TRY(c, cudaMemcpyAsync(&max_dev, d_m, 4, cudaMemcpyDeviceToHost, st));
+      CTX_TRY(c, cudaStreamSynchronize(st));
+      cudaFreeAsync(d_m, st);
+      launches++;
+    }
+    arr = ex_res.canon;
+    arr_n = ex_res.m;
+    c->canon_keep = ex_res.canon;
+    c->canon_n = ex_res.m;
+    if (int e = run_fast(c, arr, arr_n, gcap, explicit_d, ex, n_comms, st, &ro)) return e;
+    launches += ro.launches;
+    if (ro.gs.flags & F_NONCANON) return fail(c, CT_ERR_CUDA, "internal: canonical stream rejected");
+  }
+  const int64_t d = explicit_d ? cfg->d : (int64_t)max_dev + 1;
+  if (!explicit_d && d > gcap) {
+    // histogram too small for the inferred device count: rerun with the exact size
+    gcap = (int)d;
+    if (int e = run_fast(c, arr, arr_n, gcap, false, ex, n_comms, st, &ro)) return e;
+    launches += ro.launches;
+  }
+  {
+    const uint64_t extra[3] = {ran_exact ? ex_res.n_incomplete : 0, ran_exact ? ex_res.n_unmatched_send : 0,
+                               ran_exact ? ex_res.n_unmatched_recv : 0};
+    if (int e = summarize_state(c, ro.gs, gcap, d, path, extra, arr, n_comms, st, out)) return e;
+  }
+  CTX_TRY(c, cudaEventRecord(c->ev[3], st));
+  CTX_TRY(c, cudaEventSynchronize(c->ev[3]));
+  CTX_TRY(c, cudaEventElapsedTime(&out->ms_total, c->ev[2], c->ev[3]));
+  out->ms_kernel = ro.ms_kernel;
+  out->n_launches = launches;
+  c->last = *out;
+  return out->status;
+}
+
+int ct_result_cells(ct_context* c, uint64_t* bytes, uint64_t* freq, uint64_t n_cells) {
+  if (!c || !bytes || !freq) return fail(c, CT_ERR_ARGUMENT, "null argument");
+  const size_t ncell = (size_t)kTypes * c->last_g2 * c->last_g2;
+  if (n_cells < ncell) return fail(c, CT_ERR_ARGUMENT, "cell buffer too small");
+  CTX_TRY(c, cudaMemcpyAsync(bytes, c->cells, ncell * 8, cudaMemcpyDeviceToHost, c->stream));
+  CTX_TRY(c, cudaMemcpyAsync(freq, c->cells + ncell, ncell * 8, cudaMemcpyDeviceToHost, c->stream));
+  CTX_TRY(c, cudaStreamSynchronize(c->stream));
+  return CT_OK;
+}
+
+static int ensure_materialized(ct_context* c) {
+  if (c->mat_valid) return 0;
+  c->mat = ExactResult();
+  int e = exact_canonicalize(c->last_input, c->last_n, c->last_comms, c->stream, true, &c->mat);
+  if (e) return cuda_fail(c, (cudaError_t)e, "materialize");
+  if (c->mat.canon) cudaFreeAsync(c->mat.canon, c->stream);
+  c->mat.canon = nullptr;
+  cudaStreamSynchronize(c->stream);
+  c->mat_valid = true;
+  return 0;
+}
+
+int ct_materialize(ct_context* c, const ct_record* recs, uint64_t n, int on_device, int32_t n_comms,
+                   ct_summary* out) {
+  if (!c || !out || (n && !recs)) return fail(c, CT_ERR_ARGUMENT, "null argument");
+  memset(out, 0, sizeof *out);
+  CTX_TRY(c, cudaSetDevice(c->device));
+  const ct_record* d_recs = recs;
+  if (!on_device && n) {
+    size_t cap = c->in_cap;
+    if (ensure(c, c->in_buf, cap, n)) return CT_ERR_CUDA;
+    c->in_cap = cap;
+    CTX_TRY(c, cudaMemcpyAsync(c->in_buf, recs, n * sizeof(ct_record), cudaMemcpyHostToDevice, c->stream));
+    d_recs = c->in_buf;
+  }
+  c->last_input = d_recs;
+  c->last_n = n;
+  c->last_comms = (uint32_t)std::max(n_comms, 1);
+  c->mat_valid = false;
+  if (int e = ensure_materialized(c)) return e;
+  if (c->mat.fatal) {
+    out->status = c->mat.fatal;
+    out->path = 2;
+    out->err_index = c->mat.err_index;
+    memcpy(out->err_aux, c->mat.err_aux, sizeof out->err_aux);
+    out->err_aux[3] = (uint64_t)c->mat.fatal_kind;
+    c->mat_valid = false;
+    return out->status;
+  }
+  return CT_OK;
+}
+
+int ct_infer_device_count(ct_context* c, const ct_record* recs, uint64_t n, int on_device, int64_t* d) {
+  if (!c || !d || (n && !recs)) return fail(c, CT_ERR_ARGUMENT, "null argument");
+  CTX_TRY(c, cudaSetDevice(c->device));
+  cudaStream_t st = c->stream;
+  const ct_record* d_recs = recs;
+  if (!on_device && n) {
+    size_t cap = c->in_cap;
+    if (ensure(c, c->in_buf, cap, n)) return CT_ERR_CUDA;
+    c->in_cap = cap;
+    CTX_TRY(c, cudaMemcpyAsync(c->in_buf, recs, n * sizeof(ct_record), cudaMemcpyHostToDevice, st));
+    d_recs = c->in_buf;
+  }
+  int* d_m;
+  int m = -1;
+  CTX_TRY(c, cudaMallocAsync(&d_m, 4, st));
+  CTX_TRY(c, cudaMemcpyAsync(d_m, &m, 4, cudaMemcpyHostToDevice, st));
+  if (n) k_max_dev<<<(unsigned)std::min<uint64_t>((n + 255) / 256, 4096), 256, 0, st>>>(d_recs, n, d_m);
+  CTX_TRY(c, cudaMemcpyAsync(&m, d_m, 4, cudaMemcpyDeviceToHost, st));
+  CTX_TRY(c, cudaStreamSynchronize(st));
+  cudaFreeAsync(d_m, st);
+  *d = (int64_t)m + 1;
+  return CT_OK;
+}
+
+int ct_result_groups(ct_context* c, uint64_t* rows, uint64_t row_cap, uint64_t* members,
+                     uint64_t member_cap, uint64_t* n_rows, uint64_t* n_members) {
+  if (!c || !n_rows || !n_members) return fail(c, CT_ERR_ARGUMENT, "null argument");
+  if (int e = ensure_materialized(c)) return e;
+  *n_rows = c->mat.groups.size();
+  *n_members = c->mat.members.size();
+  if (rows && row_cap >= *n_rows)
+    for (size_t k = 0; k < c->mat.groups.size(); k++) {
+      const GroupRow& g = c->mat.groups[k];
+      uint64_t* o = rows + 5 * k;
+      o[0] = g.comm; o[1] = g.ordinal; o[2] = g.status; o[3] = g.n_members; o[4] = g.member_off;
+    }
+  if (members && member_cap >= *n_members)
+    std::copy(c->mat.members.begin(), c->mat.members.end(), members);
+  return CT_OK;
+}
+
+int ct_result_p2p_diags(ct_context* c, uint64_t* rows, uint64_t row_cap, uint64_t* n_rows) {
+  if (!c || !n_rows) return fail(c, CT_ERR_ARGUMENT, "null argument");
+  if (int e = ensure_materialized(c)) return e;
+  *n_rows = c->mat.p2p_diags.size();
+  if (rows && row_cap >= *n_rows)
+    for (size_t k = 0; k < c->mat.p2p_diags.size(); k++) {
+      const P2PDiagRow& g = c->mat.p2p_diags[k];
+      uint64_t* o = rows + 7 * k;
+      o[0] = g.reason; o[1] = g.comm; o[2] = g.src; o[3] = g.dst; o[4] = g.k; o[5] = g.send_idx; o[6] = g.recv_idx;
+    }
+  return CT_OK;
+}
+
+int ct_emit_transfers(ct_context* c, const ct_record* recs, uint64_t n, int on_device, const ct_config* cfg,
+                      int64_t* rows, uint64_t row_cap, uint64_t* n_rows) {
+  if (!c || !cfg || !n_rows || (n && !recs)) return fail(c, CT_ERR_ARGUMENT, "null argument");
+  CTX_TRY(c, cudaSetDevice(c->device));
+  cudaStream_t st = c->stream;
+  const ct_record* d_recs = recs;
+  if (!on_device && n) {
+    size_t cap = c->in_cap;
+    if (ensure(c, c->in_buf, cap, n)) return CT_ERR_CUDA;
+    c->in_cap = cap;
+    CTX_TRY(c, cudaMemcpyAsync(c->in_buf, recs, n * sizeof(ct_record), cudaMemcpyHostToDevice, st));
+    d_recs = c->in_buf;
+  }
+  ExpandParams ex{};
+  ex.tree_threshold = cfg->tree_threshold;
+  ex.ring_len = cfg->ring_len > 0 ? cfg->ring_len : -1;
+  ex.ring_valid = 1;
+  if (cfg->ring_len > 0) {
+    const int L = cfg->ring_len;
+    std::vector<uint16_t> h(2 * (size_t)L, 0);
+    std::vector<int> seen(L, 0);
+    for (int k = 0; k < L; k++) {
+      uint16_t v = cfg->ring_order[k];
+      h[k] = v;
+      if (v >= L || seen[v]) ex.ring_valid = 0;
+      else { seen[v] = 1; h[L + v] = (uint16_t)k; }
+    }
+    size_t cap = (size_t)c->ring_cap;
+    if (ensure(c, c->ring, cap, 2 * (size_t)L)) return CT_ERR_CUDA;
+    c->ring_cap = (int)cap;
+    CTX_TRY(c, cudaMemcpyAsync(c->ring, h.data(), 2 * (size_t)L * 2, cudaMemcpyHostToDevice, st));
+    ex.ring_order = c->ring;
+    ex.ring_inv = c->ring + L;
+  }
+  uint32_t* counts;
+  uint64_t* offs;
+  unsigned int* flags;
+  CTX_TRY(c, cudaMallocAsync(&counts, (n + 1) * 4, st));
+  CTX_TRY(c, cudaMallocAsync(&offs, (n + 1) * 8, st));
+  CTX_TRY(c, cudaMallocAsync(&flags, 4, st));
+  CTX_TRY(c, cudaMemsetAsync(flags, 0, 4, st));
+  CTX_TRY(c, cudaMemsetAsync(counts + n, 0, 4, st));
+  launch_emit(d_recs, n, ex, counts, nullptr, nullptr, 0, flags, st);
+  size_t tmp = 0;
+  void* t = nullptr;
+  CTX_TRY(c, cub::DeviceScan::ExclusiveSum(nullptr, tmp, counts, offs, (int64_t)(n + 1), st));
+  CTX_TRY(c, cudaMallocAsync(&t, tmp, st));
+  CTX_TRY(c, cub::DeviceScan::ExclusiveSum(t, tmp, counts, offs, (int64_t)(n + 1), st));
+  uint64_t total = 0;
+  unsigned int hflags = 0;
+  CTX_TRY(c, cudaMemcpyAsync(&total, offs + n, 8, cudaMemcpyDeviceToHost, st));
+  CTX_TRY(c, cudaMemcpyAsync(&hflags, flags, 4, cudaMemcpyDeviceToHost, st));
+  CTX_TRY(c, cudaStreamSynchronize(st));
+  *n_rows = total;
+  int status = CT_OK;
+  if (hflags & F_BAD_RING) status = CT_ERR_INVALID_CONFIG;
+  else if (hflags & F_WRONG_ALGO) status = CT_ERR_WRONG_ALGORITHM;
+  else if (hflags & F_MISSING_ROOT) status = CT_ERR_MISSING_ROOT;
+  if (status == CT_OK && rows && row_cap >= total && total) {
+    int64_t* d_rows;
+    CTX_TRY(c, cudaMallocAsync(&d_rows, total * 7 * 8, st));
+    launch_emit(d_recs, n, ex, counts, offs, d_rows, 1, flags, st);
+    CTX_TRY(c, cudaMemcpyAsync(rows, d_rows, total * 7 * 8, cudaMemcpyDeviceToHost, st));
+    CTX_TRY(c, cudaStreamSynchronize(st));
+    cudaFreeAsync(d_rows, st);
+  }
+  cudaFreeAsync(t, st);
+  cudaFreeAsync(counts, st);
+  cudaFreeAsync(offs, st);
+  cudaFreeAsync(flags, st);
+  CTX_TRY(c, cudaStreamSynchronize(st));
+  return status;
+}
+
+int ct_generate(ct_context* c, int kind, uint64_t seed, uint64_t first, uint64_t n, ct_record* dev_out,
+                void* stream) {
+  if (!c || (n && !dev_out)) return fail(c, CT_ERR_ARGUMENT, "null argument");
+  CTX_TRY(c, cudaSetDevice(c->device));
+  cudaStream_t st = stream ? (cudaStream_t)stream : c->stream;
+  int e = generate(kind, seed, first, n, dev_out, st);
+  if (e) return fail(c, CT_ERR_ARGUMENT, "unknown generator kind");
+  CTX_TRY(c, cudaGetLastError());
+  CTX_TRY(c, cudaStreamSynchronize(st));
+  return CT_OK;
+}
+
+uint64_t ct_generate_boundary(int kind, uint64_t at) { return generate_boundary(kind, at); }
+
+}  // extern "C"
+
+// ------------------------------------------------------------------ multi-GPU partials
+// Layout (uint64 words): header[16] | calls[9] pay_lo[9] pay_hi[9] diag[6] |
+// tcf[6 * n_comms] | cells[ncell] | freq[ncell] | kChainExport slots of chain-boundary
+// records.  Header: magic, g2, n_comms, n, flags, max_dev + 1, oor_key, oor_gpu,
+// copy_first[3], path, d_explicit + 1, 3 reserved.
+namespace {
+constexpr uint64_t kPartialMagic = 0x4354503250415254ull;
+constexpr int kChainExport = 16;
+constexpr int kExportN = 64;  // largest communicator whose boundary blocks are exported
+constexpr uint64_t kSlotWords = 5 + 2 * (uint64_t)kExportN * 4;
+constexpr uint64_t kHdr = 16, kStats = 33;
+
+uint64_t partial_words(int g2, uint32_t n_comms) {
+  return kHdr + kStats + 6ull * n_comms + 2ull * kTypes * g2 * g2 + kChainExport * kSlotWords;
+}
+
+__global__ void k_merge_partials(const uint64_t* parts, int world, uint64_t words, int g2, uint32_t n_comms,
+                                 unsigned long long* cells, unsigned long long* tcf, GlobalState* gs) {
+  const uint64_t ncell = (uint64_t)kTypes * g2 * g2;
+  const uint64_t o_tcf = kHdr + kStats, o_cells = o_tcf + 6ull * n_comms;
+  const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t j = tid; j < 2 * ncell; j += stride) {
+    unsigned __int128 s = 0;
+    for (int w = 0; w < world; w++) s += parts[w * words + o_cells + j];
+    if (s >> 64) { atomicOr(&gs->flags, F_OVERFLOW); s = ~0ull; }
+    cells[j] = (unsigned long long)s;
+  }
+  for (uint64_t j = tid; j < 6ull * n_comms; j += stride) {
+    uint64_t best = ~0ull, base = 0;
+    for (int w = 0; w < world; w++) {
+      const uint64_t v = parts[w * words + o_tcf + j];
+      if (v != ~0ull && v + base < best) best = v + base;
+      base += parts[w * words + 3];
+    }
+    tcf[j] = best;
+  }
+  if (tid == 0) {
+    GlobalState g{};
+    g.max_dev = -1;
+    g.oor_key = ~0ull;
+    g.of_cell = ~0ull;
+    for (int k = 0; k < 3; k++) g.copy_first[k] = ~0ull;
+    uint64_t base = 0;
+    for (int w = 0; w < world; w++) {
+      const uint64_t* p = parts + w * words;
+      g.flags |= (uint32_t)p[4];
+      if (p[11] != 1) g.flags |= F_NONCANON;  // shards must have taken the fast path
+      g.max_dev = max(g.max_dev, (int)p[5] - 1);
+      if (p[6] != ~0ull) {
+        const uint64_t k = p[6] + (base << 21);
+        if (k < g.oor_key) { g.oor_key = k; g.err_index = p[7]; }
+      }
+      for (int k = 0; k < 3; k++)
+        if (p[8 + k] != ~0ull && p[8 + k] + base < g.copy_first[k]) g.copy_first[k] = p[8 + k] + base;
+      for (int t = 0; t < kTypes; t++) {
+        g.calls[t] += p[kHdr + t];
+        const unsigned long long lo = p[kHdr + 9 + t];
+        const unsigned long long old = g.pay_lo[t];
+        g.pay_lo[t] = old + lo;
+        g.pay_hi[t] += p[kHdr + 18 + t] + (g.pay_lo[t] < old ? 1 : 0);
+      }
+      for (int k = 0; k < CT_NDIAG; k++) g.diag[k] += p[kHdr + 27 + k];
+      base += p[3];
+    }
+    // shard-boundary chains: the last element of a chain in shard w must precede its
+    // first element in the next shard holding it (grouping.py:118, decompose.py:359-360)
+    const uint64_t o_chain = kHdr + kStats + 6ull * n_comms + 2 * ncell;
+    for (int w = 0; w < world; w++) {
+      const uint64_t* pw = parts + w * words + o_chain;
+      for (int s = 0; s < kChainExport; s++) {
+        const uint64_t* a = pw + s * kSlotWords;
+        if (a[1] == ~0ull) continue;
+        bool found = false;
+        for (int v = w + 1; v < world && !found; v++) {
+          const uint64_t* pv = parts + v * words + o_chain;
+          for (int t = 0; t < kChainExport; t++) {
+            const uint64_t* b = pv + t * kSlotWords;
+            if (b[1] == ~0ull || b[0] != a[0] || b[1] != a[1]) continue;
+            found = true;
+            // a: last element records at offset 5 + kExportN*4; b: first element at offset 5
+            const ct_record* ra = reinterpret_cast<const ct_record*>(a + 5 + kExportN * 4);
+            const ct_record* rb = reinterpret_cast<const ct_record*>(b + 5);
+            bool ok;
+            if (a[1] == 0) {
+              ok = ra[0].nranks == rb[0].nranks;
+              for (uint32_t r = 0; ok && r < rb[0].nranks; r++) ok = ra[r].seq < rb[r].seq;
+            } else {
+              ok = ra[0].seq <= rb[0].seq && ra[1].seq <= rb[1].seq;
+            }
+            if (!ok) g.flags |= F_NONCANON;
+            break;
+          }
+        }
+      }
+    }
+    *gs = g;
+  }
+}
+}  // namespace
+
+extern "C" {
+
+int ct_partial_size(ct_context* c, uint64_t* words) {
+  if (!c || !words) return fail(c, CT_ERR_ARGUMENT, "null argument");
+  *words = partial_words(c->last_g2, c->last_comms);
+  return CT_OK;
+}
+
+int ct_partial_export(ct_context* c, uint64_t* dev_out, uint64_t words, void* stream) {
+  if (!c || !dev_out) return fail(c, CT_ERR_ARGUMENT, "null argument");
+  const int g2 = c->last_g2;
+  const uint32_t nc = c->last_comms;
+  if (words != partial_words(g2, nc)) return fail(c, CT_ERR_ARGUMENT, "partial size mismatch");
+  CTX_TRY(c, cudaSetDevice(c->device));
+  cudaStream_t st = stream ? (cudaStream_t)stream : c->stream;
+  const GlobalState& gs = c->last_state;
+  const uint64_t ncell = (uint64_t)kTypes * g2 * g2;
+  std::vector<uint64_t> hdr(kHdr + kStats, 0);
+  hdr[0] = kPartialMagic;
+  hdr[1] = (uint64_t)g2;
+  hdr[2] = nc;
+  hdr[3] = c->last_n;
+  hdr[4] = gs.flags;
+  hdr[5] = (uint64_t)(gs.max_dev + 1);
+  hdr[6] = gs.oor_key;
+  hdr[7] = (c->last.status == CT_ERR_ENDPOINT_RANGE) ? c->last.err_aux[0] : 0;
+  for (int k = 0; k < 3; k++) hdr[8 + k] = gs.copy_first[k];
+  hdr[11] = (uint64_t)c->last.path;
+  hdr[12] = 0;
+  for (int t = 0; t < kTypes; t++) {
+    hdr[kHdr + t] = gs.calls[t];
+    hdr[kHdr + 9 + t] = gs.pay_lo[t];
+    hdr[kHdr + 18 + t] = gs.pay_hi[t];
+  }
+  for (int k = 0; k < CT_NDIAG; k++) hdr[kHdr + 27 + k] = c->last.diag[k];
+  // chain boundary elements: per key, the first element and the last element of this shard
+  const uint32_t E = std::min(gs.n_chain, c->chain_cap);
+  std::vector<ChainEntry> ch(E);
+  if (E) {
+    CTX_TRY(c, cudaMemcpyAsync(ch.data(), c->chain, E * sizeof(ChainEntry), cudaMemcpyDeviceToHost, st));
+    CTX_TRY(c, cudaStreamSynchronize(st));
+  }
+  std::vector<std::pair<uint64_t, std::pair<uint64_t, uint64_t>>> keys;  // key -> (min first, max last)
+  for (const ChainEntry& e : ch) {
+    bool hit = false;
+    for (auto& k : keys)
+      if (k.first == e.key) {
+        k.second.first = std::min(k.second.first, e.first);
+        k.second.second = std::max(k.second.second, e.last);
+        hit = true;
+      }
+    if (!hit) keys.push_back({e.key, {e.first, e.last}});
+  }
+  if (keys.size() > (size_t)kChainExport) hdr[4] |= F_CHAIN_CAP | F_NONCANON;
+  CTX_TRY(c, cudaMemcpyAsync(dev_out, hdr.data(), hdr.size() * 8, cudaMemcpyHostToDevice, st));
+  const uint64_t o_tcf = kHdr + kStats, o_cells = o_tcf + 6ull * nc, o_chain = o_cells + 2 * ncell;
+  CTX_TRY(c, cudaMemcpyAsync(dev_out + o_tcf, c->tcf, 6ull * nc * 8, cudaMemcpyDeviceToDevice, st));
+  CTX_TRY(c, cudaMemcpyAsync(dev_out + o_cells, c->cells, 2 * ncell * 8, cudaMemcpyDeviceToDevice, st));
+  std::vector<uint64_t> slots(kChainExport * kSlotWords, 0);
+  for (int s = 0; s < kChainExport; s++) slots[s * kSlotWords + 1] = ~0ull;
+  for (size_t s = 0; s < keys.size() && s < (size_t)kChainExport; s++) {
+    uint64_t* o = slots.data() + s * kSlotWords;
+    const bool p2p = (keys[s].first >> 63) != 0;
+    o[0] = keys[s].first;
+    o[1] = p2p ? 1 : 0;
+    o[3] = keys[s].second.first;
+    o[4] = keys[s].second.second;
+  }
+  CTX_TRY(c, cudaMemcpyAsync(dev_out + o_chain, slots.data(), slots.size() * 8, cudaMemcpyHostToDevice, st));
+  for (size_t s = 0; s < keys.size() && s < (size_t)kChainExport; s++) {
+    const bool p2p = (keys[s].first >> 63) != 0;
+    ct_record head{};
+    if (host_dev_of(c, c->last_input, keys[s].second.first, st, &head)) return CT_ERR_CUDA;
+    const uint64_t m = p2p ? 2 : head.nranks;
+    if (m > (uint64_t)kExportN) {
+      hdr[4] |= F_CHAIN_CAP | F_NONCANON;
+      CTX_TRY(c, cudaMemcpyAsync(dev_out + 4, &hdr[4], 8, cudaMemcpyHostToDevice, st));
+      continue;
+    }
+    uint64_t* o = dev_out + o_chain + s * kSlotWords;
+    CTX_TRY(c, cudaMemcpyAsync(o + 5, c->last_input + keys[s].second.first, m * sizeof(ct_record),
+                               cudaMemcpyDeviceToDevice, st));
+    CTX_TRY(c, cudaMemcpyAsync(o + 5 + kExportN * 4, c->last_input + keys[s].second.second,
+                               m * sizeof(ct_record), cudaMemcpyDeviceToDevice, st));
+  }
+  CTX_TRY(c, cudaStreamSynchronize(st));
+  return CT_OK;
+}
+
+int ct_partial_merge(ct_context* c, const uint64_t* dev_in, int world, uint64_t words, ct_summary* out,
+                     void* stream) {
+  if (!c || !dev_in || !out || world < 1) return fail(c, CT_ERR_ARGUMENT, "bad argument");
+  CTX_TRY(c, cudaSetDevice(c->device));
+  cudaStream_t st = stream ? (cudaStream_t)stream : c->stream;
+  uint64_t h0[3];
+  CTX_TRY(c, cudaMemcpyAsync(h0, dev_in, 24, cudaMemcpyDeviceToHost, st));
+  CTX_TRY(c, cudaStreamSynchronize(st));
+  if (h0[0] != kPartialMagic) return fail(c, CT_ERR_ARGUMENT, "not a ct partial");
+  const int g2 = (int)h0[1];
+  const uint32_t nc = (uint32_t)h0[2];
+  if (words != partial_words(g2, nc)) return fail(c, CT_ERR_ARGUMENT, "partial size mismatch");
+  for (int w = 1; w < world; w++) {
+    uint64_t hw[3];
+    CTX_TRY(c, cudaMemcpyAsync(hw, dev_in + w * words, 24, cudaMemcpyDeviceToHost, st));
+    CTX_TRY(c, cudaStreamSynchronize(st));
+    if (hw[0] != kPartialMagic || hw[1] != h0[1] || hw[2] != h0[2])
+      return fail(c, CT_ERR_ARGUMENT, "partials disagree on layout (use the same d / dev_hint on every rank)");
+  }
+  const uint64_t ncell = (uint64_t)kTypes * g2 * g2;
+  size_t cap = c->cells_cap;
+  if (ensure(c, c->cells, cap, 2 * ncell)) return CT_ERR_CUDA;
+  c->cells_cap = cap;
+  cap = c->tcf_cap;
+  if (ensure(c, c->tcf, cap, 6ull * nc)) return CT_ERR_CUDA;
+  c->tcf_cap = cap;
+  memset(out, 0, sizeof *out);
+  CTX_TRY(c, cudaEventRecord(c->ev[2], st));
+  k_merge_partials<<<64, 256, 0, st>>>(dev_in, world, words, g2, nc, c->cells, c->tcf, c->st);
+  CTX_TRY(c, cudaGetLastError());
+  GlobalState gs;
+  CTX_TRY(c, cudaMemcpyAsync(&gs, c->st, sizeof gs, cudaMemcpyDeviceToHost, st));
+  uint64_t dexp = 0;
+  CTX_TRY(c, cudaMemcpyAsync(&dexp, dev_in + 12, 8, cudaMemcpyDeviceToHost, st));
+  CTX_TRY(c, cudaStreamSynchronize(st));
+  if (gs.flags & F_NONCANON)
+    return fail(c, CT_ERR_NOT_CANONICAL, "sharded analysis needs the canonical layout in every shard");
+  uint64_t n = 0;
+  for (int w = 0; w < world; w++) {
+    uint64_t nw;
+    CTX_TRY(c, cudaMemcpyAsync(&nw, dev_in + w * words + 3, 8, cudaMemcpyDeviceToHost, st));
+    CTX_TRY(c, cudaStreamSynchronize(st));
+    n += nw;
+  }
+  const int gcap = g2 - 2;
+  const int64_t d = c->last.d >= 0 && (c->last.status == CT_OK || c->last.status == CT_ERR_ENDPOINT_RANGE) &&
+                            c->last_explicit ? c->last.d : (int64_t)gs.max_dev + 1;
+  const uint64_t extra[3] = {0, 0, 0};
+  if (int e = summarize_state(c, gs, gcap, d, 1, extra, nullptr, nc, st, out)) return e;
+  out->n_records = n;
+  CTX_TRY(c, cudaEventRecord(c->ev[3], st));
+  CTX_TRY(c, cudaEventSynchronize(c->ev[3]));
+  CTX_TRY(c, cudaEventElapsedTime(&out->ms_total, c->ev[2], c->ev[3]));
+  out->n_launches = 1;
+  c->last = *out;
+  return out->status;
+}
+
+}  // extern "C"
