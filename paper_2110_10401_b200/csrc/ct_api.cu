@@ -18,10 +18,8 @@
 
 namespace ct {
 __global__ void fast_kernel(FastParams P);
-__global__ void chain_sort_check_kernel(const ct_record* recs, uint64_t n, const ChainEntry* chain,
-                                        GlobalState* st);
-__global__ void chain_check_kernel(const ct_record* recs, uint64_t n, const ChainEntry* chain,
-                                   const uint32_t* order, uint32_t count, GlobalState* st);
+__global__ void range_check_kernel(const ct_record* recs, const WarpSlot* slots, const P2PEntry* chans,
+                                   uint32_t total_warps, GlobalState* st);
 int generate(int kind, uint64_t seed, uint64_t first, uint64_t n, ct_record* out, cudaStream_t st);
 uint64_t generate_boundary(int kind, uint64_t at);
 void launch_emit(const ct_record* recs, uint64_t n, const ExpandParams& ex, uint32_t* counts,
@@ -42,8 +40,11 @@ struct ct_context {
   size_t cells_cap = 0;                 // entries per array
   unsigned long long* tcf = nullptr;    // [5][n_comms] type_comm_first, then [n_comms] comm_first
   size_t tcf_cap = 0;
-  ChainEntry* chain = nullptr;
-  uint32_t chain_cap = 0;
+  WarpSlot* slots = nullptr;   // per (warp range, comm slot) order summaries
+  size_t slots_cap = 0;
+  P2PEntry* chans = nullptr;   // per (warp range, p2p channel) order summaries
+  size_t chans_cap = 0;
+  uint32_t last_total_warps = 0;
   uint16_t* ring = nullptr;  // order then inverse
   int ring_cap = 0;
   cudaEvent_t ev[4];
@@ -96,7 +97,7 @@ struct RunOut {
   uint32_t launches;
 };
 
-// One pass of the fast kernel (+ cross-CTA chain check) over ``recs``.
+// One pass of the fast kernel + the cross-range order check over ``recs``.
 int run_fast(ct_context* c, const ct_record* recs, uint64_t n, int gcap, bool explicit_d,
              const ExpandParams& ex, uint32_t n_comms, cudaStream_t st, RunOut* out) {
   const int g2 = gcap + 2;
@@ -104,19 +105,19 @@ int run_fast(ct_context* c, const ct_record* recs, uint64_t n, int gcap, bool ex
   if (ensure(c, c->cells, c->cells_cap, 2 * ncell)) return CT_ERR_CUDA;
   size_t tcf_need = 6 * (size_t)std::max<uint32_t>(n_comms, 1);
   if (ensure(c, c->tcf, c->tcf_cap, tcf_need)) return CT_ERR_CUDA;
-  const uint64_t n_subs = (n + kSub - 1) / kSub;
-  uint32_t grid = (uint32_t)std::min<uint64_t>(n_subs, (uint64_t)c->num_sms);
+  const uint64_t n_chunks = (n + 31) / 32;
+  // one CTA (16 warps) per SM; small traces use fewer CTAs (>= 4 chunks per warp)
+  uint32_t grid = (uint32_t)std::min<uint64_t>((uint64_t)c->num_sms, (n_chunks + 4 * kWarps - 1) / (4 * kWarps));
   if (grid == 0) grid = 1;
-  uint32_t per = (uint32_t)((n_subs + grid - 1) / grid);
-  if (per == 0) per = 1;
-  grid = (uint32_t)((n_subs + per - 1) / per);
-  if (grid == 0) grid = 1;
-  // chain list capacity: every warp table of every CTA could be full
-  size_t cc = c->chain_cap;
-  if (ensure(c, c->chain, cc, (size_t)grid * kWarps * kChainW)) return CT_ERR_CUDA;
-  c->chain_cap = (uint32_t)cc;
+  const uint32_t total_warps = grid * kWarps;
+  size_t sc = c->slots_cap;
+  if (ensure(c, c->slots, sc, (size_t)total_warps * kCS)) return CT_ERR_CUDA;
+  c->slots_cap = sc;
+  size_t pc = c->chans_cap;
+  if (ensure(c, c->chans, pc, (size_t)total_warps * kPC)) return CT_ERR_CUDA;
+  c->chans_cap = pc;
+  c->last_total_warps = total_warps;
 
-  CTX_TRY(c, cudaMemsetAsync(c->st, 0, sizeof(GlobalState), st));
   CTX_TRY(c, cudaMemsetAsync(c->cells, 0, 2 * ncell * sizeof(unsigned long long), st));
   CTX_TRY(c, cudaMemsetAsync(c->tcf, 0xFF, tcf_need * sizeof(unsigned long long), st));
   {
@@ -130,7 +131,6 @@ int run_fast(ct_context* c, const ct_record* recs, uint64_t n, int gcap, bool ex
   FastParams P{};
   P.recs = recs;
   P.n = n;
-  P.base = 0;
   P.gcap = gcap;
   P.g2 = g2;
   P.explicit_d = explicit_d;
@@ -144,10 +144,10 @@ int run_fast(ct_context* c, const ct_record* recs, uint64_t n, int gcap, bool ex
   P.freq = c->cells + ncell;
   P.type_comm_first = c->tcf;
   P.comm_first = c->tcf + 5 * (size_t)std::max<uint32_t>(n_comms, 1);
-  P.chain = c->chain;
-  P.chain_cap = c->chain_cap;
-  P.subs_per_cta = per;
-  P.n_subs = (uint32_t)n_subs;
+  P.slots = c->slots;
+  P.chans = c->chans;
+  P.total_warps = total_warps;
+  P.n_chunks = n_chunks;
   uint32_t launches = 0;  // kernels launched (cudaMemset/Memcpy are copy-engine work)
   out->ms_kernel = 0;
   if (n) {
@@ -156,55 +156,15 @@ int run_fast(ct_context* c, const ct_record* recs, uint64_t n, int gcap, bool ex
     fast_kernel<<<grid, kThreads, smem, st>>>(P);
     CTX_TRY(c, cudaGetLastError());
     CTX_TRY(c, cudaEventRecord(c->ev[1], st));
-    const int csm = (int)(kChainSortMax * (8 + 8 + 4));
-    CTX_TRY(c, cudaFuncSetAttribute(chain_sort_check_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, csm));
-    chain_sort_check_kernel<<<1, 1024, csm, st>>>(recs, n, c->chain, c->st);
+    const uint64_t threads = (uint64_t)total_warps * (kCS + kPC);
+    range_check_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(recs, c->slots, c->chans, total_warps,
+                                                                          c->st);
     CTX_TRY(c, cudaGetLastError());
     launches += 2;
   }
   CTX_TRY(c, cudaMemcpyAsync(&out->gs, c->st, sizeof(GlobalState), cudaMemcpyDeviceToHost, st));
   CTX_TRY(c, cudaStreamSynchronize(st));
   if (n) CTX_TRY(c, cudaEventElapsedTime(&out->ms_kernel, c->ev[0], c->ev[1]));
-  const uint32_t E = std::min(out->gs.n_chain, c->chain_cap);
-  if (E > 1 && (out->gs.flags & F_CHAIN_BIG) && !(out->gs.flags & F_NONCANON)) {
-    // order entries by (key, first) with two stable radix passes, then check neighbours
-    uint64_t *k1, *k2;
-    uint32_t *v1, *v2;
-    CTX_TRY(c, cudaMallocAsync(&k1, E * 8, st));
-    CTX_TRY(c, cudaMallocAsync(&k2, E * 8, st));
-    CTX_TRY(c, cudaMallocAsync(&v1, E * 4, st));
-    CTX_TRY(c, cudaMallocAsync(&v2, E * 4, st));
-    std::vector<ChainEntry> h(E);
-    CTX_TRY(c, cudaMemcpyAsync(h.data(), c->chain, E * sizeof(ChainEntry), cudaMemcpyDeviceToHost, st));
-    CTX_TRY(c, cudaStreamSynchronize(st));
-    std::vector<uint64_t> hk(E), hf(E);
-    std::vector<uint32_t> hv(E);
-    for (uint32_t i = 0; i < E; i++) { hk[i] = h[i].key; hf[i] = h[i].first; hv[i] = i; }
-    CTX_TRY(c, cudaMemcpyAsync(k1, hf.data(), E * 8, cudaMemcpyHostToDevice, st));
-    CTX_TRY(c, cudaMemcpyAsync(v1, hv.data(), E * 4, cudaMemcpyHostToDevice, st));
-    size_t tmp = 0;
-    void* t = nullptr;
-    CTX_TRY(c, cub::DeviceRadixSort::SortPairs(nullptr, tmp, k1, k2, v1, v2, E, 0, 64, st));
-    CTX_TRY(c, cudaMallocAsync(&t, tmp, st));
-    CTX_TRY(c, cub::DeviceRadixSort::SortPairs(t, tmp, k1, k2, v1, v2, E, 0, 64, st));
-    // second pass keys: chain key of the sorted entries
-    std::vector<uint32_t> hv2(E);
-    CTX_TRY(c, cudaMemcpyAsync(hv2.data(), v2, E * 4, cudaMemcpyDeviceToHost, st));
-    CTX_TRY(c, cudaStreamSynchronize(st));
-    for (uint32_t i = 0; i < E; i++) hk[i] = h[hv2[i]].key;
-    CTX_TRY(c, cudaMemcpyAsync(k1, hk.data(), E * 8, cudaMemcpyHostToDevice, st));
-    CTX_TRY(c, cub::DeviceRadixSort::SortPairs(t, tmp, k1, k2, v2, v1, E, 0, 64, st));
-    chain_check_kernel<<<(E + 255) / 256, 256, 0, st>>>(recs, n, c->chain, v1, E, c->st);
-    CTX_TRY(c, cudaGetLastError());
-    CTX_TRY(c, cudaMemcpyAsync(&out->gs.flags, &c->st->flags, 4, cudaMemcpyDeviceToHost, st));
-    CTX_TRY(c, cudaStreamSynchronize(st));
-    cudaFreeAsync(t, st);
-    cudaFreeAsync(k1, st);
-    cudaFreeAsync(k2, st);
-    cudaFreeAsync(v1, st);
-    cudaFreeAsync(v2, st);
-    launches += 3;
-  }
   out->launches = launches;
   return 0;
 }
@@ -369,7 +329,8 @@ int ct_context_destroy(ct_context* c) {
   cudaFree(c->st);
   cudaFree(c->cells);
   cudaFree(c->tcf);
-  cudaFree(c->chain);
+  cudaFree(c->slots);
+  cudaFree(c->chans);
   cudaFree(c->ring);
   if (c->canon_keep) cudaFree(c->canon_keep);
   for (int k = 0; k < 4; k++) cudaEventDestroy(c->ev[k]);
@@ -457,6 +418,7 @@ int ct_analyze(ct_context* c, const ct_record* recs, uint64_t n, int on_device, 
     max_dev = ro.gs.max_dev;
     if (ro.gs.flags & F_NONCANON) {
       if (cfg->force_path == 1) return fail(c, CT_ERR_NOT_CANONICAL, "trace is not in the canonical layout");
+      max_dev = -1;  // the aborted pass may not have visited every record: re-infer d below
       if (int e = do_exact()) return e;
     }
   }
@@ -709,18 +671,94 @@ uint64_t ct_generate_boundary(int kind, uint64_t at) { return generate_boundary(
 
 // ------------------------------------------------------------------ multi-GPU partials
 // Layout (uint64 words): header[16] | calls[9] pay_lo[9] pay_hi[9] diag[6] |
-// tcf[6 * n_comms] | cells[ncell] | freq[ncell] | kChainExport slots of chain-boundary
-// records.  Header: magic, g2, n_comms, n, flags, max_dev + 1, oor_key, oor_gpu,
-// copy_first[3], path, d_explicit + 1, 3 reserved.
+// tcf[6 * n_comms] | cells[ncell] | freq[ncell] | kExport comm summaries | 1 flag word.
+// Header: magic, g2, n_comms, n, flags, max_dev + 1, oor_key, oor_gpu, copy_first[3],
+// path, 4 reserved.  A comm summary: comm, n, first / last block head, the records of
+// the shard's first and last block of the comm (<= 32 each), p2p first / last seq per
+// (rank, send|recv) — what the merge needs to re-check seq order across shards.
 namespace {
 constexpr uint64_t kPartialMagic = 0x4354503250415254ull;
-constexpr int kChainExport = 16;
-constexpr int kExportN = 64;  // largest communicator whose boundary blocks are exported
-constexpr uint64_t kSlotWords = 5 + 2 * (uint64_t)kExportN * 4;
+constexpr int kExport = 16;
+constexpr uint64_t kExpWords = 4 + 2 * 32 * 4;  // comm, n, first / last head, 2 x 32 records
+constexpr int kExportCh = 64;                    // p2p channel summaries
+constexpr uint64_t kChWords = 5;                 // key, first_s, first_r, last_s, last_r
 constexpr uint64_t kHdr = 16, kStats = 33;
 
 uint64_t partial_words(int g2, uint32_t n_comms) {
-  return kHdr + kStats + 6ull * n_comms + 2ull * kTypes * g2 * g2 + kChainExport * kSlotWords;
+  return kHdr + kStats + 6ull * n_comms + 2ull * kTypes * g2 * g2 + kExport * kExpWords + kExportCh * kChWords + 1;
+}
+
+// comm / channel lists of a shard in first-seen order (single thread, once per export)
+__global__ void k_shard_lists(const WarpSlot* slots, const P2PEntry* chans, uint32_t total_warps, uint64_t* exp,
+                              uint64_t* chx, uint64_t* overflow) {
+  int cnt = 0, cc = 0;
+  for (uint32_t w = 0; w < total_warps; w++) {
+    for (int s = 0; s < kCS; s++) {
+      const WarpSlot& x = slots[(size_t)w * kCS + s];
+      if (x.comm == 0xFFFFFFFFu || x.n == 0) continue;
+      bool seen = false;
+      for (int e = 0; e < cnt; e++) seen |= exp[e * kExpWords] == x.comm;
+      if (seen) continue;
+      if (cnt == kExport) { *overflow = 1; return; }
+      exp[(cnt++) * kExpWords] = x.comm;
+    }
+    for (int q = 0; q < kPC; q++) {
+      const uint64_t key = chans[(size_t)w * kPC + q].key;
+      if (key == ~0ull) continue;
+      bool seen = false;
+      for (int e = 0; e < cc; e++) seen |= chx[e * kChWords] == key;
+      if (seen) continue;
+      if (cc == kExportCh) { *overflow = 1; return; }
+      chx[(cc++) * kChWords] = key;
+    }
+  }
+}
+
+// block e < kExport: collective summary of comm e; block kExport: channel summaries
+__global__ void k_shard_summary(const WarpSlot* slots, const P2PEntry* chans, uint32_t total_warps,
+                                const ct_record* recs, uint64_t* exp, uint64_t* chx) {
+  if (blockIdx.x == kExport) {
+    const int e = threadIdx.x;
+    if (e >= kExportCh) return;
+    uint64_t* o = chx + e * kChWords;
+    if (o[0] == ~0ull) return;
+    bool got = false;
+    for (uint32_t w = 0; w < total_warps && !got; w++)
+      for (int q = 0; q < kPC; q++) {
+        const P2PEntry& x = chans[(size_t)w * kPC + q];
+        if (x.key == o[0]) { o[1] = x.first_s; o[2] = x.first_r; got = true; break; }
+      }
+    got = false;
+    for (int64_t w = (int64_t)total_warps - 1; w >= 0 && !got; w--)
+      for (int q = 0; q < kPC; q++) {
+        const P2PEntry& x = chans[(size_t)w * kPC + q];
+        if (x.key == o[0]) { o[3] = x.last_s; o[4] = x.last_r; got = true; break; }
+      }
+    return;
+  }
+  if (threadIdx.x) return;
+  uint64_t* o = exp + blockIdx.x * kExpWords;
+  const uint64_t cm = o[0];
+  if (cm == ~0ull) return;
+  uint64_t first = ~0ull, last = ~0ull, n = 0;
+  for (uint32_t w = 0; w < total_warps && first == ~0ull; w++)
+    for (int s = 0; s < kCS; s++) {
+      const WarpSlot& x = slots[(size_t)w * kCS + s];
+      if (x.comm == cm && x.n) { first = x.coll_first; n = x.n; break; }
+    }
+  for (int64_t w = (int64_t)total_warps - 1; w >= 0 && last == ~0ull; w--)
+    for (int s = 0; s < kCS; s++) {
+      const WarpSlot& x = slots[(size_t)w * kCS + s];
+      if (x.comm == cm && x.n) { last = x.coll_last; break; }
+    }
+  o[1] = n;
+  o[2] = first;
+  o[3] = last;
+  if (n && n <= 32) {
+    ct_record* fr = reinterpret_cast<ct_record*>(o + 4);
+    ct_record* lr = reinterpret_cast<ct_record*>(o + 4 + 32 * 4);
+    for (uint64_t r = 0; r < n; r++) { fr[r] = recs[first + r]; lr[r] = recs[last + r]; }
+  }
 }
 
 __global__ void k_merge_partials(const uint64_t* parts, int world, uint64_t words, int g2, uint32_t n_comms,
@@ -728,12 +766,6 @@ __global__ void k_merge_partials(const uint64_t* parts, int world, uint64_t word
   const uint64_t ncell = (uint64_t)kTypes * g2 * g2;
   const uint64_t o_tcf = kHdr + kStats, o_cells = o_tcf + 6ull * n_comms;
   const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t j = tid; j < 2 * ncell; j += stride) {
-    unsigned __int128 s = 0;
-    for (int w = 0; w < world; w++) s += parts[w * words + o_cells + j];
-    if (s >> 64) { atomicOr(&gs->flags, F_OVERFLOW); s = ~0ull; }
-    cells[j] = (unsigned long long)s;
-  }
   for (uint64_t j = tid; j < 6ull * n_comms; j += stride) {
     uint64_t best = ~0ull, base = 0;
     for (int w = 0; w < world; w++) {
@@ -753,7 +785,8 @@ __global__ void k_merge_partials(const uint64_t* parts, int world, uint64_t word
     for (int w = 0; w < world; w++) {
       const uint64_t* p = parts + w * words;
       g.flags |= (uint32_t)p[4];
-      if (p[11] != 1) g.flags |= F_NONCANON;  // shards must have taken the fast path
+      if (p[11] != 1) g.flags |= F_NONCANON;  // every shard must have taken the fast path
+      if (p[words - 1]) g.flags |= F_NONCANON;  // comm summary overflow
       g.max_dev = max(g.max_dev, (int)p[5] - 1);
       if (p[6] != ~0ull) {
         const uint64_t k = p[6] + (base << 21);
@@ -763,47 +796,64 @@ __global__ void k_merge_partials(const uint64_t* parts, int world, uint64_t word
         if (p[8 + k] != ~0ull && p[8 + k] + base < g.copy_first[k]) g.copy_first[k] = p[8 + k] + base;
       for (int t = 0; t < kTypes; t++) {
         g.calls[t] += p[kHdr + t];
-        const unsigned long long lo = p[kHdr + 9 + t];
         const unsigned long long old = g.pay_lo[t];
-        g.pay_lo[t] = old + lo;
+        g.pay_lo[t] = old + p[kHdr + 9 + t];
         g.pay_hi[t] += p[kHdr + 18 + t] + (g.pay_lo[t] < old ? 1 : 0);
       }
       for (int k = 0; k < CT_NDIAG; k++) g.diag[k] += p[kHdr + 27 + k];
       base += p[3];
     }
-    // shard-boundary chains: the last element of a chain in shard w must precede its
-    // first element in the next shard holding it (grouping.py:118, decompose.py:359-360)
-    const uint64_t o_chain = kHdr + kStats + 6ull * n_comms + 2 * ncell;
-    for (int w = 0; w < world; w++) {
-      const uint64_t* pw = parts + w * words + o_chain;
-      for (int s = 0; s < kChainExport; s++) {
-        const uint64_t* a = pw + s * kSlotWords;
-        if (a[1] == ~0ull) continue;
-        bool found = false;
-        for (int v = w + 1; v < world && !found; v++) {
-          const uint64_t* pv = parts + v * words + o_chain;
-          for (int t = 0; t < kChainExport; t++) {
-            const uint64_t* b = pv + t * kSlotWords;
-            if (b[1] == ~0ull || b[0] != a[0] || b[1] != a[1]) continue;
-            found = true;
-            // a: last element records at offset 5 + kExportN*4; b: first element at offset 5
-            const ct_record* ra = reinterpret_cast<const ct_record*>(a + 5 + kExportN * 4);
-            const ct_record* rb = reinterpret_cast<const ct_record*>(b + 5);
-            bool ok;
-            if (a[1] == 0) {
-              ok = ra[0].nranks == rb[0].nranks;
-              for (uint32_t r = 0; ok && r < rb[0].nranks; r++) ok = ra[r].seq < rb[r].seq;
-            } else {
-              ok = ra[0].seq <= rb[0].seq && ra[1].seq <= rb[1].seq;
-            }
-            if (!ok) g.flags |= F_NONCANON;
-            break;
-          }
-        }
-      }
-    }
+    g.flags |= gs->flags;  // k_merge_order ran before this kernel
     *gs = g;
   }
+}
+
+__global__ void k_merge_cells(const uint64_t* parts, int world, uint64_t words, int g2, uint32_t n_comms,
+                              unsigned long long* cells, GlobalState* gs) {
+  const uint64_t ncell = (uint64_t)kTypes * g2 * g2;
+  const uint64_t o_cells = kHdr + kStats + 6ull * n_comms;
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < 2 * ncell; j += (uint64_t)gridDim.x * blockDim.x) {
+    unsigned __int128 s = 0;
+    for (int w = 0; w < world; w++) s += parts[w * words + o_cells + j];
+    if (s >> 64) { atomicOr(&gs->flags, F_OVERFLOW); s = ~0ull; }
+    cells[j] = (unsigned long long)s;
+  }
+}
+
+// shard-boundary order: for every (shard v, summary) with a first element, the nearest
+// earlier shard holding the same chain must end before it
+__global__ void k_merge_order(const uint64_t* parts, int world, uint64_t words, uint64_t o_exp, GlobalState* gs) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int per = kExport + kExportCh;
+  if (t >= world * per) return;
+  const int v = t / per, e = t % per;
+  if (v == 0) return;
+  const uint64_t o_ch = o_exp + kExport * kExpWords;
+  if (e < kExport) {
+    const uint64_t* me = parts + v * words + o_exp + e * kExpWords;
+    if (me[0] == ~0ull || !me[1]) return;
+    for (int w = v - 1; w >= 0; w--)
+      for (int q = 0; q < kExport; q++) {
+        const uint64_t* o = parts + w * words + o_exp + q * kExpWords;
+        if (o[0] != me[0] || !o[1]) continue;
+        bool ok = o[1] == me[1] && me[1] <= 32;
+        const ct_record* lr = reinterpret_cast<const ct_record*>(o + 4 + 32 * 4);
+        const ct_record* fr = reinterpret_cast<const ct_record*>(me + 4);
+        for (uint64_t r = 0; ok && r < me[1]; r++) ok = lr[r].seq < fr[r].seq;
+        if (!ok) atomicOr(&gs->flags, F_NONCANON);
+        return;
+      }
+    return;
+  }
+  const uint64_t* me = parts + v * words + o_ch + (e - kExport) * kChWords;
+  if (me[0] == ~0ull) return;
+  for (int w = v - 1; w >= 0; w--)
+    for (int q = 0; q < kExportCh; q++) {
+      const uint64_t* o = parts + w * words + o_ch + q * kChWords;
+      if (o[0] != me[0]) continue;
+      if (me[1] < o[3] || me[2] < o[4]) atomicOr(&gs->flags, F_NONCANON);
+      return;
+    }
 }
 }  // namespace
 
@@ -835,64 +885,25 @@ int ct_partial_export(ct_context* c, uint64_t* dev_out, uint64_t words, void* st
   hdr[7] = (c->last.status == CT_ERR_ENDPOINT_RANGE) ? c->last.err_aux[0] : 0;
   for (int k = 0; k < 3; k++) hdr[8 + k] = gs.copy_first[k];
   hdr[11] = (uint64_t)c->last.path;
-  hdr[12] = 0;
   for (int t = 0; t < kTypes; t++) {
     hdr[kHdr + t] = gs.calls[t];
     hdr[kHdr + 9 + t] = gs.pay_lo[t];
     hdr[kHdr + 18 + t] = gs.pay_hi[t];
   }
   for (int k = 0; k < CT_NDIAG; k++) hdr[kHdr + 27 + k] = c->last.diag[k];
-  // chain boundary elements: per key, the first element and the last element of this shard
-  const uint32_t E = std::min(gs.n_chain, c->chain_cap);
-  std::vector<ChainEntry> ch(E);
-  if (E) {
-    CTX_TRY(c, cudaMemcpyAsync(ch.data(), c->chain, E * sizeof(ChainEntry), cudaMemcpyDeviceToHost, st));
-    CTX_TRY(c, cudaStreamSynchronize(st));
-  }
-  std::vector<std::pair<uint64_t, std::pair<uint64_t, uint64_t>>> keys;  // key -> (min first, max last)
-  for (const ChainEntry& e : ch) {
-    bool hit = false;
-    for (auto& k : keys)
-      if (k.first == e.key) {
-        k.second.first = std::min(k.second.first, e.first);
-        k.second.second = std::max(k.second.second, e.last);
-        hit = true;
-      }
-    if (!hit) keys.push_back({e.key, {e.first, e.last}});
-  }
-  if (keys.size() > (size_t)kChainExport) hdr[4] |= F_CHAIN_CAP | F_NONCANON;
+  const uint64_t o_tcf = kHdr + kStats, o_cells = o_tcf + 6ull * nc, o_exp = o_cells + 2 * ncell;
   CTX_TRY(c, cudaMemcpyAsync(dev_out, hdr.data(), hdr.size() * 8, cudaMemcpyHostToDevice, st));
-  const uint64_t o_tcf = kHdr + kStats, o_cells = o_tcf + 6ull * nc, o_chain = o_cells + 2 * ncell;
   CTX_TRY(c, cudaMemcpyAsync(dev_out + o_tcf, c->tcf, 6ull * nc * 8, cudaMemcpyDeviceToDevice, st));
   CTX_TRY(c, cudaMemcpyAsync(dev_out + o_cells, c->cells, 2 * ncell * 8, cudaMemcpyDeviceToDevice, st));
-  std::vector<uint64_t> slots(kChainExport * kSlotWords, 0);
-  for (int s = 0; s < kChainExport; s++) slots[s * kSlotWords + 1] = ~0ull;
-  for (size_t s = 0; s < keys.size() && s < (size_t)kChainExport; s++) {
-    uint64_t* o = slots.data() + s * kSlotWords;
-    const bool p2p = (keys[s].first >> 63) != 0;
-    o[0] = keys[s].first;
-    o[1] = p2p ? 1 : 0;
-    o[3] = keys[s].second.first;
-    o[4] = keys[s].second.second;
+  CTX_TRY(c, cudaMemsetAsync(dev_out + o_exp, 0xFF, (kExport * kExpWords + kExportCh * kChWords) * 8, st));
+  CTX_TRY(c, cudaMemsetAsync(dev_out + words - 1, 0, 8, st));
+  if (c->last.path == 1 && c->last_total_warps) {
+    uint64_t* chx = dev_out + o_exp + kExport * kExpWords;
+    k_shard_lists<<<1, 1, 0, st>>>(c->slots, c->chans, c->last_total_warps, dev_out + o_exp, chx, dev_out + words - 1);
+    k_shard_summary<<<kExport + 1, 64, 0, st>>>(c->slots, c->chans, c->last_total_warps, c->last_input,
+                                                dev_out + o_exp, chx);
+    CTX_TRY(c, cudaGetLastError());
   }
-  CTX_TRY(c, cudaMemcpyAsync(dev_out + o_chain, slots.data(), slots.size() * 8, cudaMemcpyHostToDevice, st));
-  for (size_t s = 0; s < keys.size() && s < (size_t)kChainExport; s++) {
-    const bool p2p = (keys[s].first >> 63) != 0;
-    ct_record head{};
-    if (host_dev_of(c, c->last_input, keys[s].second.first, st, &head)) return CT_ERR_CUDA;
-    const uint64_t m = p2p ? 2 : head.nranks;
-    if (m > (uint64_t)kExportN) {
-      hdr[4] |= F_CHAIN_CAP | F_NONCANON;
-      CTX_TRY(c, cudaMemcpyAsync(dev_out + 4, &hdr[4], 8, cudaMemcpyHostToDevice, st));
-      continue;
-    }
-    uint64_t* o = dev_out + o_chain + s * kSlotWords;
-    CTX_TRY(c, cudaMemcpyAsync(o + 5, c->last_input + keys[s].second.first, m * sizeof(ct_record),
-                               cudaMemcpyDeviceToDevice, st));
-    CTX_TRY(c, cudaMemcpyAsync(o + 5 + kExportN * 4, c->last_input + keys[s].second.second,
-                               m * sizeof(ct_record), cudaMemcpyDeviceToDevice, st));
-  }
-  CTX_TRY(c, cudaStreamSynchronize(st));
   return CT_OK;
 }
 
@@ -901,19 +912,19 @@ int ct_partial_merge(ct_context* c, const uint64_t* dev_in, int world, uint64_t 
   if (!c || !dev_in || !out || world < 1) return fail(c, CT_ERR_ARGUMENT, "bad argument");
   CTX_TRY(c, cudaSetDevice(c->device));
   cudaStream_t st = stream ? (cudaStream_t)stream : c->stream;
-  uint64_t h0[3];
-  CTX_TRY(c, cudaMemcpyAsync(h0, dev_in, 24, cudaMemcpyDeviceToHost, st));
+  std::vector<uint64_t> h0(4 * (size_t)world);
+  for (int w = 0; w < world; w++)
+    CTX_TRY(c, cudaMemcpyAsync(&h0[4 * w], dev_in + w * words, 32, cudaMemcpyDeviceToHost, st));
   CTX_TRY(c, cudaStreamSynchronize(st));
   if (h0[0] != kPartialMagic) return fail(c, CT_ERR_ARGUMENT, "not a ct partial");
   const int g2 = (int)h0[1];
   const uint32_t nc = (uint32_t)h0[2];
   if (words != partial_words(g2, nc)) return fail(c, CT_ERR_ARGUMENT, "partial size mismatch");
-  for (int w = 1; w < world; w++) {
-    uint64_t hw[3];
-    CTX_TRY(c, cudaMemcpyAsync(hw, dev_in + w * words, 24, cudaMemcpyDeviceToHost, st));
-    CTX_TRY(c, cudaStreamSynchronize(st));
-    if (hw[0] != kPartialMagic || hw[1] != h0[1] || hw[2] != h0[2])
+  uint64_t n = 0;
+  for (int w = 0; w < world; w++) {
+    if (h0[4 * w] != kPartialMagic || h0[4 * w + 1] != h0[1] || h0[4 * w + 2] != h0[2])
       return fail(c, CT_ERR_ARGUMENT, "partials disagree on layout (use the same d / dev_hint on every rank)");
+    n += h0[4 * w + 3];
   }
   const uint64_t ncell = (uint64_t)kTypes * g2 * g2;
   size_t cap = c->cells_cap;
@@ -924,32 +935,26 @@ int ct_partial_merge(ct_context* c, const uint64_t* dev_in, int world, uint64_t 
   c->tcf_cap = cap;
   memset(out, 0, sizeof *out);
   CTX_TRY(c, cudaEventRecord(c->ev[2], st));
-  k_merge_partials<<<64, 256, 0, st>>>(dev_in, world, words, g2, nc, c->cells, c->tcf, c->st);
+  CTX_TRY(c, cudaMemsetAsync(c->st, 0, sizeof(GlobalState), st));
+  const uint64_t o_exp = kHdr + kStats + 6ull * nc + 2 * ncell;
+  k_merge_order<<<(world * (kExport + kExportCh) + 255) / 256, 256, 0, st>>>(dev_in, world, words, o_exp, c->st);
+  k_merge_partials<<<1, 256, 0, st>>>(dev_in, world, words, g2, nc, c->cells, c->tcf, c->st);
+  k_merge_cells<<<64, 256, 0, st>>>(dev_in, world, words, g2, nc, c->cells, c->st);
   CTX_TRY(c, cudaGetLastError());
   GlobalState gs;
   CTX_TRY(c, cudaMemcpyAsync(&gs, c->st, sizeof gs, cudaMemcpyDeviceToHost, st));
-  uint64_t dexp = 0;
-  CTX_TRY(c, cudaMemcpyAsync(&dexp, dev_in + 12, 8, cudaMemcpyDeviceToHost, st));
   CTX_TRY(c, cudaStreamSynchronize(st));
   if (gs.flags & F_NONCANON)
-    return fail(c, CT_ERR_NOT_CANONICAL, "sharded analysis needs the canonical layout in every shard");
-  uint64_t n = 0;
-  for (int w = 0; w < world; w++) {
-    uint64_t nw;
-    CTX_TRY(c, cudaMemcpyAsync(&nw, dev_in + w * words + 3, 8, cudaMemcpyDeviceToHost, st));
-    CTX_TRY(c, cudaStreamSynchronize(st));
-    n += nw;
-  }
+    return fail(c, CT_ERR_NOT_CANONICAL, "sharded analysis needs the canonical layout in every shard and across shard boundaries");
   const int gcap = g2 - 2;
-  const int64_t d = c->last.d >= 0 && (c->last.status == CT_OK || c->last.status == CT_ERR_ENDPOINT_RANGE) &&
-                            c->last_explicit ? c->last.d : (int64_t)gs.max_dev + 1;
+  const int64_t d = c->last_explicit ? c->last.d : (int64_t)gs.max_dev + 1;
   const uint64_t extra[3] = {0, 0, 0};
   if (int e = summarize_state(c, gs, gcap, d, 1, extra, nullptr, nc, st, out)) return e;
   out->n_records = n;
   CTX_TRY(c, cudaEventRecord(c->ev[3], st));
   CTX_TRY(c, cudaEventSynchronize(c->ev[3]));
   CTX_TRY(c, cudaEventElapsedTime(&out->ms_total, c->ev[2], c->ev[3]));
-  out->n_launches = 1;
+  out->n_launches = 3;
   c->last = *out;
   return out->status;
 }

@@ -148,6 +148,28 @@ __device__ __forceinline__ void tree_edges(int n, int r, bool with_t2, TreeEdges
   }
 }
 
+// floor(s / n) for a small divisor without the 64-bit integer division sequence: one
+// double-precision reciprocal multiply (exact to +-1 for s < 2^52) and one correction.
+__device__ __forceinline__ uint64_t udiv_small(uint64_t s, uint32_t n) {
+  if (s < (1ull << 52)) {
+    uint64_t q = (uint64_t)((double)s * __drcp_rn((double)n));
+    const int64_t r = (int64_t)(s - q * n);
+    if (r < 0) q--;
+    else if (r >= (int64_t)n) q++;
+    return q;
+  }
+  return s / n;
+}
+
+__device__ __forceinline__ uint64_t ceil_div(uint64_t s, uint32_t n) {
+  const uint64_t q = udiv_small(s, n);
+  return q + (q * n != s ? 1 : 0);
+}
+
+__device__ __forceinline__ unsigned __int128 ceil_div(unsigned __int128 s, uint32_t n) {
+  return (s + (unsigned __int128)(n - 1)) / (unsigned __int128)n;
+}
+
 // ring block size b[i] for an n-way split of s with chunk = ceil(s/n) (decompose.py:104-107)
 __device__ __forceinline__ uint64_t ring_block(uint64_t s, uint64_t chunk, int i) {
   uint64_t off = (uint64_t)i * chunk;

@@ -70,7 +70,7 @@ __device__ void expand_collective(const ExpandParams& P, const DevOf& v, Sink& a
   U bytes;
   switch (coll) {
     case CT_COLL_ALLREDUCE: {
-      const U chunk = (s + (U)(n - 1)) / (U)n;
+      const U chunk = ceil_div(s, (uint32_t)n);
       int p1 = p + 1 == n ? 0 : p + 1;
       int p2 = p1 + 1 == n ? 0 : p1 + 1;
       U o1 = (U)p1 * chunk, o2 = (U)p2 * chunk;

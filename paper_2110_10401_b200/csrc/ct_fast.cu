@@ -1,29 +1,32 @@
-// Fast path: fused layout check + expand + accumulate (see ct_fast.cuh for the plan).
+// Fast path: warp-autonomous streaming layout check + join + expand + accumulate
+// (design notes in ct_fast.cuh).
 #include "ct_fast.cuh"
 
 namespace ct {
 
 namespace {
 
-constexpr uint64_t kEmptyKey = 0x7FFFFFFFFFFFFFFFull;
-constexpr uint32_t kEmptyTag = 0xFFFFFFFFu;
 constexpr uint64_t kNone = ~0ull;
+constexpr uint32_t kEmptyTag = 0xFFFFFFFFu;
+constexpr unsigned kFull = 0xFFFFFFFFu;
 
-struct __align__(128) SmemFixed {
-  ct_record ring[kStages][kSub];
-  unsigned long long mbar[kStages];
-  uint64_t ekey[kSub];
-  uint16_t elist[kSub];
-  uint8_t status[kSub];
-  uint8_t iselem[kSub];
-  ChainEntry chain[kWarps][kChainW];
+struct __align__(16) WarpMem {
+  ct_record ring[kRing][32];                 // TMA ring: chunk k lives in slot (k - k0) % kRing
+  unsigned long long bar[kRing];
+  unsigned long long cseq[kCS][kMaxN];       // last collective block: seq per rank
+  P2PEntry chan[kPC];                        // p2p channels: first / last send and recv seq
+  unsigned long long cfirst[kCS], clast[kCS];
+  unsigned long long tfirst[kCS][5];
+  uint16_t cdev[kCS][kMaxN];                 // last collective block: device per rank
+  uint32_t tag[kCS];                         // comm id of the slot
+  uint32_t sn[kCS];                          // collective nranks of the slot (0: none yet)
+  uint32_t sver[kCS];                        // last block's devices pairwise distinct
+};
+
+struct __align__(16) CtaMem {
   unsigned long long calls[kTypes], pay_lo[kTypes], pay_hi[kTypes];
-  unsigned long long tf[5][kCommSm];
-  unsigned long long cf[kCommSm];
   unsigned long long copy_first[3];
-  uint32_t warp_cnt[kWarps];
   unsigned int diag[CT_NDIAG];
-  uint32_t ne;
   uint32_t flags;
   int max_dev;
 };
@@ -37,14 +40,9 @@ __device__ __forceinline__ void mbar_init(unsigned long long* bar, uint32_t coun
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
 }
 
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
-               "r"(bytes)
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
                : "memory");
-}
-
-__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes,
-                                          unsigned long long* bar) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
           smem_addr(dst)),
@@ -63,464 +61,555 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t pari
   }
 }
 
-// ------------------------------------------------------------ record access
-struct View {
-  const ct_record* g;    // whole analyzed array
-  const ct_record* cur;  // current sub-tile in shared memory
-  uint64_t base;         // index of cur[0]
-  uint32_t len;
-  uint64_t n;
-  __device__ __forceinline__ Rec get(uint64_t i) const {
-    uint64_t off = i - base;
-    return off < len ? load_shared(cur + off) : load_global(g + i);
-  }
-  __device__ __forceinline__ uint32_t dev_of(uint64_t i) const {
-    uint64_t off = i - base;
-    const uint32_t* w = off < len ? reinterpret_cast<const uint32_t*>(cur + off)
-                                  : reinterpret_cast<const uint32_t*>(g + i);
-    return (off < len ? w[6] : __ldg(w + 6)) & 0xFFFF;
-  }
-  __device__ __forceinline__ uint64_t seq_of(uint64_t i) const {
-    uint64_t off = i - base;
-    if (off < len) return reinterpret_cast<const uint64_t*>(cur + off)[1];
-    return __ldg(reinterpret_cast<const unsigned long long*>(g + i) + 1);
-  }
-};
-
-// Instance validity of the block headed at ``i`` (grouping.py:144-167): signature
-// equality first, then pairwise-distinct devices.  Assumes the block lies in [0, n).
-__device__ uint8_t head_status(const View& v, uint64_t i, const Rec& head) {
-  const uint32_t n = head.nranks;
-  if (i + n > v.n) return ST_NONE;
-  bool incompat = false, dup = false, wide = false;
-  uint64_t seen[4] = {0, 0, 0, 0};
-  for (uint32_t m = 0; m < n; m++) {
-    Rec q = m == 0 ? head : v.get(i + m);
-    if (m && !same_sig(q, head)) incompat = true;
-    uint32_t d = q.dev;
-    if (d < 256) {
-      uint64_t bit = 1ull << (d & 63);
-      uint32_t w = d >> 6;
-      uint64_t word = w == 0 ? seen[0] : w == 1 ? seen[1] : w == 2 ? seen[2] : seen[3];
-      if (word & bit) dup = true;
-      word |= bit;
-      if (w == 0) seen[0] = word; else if (w == 1) seen[1] = word; else if (w == 2) seen[2] = word; else seen[3] = word;
-    } else {
-      wide = true;
-    }
-  }
-  if (wide && !dup) {  // devices >= 256: pairwise among the wide ones
-    for (uint32_t a = 0; a < n && !dup; a++) {
-      uint32_t da = v.dev_of(i + a);
-      if (da < 256) continue;
-      for (uint32_t b = a + 1; b < n; b++)
-        if (v.dev_of(i + b) == da) { dup = true; break; }
-    }
-  }
-  return incompat ? ST_INCOMPAT : dup ? ST_DUPDEV : ST_VALID;
+// conflict-free 32-B record read from shared memory: lanes alternate which 16-B half
+// they fetch first so each quarter-warp covers all 32 banks
+__device__ __forceinline__ Rec load_swz(const ct_record* base, int i) {
+  const uint4* q = reinterpret_cast<const uint4*>(base + i);
+  const int f = (i >> 2) & 1;
+  const uint4 x = q[f], y = q[f ^ 1];
+  return f ? unpack(y, x) : unpack(x, y);
 }
 
-// consecutive chain elements (pred before cur): reference seq ordering holds
-__device__ bool chain_ok(const View& v, uint64_t pred, uint64_t cur) {
-  Rec a = v.get(pred), b = v.get(cur);
-  if (b.kind() == CT_KIND_COLLECTIVE) {
-    const uint32_t n = b.nranks;
-    if (a.nranks != n || pred + n > v.n || cur + n > v.n) return false;
-    for (uint32_t r = 0; r < n; r++) {
-      uint64_t sa = r ? v.seq_of(pred + r) : a.seq;
-      uint64_t sb = r ? v.seq_of(cur + r) : b.seq;
-      if (!(sa < sb)) return false;
-    }
-    return true;
-  }
-  if (pred + 1 >= v.n || cur + 1 >= v.n) return false;
-  return a.seq <= b.seq && v.seq_of(pred + 1) <= v.seq_of(cur + 1);
+__device__ __forceinline__ bool is_start(int kind, uint32_t rank) {
+  return kind == CT_KIND_COLLECTIVE ? rank == 0
+                                    : (kind == CT_KIND_SEND || (kind >= CT_KIND_MEMCPY && kind <= CT_KIND_ZEROCOPY));
 }
 
-__device__ __forceinline__ uint32_t hash64(uint64_t k) {
-  return static_cast<uint32_t>((k * 0x9E3779B97F4A7C15ull) >> 32);
+// first element start at or after x (warp-cooperative, reads global memory)
+__device__ uint64_t first_start(const ct_record* g, uint64_t n, uint64_t x, bool& bad) {
+  const int lane = threadIdx.x & 31;
+  for (int probe = 0; probe < 3; probe++) {
+    const uint64_t base = x + 32ull * probe;
+    if (base >= n) return n;
+    const uint64_t i = base + lane;
+    bool st = false;
+    if (i < n) {
+      const uint4 w = __ldg(reinterpret_cast<const uint4*>(g + i) + 1);
+      st = is_start((w.w >> 16) & 7, w.y >> 16);
+    }
+    const unsigned m = __ballot_sync(kFull, st);
+    if (m) return base + (__ffs(m) - 1);
+  }
+  bad = true;  // no element start within 96 records: not the canonical layout
+  return x;
 }
 
 // ------------------------------------------------------------ accumulation
 struct Acc {
-  // register cache: (key, bytes, count); key = cell index or kStatsKeyBit | type
-  uint32_t tag[kCacheE];
-  unsigned long long sum[kCacheE];
-  uint32_t cnt[kCacheE];
+  // two small register caches: transfer cells and per-type statistics; a miss evicts the
+  // older entry into the CTA histogram (shared-memory atomics)
+  uint32_t ctag[2], stag[2];
+  unsigned long long csum[2], ssum[2];
+  uint32_t ccnt[2], scnt[2];
   uint32_t flags;
-  unsigned long long* hb;  // histogram bytes (shared or global)
-  void* hf;                // histogram counts: u32 shared or u64 global
+  unsigned long long* hb;
+  void* hf;
   bool smem;
-  SmemFixed* S;
+  CtaMem* C;
   int g2, gcap;
   bool explicit_d;
   unsigned long long rec_key;  // (class << 62) | (element << 21) | (src rank << 11) for oor ordering
   unsigned long long oor_key;
   unsigned long long of_cell;
 
-  __device__ void init(SmemFixed* s, unsigned long long* b, void* f, bool sm, int g2_, int gcap_, bool ex) {
-#pragma unroll
-    for (int e = 0; e < kCacheE; e++) { tag[e] = kEmptyTag; sum[e] = 0; cnt[e] = 0; }
-    flags = 0; hb = b; hf = f; smem = sm; S = s; g2 = g2_; gcap = gcap_; explicit_d = ex;
-    rec_key = 0; oor_key = ~0ull; of_cell = ~0ull;
+  __device__ void init(CtaMem* c, unsigned long long* b, void* f, bool sm, int g2_, int gcap_, bool ex) {
+    ctag[0] = ctag[1] = stag[0] = stag[1] = kEmptyTag;
+    csum[0] = csum[1] = ssum[0] = ssum[1] = 0;
+    ccnt[0] = ccnt[1] = scnt[0] = scnt[1] = 0;
+    flags = 0; hb = b; hf = f; smem = sm; C = c; g2 = g2_; gcap = gcap_; explicit_d = ex;
+    rec_key = 0; oor_key = kNone; of_cell = kNone;
   }
 
-  __device__ void flush(uint32_t key, unsigned long long v, uint32_t c) {
-    if (key & kStatsKeyBit) {
-      int t = key & 15;
-      unsigned long long old = atomicAdd(&S->pay_lo[t], v);
-      if (old + v < old) atomicAdd(&S->pay_hi[t], 1ull);
-      atomicAdd(&S->calls[t], (unsigned long long)c);
-      return;
-    }
-    unsigned long long old = atomicAdd(hb + key, v);
+  __device__ void flush_cell(uint32_t key, unsigned long long v, uint32_t c) {
+    const unsigned long long old = atomicAdd(hb + key, v);
     if (old + v < old) { flags |= F_OVERFLOW; if (key < of_cell) of_cell = key; }
     if (smem) atomicAdd(static_cast<unsigned int*>(hf) + key, c);
     else atomicAdd(static_cast<unsigned long long*>(hf) + key, (unsigned long long)c);
   }
 
-  __device__ __forceinline__ void add(uint32_t key, unsigned long long v) {
-    bool hit = false;
-#pragma unroll
-    for (int e = 0; e < kCacheE; e++) {
-      if (tag[e] == key) {
-        unsigned long long s = sum[e] + v;
-        if (s < v) { flags |= F_OVERFLOW; if (key < of_cell) of_cell = key; }
-        sum[e] = s;
-        cnt[e] += 1;
-        hit = true;
-      }
+  __device__ void flush_stat(uint32_t t, unsigned long long v, uint32_t c) {
+    const unsigned long long old = atomicAdd(&C->pay_lo[t], v);
+    if (old + v < old) atomicAdd(&C->pay_hi[t], 1ull);
+    atomicAdd(&C->calls[t], (unsigned long long)c);
+  }
+
+  __device__ __forceinline__ void add_cell(uint32_t key, unsigned long long v) {
+    if (ctag[0] == key) {
+      const unsigned long long s = csum[0] + v;
+      if (s < v) { flags |= F_OVERFLOW; if (key < of_cell) of_cell = key; }
+      csum[0] = s; ccnt[0]++;
+    } else if (ctag[1] == key) {
+      const unsigned long long s = csum[1] + v;
+      if (s < v) { flags |= F_OVERFLOW; if (key < of_cell) of_cell = key; }
+      csum[1] = s; ccnt[1]++;
+    } else {
+      if (ctag[1] != kEmptyTag) flush_cell(ctag[1], csum[1], ccnt[1]);
+      ctag[1] = ctag[0]; csum[1] = csum[0]; ccnt[1] = ccnt[0];
+      ctag[0] = key; csum[0] = v; ccnt[0] = 1;
     }
-    if (!hit) {
-      if (tag[kCacheE - 1] != kEmptyTag) flush(tag[kCacheE - 1], sum[kCacheE - 1], cnt[kCacheE - 1]);
-#pragma unroll
-      for (int e = kCacheE - 1; e > 0; e--) { tag[e] = tag[e - 1]; sum[e] = sum[e - 1]; cnt[e] = cnt[e - 1]; }
-      tag[0] = key; sum[0] = v; cnt[0] = 1;
+  }
+
+  // payload sums are 128-bit in the CTA: flush before a register entry would wrap
+  __device__ __forceinline__ void add_stat(uint32_t t, unsigned long long v) {
+    if (stag[0] == t) {
+      if (ssum[0] + v < v) { flush_stat(t, ssum[0], scnt[0]); ssum[0] = v; scnt[0] = 1; }
+      else { ssum[0] += v; scnt[0]++; }
+    } else if (stag[1] == t) {
+      if (ssum[1] + v < v) { flush_stat(t, ssum[1], scnt[1]); ssum[1] = v; scnt[1] = 1; }
+      else { ssum[1] += v; scnt[1]++; }
+    } else {
+      if (stag[1] != kEmptyTag) flush_stat(stag[1], ssum[1], scnt[1]);
+      stag[1] = stag[0]; ssum[1] = ssum[0]; scnt[1] = scnt[0];
+      stag[0] = t; ssum[0] = v; scnt[0] = 1;
     }
   }
 
   __device__ void drain() {
-#pragma unroll
-    for (int e = 0; e < kCacheE; e++) {
-      if (tag[e] != kEmptyTag) flush(tag[e], sum[e], cnt[e]);
-      tag[e] = kEmptyTag;
-    }
+    if (ctag[0] != kEmptyTag) flush_cell(ctag[0], csum[0], ccnt[0]);
+    if (ctag[1] != kEmptyTag) flush_cell(ctag[1], csum[1], ccnt[1]);
+    if (stag[0] != kEmptyTag) flush_stat(stag[0], ssum[0], scnt[0]);
+    if (stag[1] != kEmptyTag) flush_stat(stag[1], ssum[1], scnt[1]);
+    ctag[0] = ctag[1] = stag[0] = stag[1] = kEmptyTag;
   }
 
   // stats: calls += 1, payload += s (128-bit capable)
   __device__ __forceinline__ void stat(int type, unsigned __int128 s) {
-    if ((s >> 63) == 0) { add(kStatsKeyBit | type, (unsigned long long)s); return; }
-    unsigned long long lo = (unsigned long long)s, hi = (unsigned long long)(s >> 64);
-    unsigned long long old = atomicAdd(&S->pay_lo[type], lo);
+    if ((s >> 63) == 0) { add_stat((uint32_t)type, (unsigned long long)s); return; }
+    stat_big(type, s);
+  }
+
+  __device__ __noinline__ void stat_big(int type, unsigned __int128 s) {
+    const unsigned long long lo = (unsigned long long)s;
+    unsigned long long hi = (unsigned long long)(s >> 64);
+    const unsigned long long old = atomicAdd(&C->pay_lo[type], lo);
     if (old + lo < old) hi += 1;
-    atomicAdd(&S->pay_hi[type], hi);
-    atomicAdd(&S->calls[type], 1ull);
+    atomicAdd(&C->pay_hi[type], hi);
+    atomicAdd(&C->calls[type], 1ull);
   }
 
-  // endpoint: gpu g (g >= 0) or -1 host / -2 net
-  __device__ __forceinline__ bool index(int ep, int& idx, unsigned long long k) {
-    if (ep == -1) { idx = kHost; return true; }
-    if (ep == -2) { idx = kNet; return true; }
-    if (ep >= gcap) {
-      flags |= explicit_d ? F_OOR : F_CAP;
-      if (k < oor_key) oor_key = k;
-      return false;
-    }
-    idx = ep + 2;
-    return true;
+  __device__ __noinline__ void out_of_range(unsigned long long k) {
+    flags |= explicit_d ? F_OOR : F_CAP;
+    if (k < oor_key) oor_key = k;
   }
 
-  // ``sub`` orders transfers inside one decomposition: the destination rank for
-  // collectives (transfers are sorted by rank pair, decompose.py:92), 0/1 for collnet.
+  // endpoint: gpu g (>= 0), -1 host, -2 net.  ``sub`` orders transfers inside one
+  // decomposition (destination rank of a collective edge, transfers are sorted by rank
+  // pair, decompose.py:92; 0/1 for collnet) for the EndpointOutOfRange message.
   __device__ __forceinline__ void edge(int type, int src, int dst, unsigned __int128 bytes, int sub = 0) {
-    int a, b;
-    const unsigned long long k = rec_key | ((unsigned long long)min(sub, 1023) << 1);
-    bool ok = index(src, a, k);
-    ok = index(dst, b, k | 1) && ok;
-    if (!ok) return;
+    const int a = src == -1 ? kHost : (src == -2 ? kNet : src + 2);
+    const int b = dst == -1 ? kHost : (dst == -2 ? kNet : dst + 2);
+    if (src >= gcap || dst >= gcap) {
+      const unsigned long long k = rec_key | ((unsigned long long)min(sub, 1023) << 1);
+      if (src >= gcap) out_of_range(k);
+      if (dst >= gcap) out_of_range(k | 1);
+      return;
+    }
     if ((bytes >> 63) != 0) { flags |= F_OVERFLOW; return; }
-    add((uint32_t)((type * g2 + a) * g2 + b), (unsigned long long)bytes);
+    add_cell((uint32_t)((type * g2 + a) * g2 + b), (unsigned long long)bytes);
   }
 };
 
-__device__ __forceinline__ void note_min(unsigned long long* slot, unsigned long long v) {
+// device of a window position (absolute record index) for the expansion rules
+struct WinDev {
+  const ct_record* A;
+  const ct_record* B;
+  uint64_t wbase;
+  __device__ __forceinline__ uint32_t dev_of(uint64_t abs) const {
+    const uint32_t p = (uint32_t)(abs - wbase);
+    return (p < 32 ? A[p] : B[p - 32]).dev;
+  }
+};
+
+__device__ __forceinline__ int find_slot(const WarpMem& W, uint32_t comm) {
+  int s = -1;
+#pragma unroll
+  for (int k = 0; k < kCS; k++)
+    if (W.tag[k] == comm) s = k;
+  return s;
+}
+
+// no set bit in [lo, lo + len) of a 64-bit window mask (lo + len <= 64)
+__device__ __forceinline__ bool range_clear(unsigned long long mask64, uint32_t lo, uint32_t len) {
+  if (len == 0) return true;
+  const unsigned long long m = len >= 64 ? ~0ull : ((1ull << len) - 1);
+  return ((mask64 >> lo) & m) == 0;
+}
+
+__device__ __forceinline__ void note_min_smem(unsigned long long* slot, unsigned long long v) {
   if (v < *slot) atomicMin(slot, v);
 }
 
 }  // namespace
 
 size_t fast_smem_bytes(int g2, int smem_hist) {
-  size_t b = sizeof(SmemFixed);
+  size_t b = sizeof(WarpMem) * kWarps + sizeof(CtaMem);
   if (smem_hist) b += (size_t)kTypes * g2 * g2 * (sizeof(unsigned long long) + sizeof(unsigned int));
   return b;
 }
 
 __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  SmemFixed& S = *reinterpret_cast<SmemFixed*>(smem_raw);
+  WarpMem* WM = reinterpret_cast<WarpMem*>(smem_raw);
+  CtaMem& C = *reinterpret_cast<CtaMem*>(smem_raw + sizeof(WarpMem) * kWarps);
   const int ncell = kTypes * P.g2 * P.g2;
-  unsigned long long* shb = reinterpret_cast<unsigned long long*>(smem_raw + sizeof(SmemFixed));
+  unsigned long long* shb = reinterpret_cast<unsigned long long*>(smem_raw + sizeof(WarpMem) * kWarps + sizeof(CtaMem));
   unsigned int* shf = reinterpret_cast<unsigned int*>(shb + ncell);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  WarpMem& W = WM[warp];
+  const unsigned lt = (1u << lane) - 1;
+  const unsigned gt = lane == 31 ? 0u : ~((2u << lane) - 1);
 
-  const uint32_t s0 = blockIdx.x * P.subs_per_cta;
-  const uint32_t s1 = min(s0 + P.subs_per_cta, P.n_subs);
-  if (s0 >= s1) return;
-
-  // ---- init shared state
+  // ---- init
   if (P.smem_hist)
     for (int c = tid; c < ncell; c += kThreads) { shb[c] = 0; shf[c] = 0; }
-  for (int c = tid; c < kWarps * kChainW; c += kThreads) {
-    S.chain[c / kChainW][c % kChainW].key = kEmptyKey;
+  if (tid < kTypes) { C.calls[tid] = 0; C.pay_lo[tid] = 0; C.pay_hi[tid] = 0; }
+  if (tid < 3) C.copy_first[tid] = kNone;
+  if (tid < CT_NDIAG) C.diag[tid] = 0;
+  if (tid == 0) { C.flags = 0; C.max_dev = -1; }
+  if (lane < kCS) {
+    W.tag[lane] = kEmptyTag; W.sn[lane] = 0; W.sver[lane] = 0;
+    W.cfirst[lane] = kNone; W.clast[lane] = kNone;
+    for (int t = 0; t < 5; t++) W.tfirst[lane][t] = kNone;
   }
-  for (int c = tid; c < 5 * kCommSm; c += kThreads) S.tf[c / kCommSm][c % kCommSm] = kNone;
-  if (tid < kCommSm) S.cf[tid] = kNone;
-  if (tid < kTypes) { S.calls[tid] = 0; S.pay_lo[tid] = 0; S.pay_hi[tid] = 0; }
-  if (tid < 3) S.copy_first[tid] = kNone;
-  if (tid < CT_NDIAG) S.diag[tid] = 0;
-  if (tid == 0) {
-    S.flags = 0;
-    S.max_dev = -1;
-    for (int k = 0; k < kStages; k++) mbar_init(&S.mbar[k], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
+  for (int e = lane; e < kPC; e += 32) W.chan[e].key = kNone;
+  if (lane < kRing) mbar_init(&W.bar[lane], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
 
-  auto issue = [&](uint32_t sub, int stage) {
-    uint64_t first = (uint64_t)sub * kSub;
-    uint32_t cnt = (uint32_t)min((uint64_t)kSub, P.n - first);
-    mbar_expect_tx(&S.mbar[stage], cnt * (uint32_t)sizeof(ct_record));
-    bulk_load(S.ring[stage], P.recs + first, cnt * (uint32_t)sizeof(ct_record), &S.mbar[stage]);
-  };
-  if (tid == 0) {
-    for (uint32_t k = 0; k < (uint32_t)kStages && s0 + k < s1; k++) issue(s0 + k, k);
-  }
-
   Acc acc;
-  acc.init(&S, P.smem_hist ? shb : P.cells, P.smem_hist ? (void*)shf : (void*)P.freq,
-           P.smem_hist != 0, P.g2, P.gcap, P.explicit_d != 0);
+  acc.init(&C, P.smem_hist ? shb : P.cells, P.smem_hist ? (void*)shf : (void*)P.freq, P.smem_hist != 0, P.g2,
+           P.gcap, P.explicit_d != 0);
   int my_max_dev = -1;
   uint32_t n_incompat = 0, n_dupdev = 0, n_mismatch = 0;
-  unsigned long long my_copy_first[3] = {kNone, kNone, kNone};
+  unsigned long long cf0 = kNone, cf1 = kNone, cf2 = kNone;  // first record of each copy kind
+  uint32_t wflags = 0;
 
-  for (uint32_t s = s0; s < s1; s++) {
-    const uint32_t k = s - s0;
-    const int stage = k % kStages;
-    const uint64_t base = (uint64_t)s * kSub;
-    const uint32_t len = (uint32_t)min((uint64_t)kSub, P.n - base);
-    mbar_wait(&S.mbar[stage], (k / kStages) & 1);
-    View v{P.recs, S.ring[stage], base, len, P.n};
+  // ---- this warp's range, cut at element starts
+  const uint32_t gw = blockIdx.x * kWarps + warp;
+  const uint64_t NC = P.n_chunks;
+  const uint64_t c0 = NC * gw / P.total_warps, c1 = NC * (gw + 1) / P.total_warps;
+  bool bad = false;
+  const uint64_t start = c0 == 0 ? 0 : first_start(P.recs, P.n, c0 * 32, bad);
+  const uint64_t end = c1 >= NC ? P.n : first_start(P.recs, P.n, c1 * 32, bad);
+  if (bad) wflags |= F_NONCANON;
+  if (start < end && !bad) {
+    uint64_t b = start & ~31ull;
+    uint32_t carry = (uint32_t)(start - b);
+    const uint64_t last_chunk = min(NC, (end + 31) / 32 + 1);  // chunks below this may be read
+    const uint64_t k0 = b / 32;  // first chunk of the range: ring slot / mbarrier phase origin
+    uint64_t issued = k0;
+    auto issue_upto = [&](uint64_t lim) {
+      lim = min(lim, last_chunk);
+      while (issued < lim) {
+        if (lane == 0) {
+          const uint64_t first = issued * 32;
+          const uint32_t cnt = (uint32_t)min((uint64_t)32, P.n - first);
+          bulk_load(W.ring[(issued - k0) % kRing], P.recs + first, cnt * (uint32_t)sizeof(ct_record),
+                    &W.bar[(issued - k0) % kRing]);
+        }
+        issued++;
+      }
+    };
+    issue_upto(b / 32 + kRing);
 
-    // ---------------- A1: decode, local layout checks, element status
-#pragma unroll
-    for (int q = 0; q < kPer; q++) {
-      const uint32_t j = tid + q * kThreads;
-      uint8_t st = ST_NONE, elem = 0;
-      uint64_t key = 0;
-      if (j < len) {
-        const uint64_t i = base + j;
-        const Rec rc = load_shared(v.cur + j);
-        const int kind = rc.kind();
-        my_max_dev = max(my_max_dev, (int)rc.dev);
-        if (rc.comm >= P.n_comms) acc.flags |= F_COMM_RANGE | F_NONCANON;
-        if (kind == CT_KIND_COLLECTIVE) {
-          const uint32_t n = rc.nranks, r = rc.rank;
-          bool ok = r < n;
-          if (ok && r > 0) {
-            ok = i > 0;
-            if (ok) {
-              Rec p = v.get(i - 1);
-              ok = p.kind() == CT_KIND_COLLECTIVE && p.comm == rc.comm && p.nranks == n && p.rank == r - 1;
-            }
-          }
-          if (ok && r + 1 < n) {
-            ok = i + 1 < P.n;
-            if (ok) {
-              Rec q2 = v.get(i + 1);
-              ok = q2.kind() == CT_KIND_COLLECTIVE && q2.comm == rc.comm && q2.nranks == n && q2.rank == r + 1;
-            }
-          }
-          if (!ok) {
-            acc.flags |= F_NONCANON;
-          } else if (r == 0) {
-            st = head_status(v, i, rc);
-            if (st == ST_NONE) acc.flags |= F_NONCANON;
-            n_incompat += st == ST_INCOMPAT;
-            n_dupdev += st == ST_DUPDEV;
-            elem = 1;
-            key = rc.comm;
-            const unsigned long long gi = P.base + i;
-            if (rc.comm < kCommSm) note_min(&S.cf[rc.comm], gi);
-            else if (rc.comm < P.n_comms) note_min(&P.comm_first[rc.comm], gi);
-          }
-        } else if (kind == CT_KIND_SEND) {
-          bool ok = i + 1 < P.n;
-          Rec q2;
-          if (ok) {
-            q2 = v.get(i + 1);
-            ok = q2.kind() == CT_KIND_RECV && q2.comm == rc.comm && q2.rank == rc.aux && q2.aux == rc.rank;
-          }
-          if (!ok) {
-            acc.flags |= F_NONCANON;
-          } else {
-            const bool mis = q2.count != rc.count || q2.dtype() != rc.dtype();
-            st = mis ? ST_MISMATCH : ST_VALID;
-            n_mismatch += mis;
-            elem = 1;
-            key = (1ull << 63) | ((uint64_t)rc.comm << 32) | ((uint64_t)rc.rank << 16) | rc.aux;
-          }
-        } else if (kind == CT_KIND_RECV) {
-          bool ok = i > 0;
-          if (ok) {
-            Rec p = v.get(i - 1);
-            ok = p.kind() == CT_KIND_SEND && p.comm == rc.comm && p.aux == rc.rank && p.rank == rc.aux;
-          }
-          if (!ok) acc.flags |= F_NONCANON;
+    while (b + carry < end) {
+      const uint64_t k = b / 32;
+      mbar_wait(&W.bar[(k - k0) % kRing], (uint32_t)(((k - k0) / kRing) & 1));
+      const bool has_b = k + 1 < last_chunk;
+      if (has_b) mbar_wait(&W.bar[(k + 1 - k0) % kRing], (uint32_t)(((k + 1 - k0) / kRing) & 1));
+      const ct_record* A = W.ring[(k - k0) % kRing];
+      const ct_record* B = W.ring[(k + 1 - k0) % kRing];
+      const uint64_t wa = b + lane;
+
+      // ---------------- element starts in [carry, 32) below the range end
+      Rec ra{};
+      int kindA = 7;
+      if (wa < P.n) { ra = load_swz(A, lane); kindA = ra.kind(); }
+      const bool mineA = (uint32_t)lane >= carry && wa < end;
+      const bool stA = mineA && is_start(kindA, ra.rank);
+      const unsigned S = __ballot_sync(kFull, stA);
+      uint32_t len = 0;
+      if (stA) {
+        if (kindA == CT_KIND_COLLECTIVE) {
+          len = ra.nranks;
+          if (len > (uint32_t)kMaxN || len == 0) { wflags |= F_NONCANON; len = 1; }
         } else {
-          const int ck = rc.ckind();
-          if (ck != CT_CKIND_H2D) my_max_dev = max(my_max_dev, (int)rc.aux);
-          if (ck != CT_CKIND_D2H) my_max_dev = max(my_max_dev, (int)rc.aux2);
+          len = kindA == CT_KIND_SEND ? 2 : 1;
         }
       }
-      S.status[j] = st;
-      S.iselem[j] = elem;
-      S.ekey[j] = key;
-    }
-    __syncthreads();
+      const uint32_t carry_new = __reduce_max_sync(kFull, stA ? (uint32_t)max((int)(lane + len) - 32, 0) : 0u);
+      const unsigned below = S & (lt | (1u << lane));
+      const int hA = below ? 31 - __clz(below) : -1;
+      const uint32_t lenA = __shfl_sync(kFull, len, hA < 0 ? 0 : hA);
+      const bool memA = mineA && hA >= 0 && (uint32_t)lane < (uint32_t)hA + lenA;
+      if (mineA && !memA) wflags |= F_NONCANON;  // a record no element covers
+      const int hLast = S ? 31 - __clz(S) : 0;
+      const uint64_t wb = b + 32 + lane;
+      const bool memB = (uint32_t)lane < carry_new;
+      if (memB && (!has_b || wb >= P.n)) wflags |= F_NONCANON;  // element runs past the trace
+      Rec rb{};
+      if (memB && has_b) rb = load_swz(B, lane);
 
-    // ---------------- A2: compact chain elements in position order
-    {
-      const uint32_t p0 = warp * 64 + lane, p1 = p0 + 32;
-      const unsigned b0 = __ballot_sync(0xFFFFFFFFu, S.iselem[p0]);
-      const unsigned b1 = __ballot_sync(0xFFFFFFFFu, S.iselem[p1]);
-      if (lane == 0) S.warp_cnt[warp] = __popc(b0) + __popc(b1);
-      __syncthreads();
-      uint32_t off = 0, tot = 0;
-      for (int w = 0; w < kWarps; w++) {
-        uint32_t c = S.warp_cnt[w];
-        off += w < warp ? c : 0;
-        tot += c;
+      // ---------------- member checks against the element head (broadcast smem reads)
+      bool sigfA = false, sigfB = false, structf = false;
+      auto check = [&](const Rec& me, uint32_t pos, int h, bool& sigf) {
+        const Rec hd = load_shared(A + h);
+        const uint32_t off = pos - (uint32_t)h;
+        if (off == 0) return;
+        if (hd.kind() == CT_KIND_COLLECTIVE) {
+          if (me.kind() != CT_KIND_COLLECTIVE || me.comm != hd.comm || me.nranks != hd.nranks || me.rank != off)
+            structf = true;
+          else if (!same_sig(me, hd))
+            sigf = true;
+        } else if (hd.kind() == CT_KIND_SEND) {
+          if (off != 1 || me.kind() != CT_KIND_RECV || me.comm != hd.comm || me.rank != hd.aux || me.aux != hd.rank)
+            structf = true;
+        } else {
+          structf = true;  // copies have no members
+        }
+      };
+      if (memA) check(ra, (uint32_t)lane, hA, sigfA);
+      if (memB) check(rb, 32u + lane, hLast, sigfB);
+      if (__any_sync(kFull, structf)) wflags |= F_NONCANON;
+      const unsigned long long sigmask =
+          (unsigned long long)__ballot_sync(kFull, sigfA) | ((unsigned long long)__ballot_sync(kFull, sigfB) << 32);
+
+      // ---------------- heads: comm slot, in-window predecessor block of the same comm
+      const bool collA = stA && kindA == CT_KIND_COLLECTIVE;
+      const bool sendA = stA && kindA == CT_KIND_SEND;
+      const unsigned Scoll = __ballot_sync(kFull, collA);
+      const unsigned Ssend = __ballot_sync(kFull, sendA);
+      const bool keyed = collA;
+      if (sendA && ra.comm >= P.n_comms) wflags |= F_COMM_RANGE | F_NONCANON;
+      int slot = -1;
+      if (keyed) {
+        if (ra.comm >= P.n_comms) wflags |= F_COMM_RANGE | F_NONCANON;
+        slot = find_slot(W, ra.comm);
       }
-      const unsigned lt = (1u << lane) - 1;
-      if (S.iselem[p0]) S.elist[off + __popc(b0 & lt)] = (uint16_t)p0;
-      if (S.iselem[p1]) S.elist[off + __popc(b0) + __popc(b1 & lt)] = (uint16_t)p1;
-      if (tid == 0) S.ne = tot;
-    }
-    __syncthreads();
+      while (true) {  // allocate slots for unseen comms (rare, warp-serial)
+        const unsigned miss = __ballot_sync(kFull, keyed && slot < 0);
+        if (!miss) break;
+        const uint32_t cm = __shfl_sync(kFull, ra.comm, __ffs(miss) - 1);
+        int free_s = -1;
+        for (int s = kCS - 1; s >= 0; s--)
+          if (W.tag[s] == kEmptyTag) free_s = s;
+        __syncwarp();
+        if (free_s < 0) { wflags |= F_NONCANON; break; }  // more comms than slots in one range
+        if (lane == 0) W.tag[free_s] = cm;
+        __syncwarp();
+        if (keyed && slot < 0 && ra.comm == cm) slot = free_s;
+      }
+      unsigned same;
+      {
+        const uint32_t c_first = __shfl_sync(kFull, ra.comm, Scoll ? __ffs(Scoll) - 1 : 0);
+        if (__all_sync(kFull, !collA || ra.comm == c_first)) same = collA ? Scoll : 0u;
+        else same = __match_any_sync(kFull, collA ? (unsigned long long)ra.comm : (0xFFFFFFFF00000000ull | lane)) & Scoll;
+      }
+      const unsigned lowerSame = same & lt;
+      const int ph = lowerSame ? 31 - __clz(lowerSame) : -1;
+      const bool lastOfComm = collA && (same & gt) == 0;
+      const int hs = slot < 0 ? 0 : slot;
+      const bool hist = collA && slot >= 0 && W.sn[hs] != 0;
+      if (collA) {  // nranks constant per comm (grouping.py:104-108)
+        const uint32_t pn = ph >= 0 ? A[ph].nranks : (hist ? W.sn[hs] : ra.nranks);
+        if (pn != ra.nranks) wflags |= F_NONCANON;
+      }
+      const uint32_t hinfo = (uint32_t)(hs & 15) | ((uint32_t)(ph & 63) << 4) | (ph >= 0 ? 1u << 10 : 0u) |
+                             (hist ? 1u << 11 : 0u) | (hist && W.sver[hs] ? 1u << 12 : 0u) |
+                             (lastOfComm ? 1u << 13 : 0u);
+      const uint32_t infoA = __shfl_sync(kFull, hinfo, hA < 0 ? 0 : hA);
+      const uint32_t infoB = __shfl_sync(kFull, hinfo, hLast);
 
-    // ---------------- A3: chain checks, warp-partitioned by key hash
-    {
-      const uint32_t ne = S.ne;
-      ChainEntry* tab = S.chain[warp];
-      const unsigned lt = (1u << lane) - 1, gt = ~((2u << lane) - 1);
-      for (uint32_t b = 0; b < ne; b += 32) {
-        const uint32_t e = b + lane;
-        const bool act = e < ne;
-        const uint32_t pos = act ? S.elist[e] : 0;
-        const uint64_t key = act ? S.ekey[pos] : 0;
-        const uint32_t h = hash64(key);
-        const bool own = act && (h & (kWarps - 1)) == (uint32_t)warp;
-        if (!__any_sync(0xFFFFFFFFu, own)) continue;
-        const uint64_t mk = own ? key : (0x7FFFFFFF00000000ull | lane);
-        const unsigned m = __match_any_sync(0xFFFFFFFFu, mk);
-        const unsigned lower = m & lt, higher = m & gt;
-        const int src_lane = lower ? 31 - __clz(lower) : lane;
-        const uint32_t ppos = __shfl_sync(0xFFFFFFFFu, pos, src_lane);
-        const uint64_t cur = base + pos;
-        int slot = -1;
-        uint64_t pred = kNone;
-        if (own) {
-          if (lower) {
-            pred = base + ppos;
-          } else {
-            uint32_t s2 = (h >> 4) % kChainW;
-            for (int probe = 0; probe < kChainW; probe++, s2 = (s2 + 1) % kChainW) {
-              unsigned long long old = atomicCAS(reinterpret_cast<unsigned long long*>(&tab[s2].key),
-                                                 kEmptyKey, key);
-              if (old == kEmptyKey) { tab[s2].first = cur; tab[s2].last = cur; slot = s2; break; }
-              if (old == key) { pred = tab[s2].last; slot = s2; break; }
+      // ---------------- per-member seq order and device inheritance from the last block
+      bool devfA = false, devfB = false;
+      auto order_check = [&](const Rec& me, uint32_t info, bool& devf) {
+        const int s = info & 15;
+        const uint32_t r = me.rank;
+        bool have = false;
+        uint64_t pseq = 0;
+        if (info & (1u << 10)) { pseq = A[((info >> 4) & 63) + r].seq; have = true; }
+        else if (info & (1u << 11)) { pseq = W.cseq[s][r]; have = true; }
+        if (have && !(pseq < me.seq)) wflags |= F_NONCANON;  // strictly increasing per (comm, rank)
+        devf = !((info & (1u << 12)) && W.cdev[s][r] == me.dev);
+      };
+      const bool cmA = memA && kindA == CT_KIND_COLLECTIVE;
+      const bool cmB = memB && has_b && ((Scoll >> hLast) & 1) && rb.kind() == CT_KIND_COLLECTIVE;
+      if (cmA) order_check(ra, infoA, devfA);
+      if (cmB) order_check(rb, infoB, devfB);
+      const unsigned long long devmask =
+          (unsigned long long)__ballot_sync(kFull, devfA) | ((unsigned long long)__ballot_sync(kFull, devfB) << 32);
+
+      // ---------------- element status at the heads
+      uint32_t status = ST_NONE;
+      bool dist = true;
+      if (collA) {
+        const uint32_t n = ra.nranks;
+        if (!range_clear(devmask, (uint32_t)lane, n)) {
+          // pairwise-distinct devices over the members (grouping.py:156-157)
+          uint64_t seen0 = 0, seen1 = 0, seen2 = 0, seen3 = 0;
+          for (uint32_t m = 0; m < n && dist; m++) {
+            const uint32_t p = lane + m;
+            const uint32_t d = (p < 32 ? A[p] : B[p - 32]).dev;
+            if (d < 256) {
+              const uint64_t bit = 1ull << (d & 63);
+              const uint32_t wi = d >> 6;
+              const uint64_t wd = wi == 0 ? seen0 : wi == 1 ? seen1 : wi == 2 ? seen2 : seen3;
+              if (wd & bit) dist = false;
+              if (wi == 0) seen0 |= bit; else if (wi == 1) seen1 |= bit; else if (wi == 2) seen2 |= bit; else seen3 |= bit;
+            } else {
+              for (uint32_t m2 = 0; m2 < m; m2++) {
+                const uint32_t p2 = lane + m2;
+                if ((p2 < 32 ? A[p2] : B[p2 - 32]).dev == d) { dist = false; break; }
+              }
             }
-            if (slot < 0) acc.flags |= F_CHAIN_CAP | F_NONCANON;
           }
-          if (pred != kNone && !chain_ok(v, pred, cur)) acc.flags |= F_NONCANON;
         }
-        __syncwarp();
-        if (own && !higher) {
-          if (slot < 0) {
-            uint32_t s2 = (h >> 4) % kChainW;
-            for (int probe = 0; probe < kChainW; probe++, s2 = (s2 + 1) % kChainW)
-              if (tab[s2].key == key) { slot = s2; break; }
-          }
-          if (slot >= 0) tab[slot].last = cur;
-        }
-        __syncwarp();
+        const bool sig_ok = range_clear(sigmask, (uint32_t)lane + 1, n - 1);
+        status = !sig_ok ? ST_INCOMPAT : (!dist ? ST_DUPDEV : ST_VALID);
+        n_incompat += status == ST_INCOMPAT;
+        n_dupdev += status == ST_DUPDEV;
+      } else if (sendA) {
+        const Rec rv = lane + 1 < 32 ? load_shared(A + lane + 1) : load_shared(B);
+        const bool mis = rv.count != ra.count || rv.dtype() != ra.dtype();
+        status = mis ? ST_MISMATCH : ST_VALID;
+        n_mismatch += mis;
+      } else if (stA) {
+        status = ST_VALID;  // copies
       }
-    }
 
-    // ---------------- B: expansion + accumulation
-#pragma unroll
-    for (int q = 0; q < kPer; q++) {
-      const uint32_t j = tid + q * kThreads;
-      if (j >= len) continue;
-      const uint64_t i = base + j;
-      const Rec rc = load_shared(v.cur + j);
-      const int kind = rc.kind();
-      if (kind == CT_KIND_COLLECTIVE) {
-        const uint32_t r = rc.rank;
-        if (r > i || r >= rc.nranks) continue;
-        const uint64_t head = i - r;
-        uint8_t st;
-        if (head >= base) st = S.status[head - base];
-        else st = head_status(v, head, v.get(head));
-        if (st != ST_VALID) continue;
-        if (r == 0) {
-          const int t = rc.coll();
-          if (t < 5) {
-            const unsigned long long gi = P.base + i;
-            if (rc.comm < kCommSm) note_min(&S.tf[t][rc.comm], gi);
-            else if (rc.comm < P.n_comms) note_min(&P.type_comm_first[(size_t)t * P.n_comms + rc.comm], gi);
-          }
+      // ---------------- p2p order: per (comm, src, dst) channel non-decreasing send and
+      // recv seqs (decompose.py:359-361 sorts each side by seq; FIFO pairs by position)
+      if (Ssend) {
+        uint64_t key = 0xFFFFFFFF00000000ull | lane, sseq = 0, rseq = 0;
+        if (sendA) {
+          const Rec rv = lane + 1 < 32 ? load_shared(A + lane + 1) : load_shared(B);
+          key = ((uint64_t)ra.comm << 32) | ((uint64_t)ra.rank << 16) | ra.aux;
+          sseq = ra.seq;
+          rseq = rv.seq;
         }
-        acc.rec_key = (0ull << 62) | (min((unsigned long long)head, (1ull << 41) - 1) << 21) | ((unsigned long long)min(r, 1023u) << 11);
-        if ((rc.count >> 40) == 0) expand_collective<uint64_t>(P.ex, v, acc, rc, head);
-        else expand_collective<unsigned __int128>(P.ex, v, acc, rc, head);
-      } else if (kind == CT_KIND_SEND) {
-        if (S.status[j] != ST_VALID) continue;
-        const unsigned __int128 nb = (unsigned __int128)rc.count * (unsigned)dtype_width(rc.dtype());
-        acc.stat(CT_T_SENDRECV, nb);
-        acc.rec_key = (1ull << 62) | (min((unsigned long long)i, (1ull << 41) - 1) << 21);
-        const int rdev = (int)v.dev_of(i + 1);
-        if (rdev != (int)rc.dev) acc.edge(CT_T_SENDRECV, (int)rc.dev, rdev, nb);
-      } else if (kind >= CT_KIND_MEMCPY) {
-        const int ck = rc.ckind();
-        const int t = CT_T_EXPLICIT + (kind - CT_KIND_MEMCPY);
-        acc.stat(t, (unsigned __int128)rc.count);
-        acc.rec_key = (2ull << 62) | (min((unsigned long long)i, (1ull << 41) - 1) << 21);
-        acc.edge(t, ck == CT_CKIND_H2D ? -1 : (int)rc.aux, ck == CT_CKIND_D2H ? -1 : (int)rc.aux2,
-                 (unsigned __int128)rc.count);
-        const unsigned long long gi = P.base + i;
-        const int c = kind - CT_KIND_MEMCPY;
-        if (gi < my_copy_first[c]) my_copy_first[c] = gi;
+        const unsigned m = __match_any_sync(kFull, key);
+        const unsigned lower = m & lt;
+        const int pl = lower ? 31 - __clz(lower) : -1;      // in-window previous pair
+        const uint64_t ps = __shfl_sync(kFull, sseq, pl < 0 ? lane : pl);
+        const uint64_t pr = __shfl_sync(kFull, rseq, pl < 0 ? lane : pl);
+        int e = -1;
+        if (sendA && !lower) {  // first pair of the channel in this window: channel table
+          uint32_t h = (uint32_t)((key * 0x9E3779B97F4A7C15ull) >> 58) % kPC;
+          for (int probe = 0; probe < kPC; probe++, h = (h + 1) % kPC) {
+            const unsigned long long old =
+                atomicCAS(reinterpret_cast<unsigned long long*>(&W.chan[h].key), kNone, key);
+            if (old == kNone) {  // first pair of the channel in this range
+              W.chan[h].first_s = sseq; W.chan[h].first_r = rseq;
+              W.chan[h].last_s = sseq; W.chan[h].last_r = rseq;
+              e = (int)h;
+              break;
+            }
+            if (old == key) {
+              if (sseq < W.chan[h].last_s || rseq < W.chan[h].last_r) wflags |= F_NONCANON;
+              e = (int)h;
+              break;
+            }
+          }
+          if (e < 0) wflags |= F_NONCANON;  // more channels than the table holds
+        }
+        if (sendA && pl >= 0 && (sseq < ps || rseq < pr)) wflags |= F_NONCANON;
+        const int e_grp = __shfl_sync(kFull, e, sendA ? __ffs(m) - 1 : lane);
+        __syncwarp();
+        if (sendA && (m & gt) == 0 && e_grp >= 0) { W.chan[e_grp].last_s = sseq; W.chan[e_grp].last_r = rseq; }
+        __syncwarp();
       }
-    }
-    __syncthreads();  // everyone done with this stage
-    if (tid == 0 && s + kStages < s1) {
+
+      // ---------------- table update with the last block of each comm in the window
+      const uint32_t sinfo = status | (dist ? 0x100u : 0u);
+      const uint32_t stA_m = __shfl_sync(kFull, sinfo, hA < 0 ? 0 : hA);
+      const uint32_t stB_m = __shfl_sync(kFull, sinfo, hLast);
+      __syncwarp();
+      if (cmA && (infoA & (1u << 13))) { W.cseq[infoA & 15][ra.rank] = ra.seq; W.cdev[infoA & 15][ra.rank] = (uint16_t)ra.dev; }
+      if (cmB && (infoB & (1u << 13))) { W.cseq[infoB & 15][rb.rank] = rb.seq; W.cdev[infoB & 15][rb.rank] = (uint16_t)rb.dev; }
+      if (collA) {
+        const uint64_t gi = b + lane;
+        if (!hist && ph < 0) W.cfirst[hs] = gi;  // first block of this comm in the range
+        if (lastOfComm) { W.sn[hs] = ra.nranks; W.sver[hs] = dist; W.clast[hs] = gi; }
+        if (status == ST_VALID) note_min_smem(&W.tfirst[hs][ra.coll()], gi);
+      }
+      __syncwarp();
+
+      // ---------------- expansion + accumulation
+      const WinDev wdv{A, B, b};
+      auto expand = [&](const Rec& me, uint64_t abs, uint32_t st, int h) {
+        const int kind = me.kind();
+        my_max_dev = max(my_max_dev, (int)me.dev);
+        if (kind == CT_KIND_COLLECTIVE) {
+          if ((st & 0xFF) != ST_VALID) return;
+          const uint64_t head = b + (uint64_t)h;
+          acc.rec_key = (min((unsigned long long)head, (1ull << 41) - 1) << 21) |
+                        ((unsigned long long)min(me.rank, 1023u) << 11);
+          if ((me.count >> 40) == 0) expand_collective<uint64_t>(P.ex, wdv, acc, me, head);
+          else expand_collective<unsigned __int128>(P.ex, wdv, acc, me, head);
+        } else if (kind == CT_KIND_SEND) {
+          if ((st & 0xFF) != ST_VALID) return;
+          const unsigned __int128 nb = (unsigned __int128)me.count * (unsigned)dtype_width(me.dtype());
+          acc.stat(CT_T_SENDRECV, nb);
+          acc.rec_key = (1ull << 62) | (min((unsigned long long)abs, (1ull << 41) - 1) << 21);
+          const int rdev = (int)wdv.dev_of(abs + 1);
+          if (rdev != (int)me.dev) acc.edge(CT_T_SENDRECV, (int)me.dev, rdev, nb);
+        } else if (kind >= CT_KIND_MEMCPY) {
+          const int ck = me.ckind();
+          if (ck != CT_CKIND_H2D) my_max_dev = max(my_max_dev, (int)me.aux);
+          if (ck != CT_CKIND_D2H) my_max_dev = max(my_max_dev, (int)me.aux2);
+          const int t = CT_T_EXPLICIT + (kind - CT_KIND_MEMCPY);
+          acc.stat(t, (unsigned __int128)me.count);
+          acc.rec_key = (2ull << 62) | (min((unsigned long long)abs, (1ull << 41) - 1) << 21);
+          acc.edge(t, ck == CT_CKIND_H2D ? -1 : (int)me.aux, ck == CT_CKIND_D2H ? -1 : (int)me.aux2,
+                   (unsigned __int128)me.count);
+          if (kind == CT_KIND_MEMCPY) cf0 = min(cf0, (unsigned long long)abs);
+          else if (kind == CT_KIND_UM) cf1 = min(cf1, (unsigned long long)abs);
+          else cf2 = min(cf2, (unsigned long long)abs);
+        }
+      };
+      if (memA) expand(ra, wa, stA_m, hA);
+      if (memB && has_b) expand(rb, wb, stB_m, hLast);
+
+      // ---------------- slide the window
+      __syncwarp();
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue(s + kStages, stage);
+      issue_upto(k + 1 + kRing);  // chunk k's slot is free again
+      b += 32;
+      carry = carry_new;
     }
+    for (uint64_t q = b / 32; q < issued; q++)  // drain outstanding bulk copies
+      mbar_wait(&W.bar[(q - k0) % kRing], (uint32_t)(((q - k0) / kRing) & 1));
   }
 
-  // ---- CTA epilogue: drain caches, reduce, one global merge
+  // ---- per-warp summaries for the cross-range check and first-occurrence keys
+  __syncwarp();
+  if (lane < kCS) {
+    WarpSlot& o = P.slots[(size_t)gw * kCS + lane];
+    const uint32_t cm = W.tag[lane];
+    o.comm = cm;
+    o.n = W.sn[lane];
+    o.coll_first = W.cfirst[lane];
+    o.coll_last = W.clast[lane];
+    if (cm != kEmptyTag && cm < P.n_comms) {
+      if (W.cfirst[lane] != kNone) atomicMin(&P.comm_first[cm], W.cfirst[lane]);
+      for (int t = 0; t < 5; t++)
+        if (W.tfirst[lane][t] != kNone) atomicMin(&P.type_comm_first[(size_t)t * P.n_comms + cm], W.tfirst[lane][t]);
+    }
+  }
+  for (int e = lane; e < kPC; e += 32) P.chans[(size_t)gw * kPC + e] = W.chan[e];
+
+  // ---- CTA epilogue: drain caches, one global merge
   acc.drain();
-  atomicMax(&S.max_dev, my_max_dev);
-  if (n_incompat) atomicAdd(&S.diag[CT_DIAG_INCOMPATIBLE], n_incompat);
-  if (n_dupdev) atomicAdd(&S.diag[CT_DIAG_DUPLICATE_DEVICE], n_dupdev);
-  if (n_mismatch) atomicAdd(&S.diag[CT_DIAG_MISMATCHED_P2P], n_mismatch);
-  for (int c = 0; c < 3; c++)
-    if (my_copy_first[c] != kNone) atomicMin(&S.copy_first[c], my_copy_first[c]);
-  if (acc.flags) atomicOr(&S.flags, acc.flags);
-  if (acc.oor_key != ~0ull) atomicMin(&P.st->oor_key, acc.oor_key);
-  if (acc.of_cell != ~0ull) atomicMin(&P.st->of_cell, acc.of_cell);
+  atomicMax(&C.max_dev, my_max_dev);
+  if (n_incompat) atomicAdd(&C.diag[CT_DIAG_INCOMPATIBLE], n_incompat);
+  if (n_dupdev) atomicAdd(&C.diag[CT_DIAG_DUPLICATE_DEVICE], n_dupdev);
+  if (n_mismatch) atomicAdd(&C.diag[CT_DIAG_MISMATCHED_P2P], n_mismatch);
+  if (cf0 != kNone) atomicMin(&C.copy_first[0], cf0);
+  if (cf1 != kNone) atomicMin(&C.copy_first[1], cf1);
+  if (cf2 != kNone) atomicMin(&C.copy_first[2], cf2);
+  if (acc.flags | wflags) atomicOr(&C.flags, acc.flags | wflags);
+  if (acc.oor_key != kNone) atomicMin(&P.st->oor_key, acc.oor_key);
+  if (acc.of_cell != kNone) atomicMin(&P.st->of_cell, acc.of_cell);
   __syncthreads();
 
   GlobalState* G = P.st;
@@ -529,106 +618,64 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
     for (int c = tid; c < ncell; c += kThreads) {
       const unsigned int f = shf[c];
       if (!f) continue;
-      const unsigned long long b = shb[c];
-      unsigned long long old = atomicAdd(P.cells + c, b);
-      if (old + b < old) { of |= F_OVERFLOW; atomicMin(&G->of_cell, (unsigned long long)c); }
+      const unsigned long long bb = shb[c];
+      const unsigned long long old = atomicAdd(P.cells + c, bb);
+      if (old + bb < old) { of |= F_OVERFLOW; atomicMin(&G->of_cell, (unsigned long long)c); }
       atomicAdd(P.freq + c, (unsigned long long)f);
     }
-    if (of) atomicOr(&S.flags, of);
+    if (of) atomicOr(&C.flags, of);
   }
   if (tid < kTypes) {
-    const unsigned long long lo = S.pay_lo[tid], hi = S.pay_hi[tid], c = S.calls[tid];
+    const unsigned long long lo = C.pay_lo[tid], hi = C.pay_hi[tid], c = C.calls[tid];
     if (c) {
-      unsigned long long old = atomicAdd(&G->pay_lo[tid], lo);
+      const unsigned long long old = atomicAdd(&G->pay_lo[tid], lo);
       atomicAdd(&G->pay_hi[tid], hi + (old + lo < old ? 1ull : 0ull));
       atomicAdd(&G->calls[tid], c);
     }
   }
-  if (tid < CT_NDIAG && S.diag[tid]) atomicAdd(&G->diag[tid], (unsigned long long)S.diag[tid]);
-  if (tid < 3 && S.copy_first[tid] != kNone) atomicMin(&G->copy_first[tid], S.copy_first[tid]);
-  for (int c = tid; c < 5 * kCommSm; c += kThreads) {
-    const int t = c / kCommSm, cm = c % kCommSm;
-    if (S.tf[t][cm] != kNone && (uint32_t)cm < P.n_comms)
-      atomicMin(&P.type_comm_first[(size_t)t * P.n_comms + cm], S.tf[t][cm]);
-  }
-  if (tid < kCommSm && S.cf[tid] != kNone && (uint32_t)tid < P.n_comms)
-    atomicMin(&P.comm_first[tid], S.cf[tid]);
-  for (int c = tid; c < kWarps * kChainW; c += kThreads) {
-    const ChainEntry& e = S.chain[c / kChainW][c % kChainW];
-    if (e.key == kEmptyKey) continue;
-    uint32_t slot = atomicAdd(&G->n_chain, 1u);
-    if (slot < P.chain_cap) P.chain[slot] = e;
-    else atomicOr(&S.flags, F_CHAIN_CAP | F_NONCANON);
-  }
+  if (tid < CT_NDIAG && C.diag[tid]) atomicAdd(&G->diag[tid], (unsigned long long)C.diag[tid]);
+  if (tid < 3 && C.copy_first[tid] != kNone) atomicMin(&G->copy_first[tid], C.copy_first[tid]);
   __syncthreads();
   if (tid == 0) {
-    if (S.flags) atomicOr(&G->flags, S.flags);
-    atomicMax(&G->max_dev, S.max_dev);
+    if (C.flags) atomicOr(&G->flags, C.flags);
+    atomicMax(&G->max_dev, C.max_dev);
   }
 }
 
-// Cross-CTA chain check: entries sorted by (key, first); consecutive same-key entries
-// must satisfy chain_ok(last of earlier, first of later).
-__global__ void chain_check_kernel(const ct_record* recs, uint64_t n, const ChainEntry* chain,
-                                   const uint32_t* order, uint32_t count, GlobalState* st) {
-  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i == 0 || i >= count) return;
-  const ChainEntry& a = chain[order[i - 1]];
-  const ChainEntry& b = chain[order[i]];
-  if (a.key != b.key) return;
-  View v{recs, recs, 0, 0, n};
-  if (!chain_ok(v, a.last, b.first)) atomicOr(&st->flags, F_NONCANON);
-}
-
-}  // namespace ct
-
-namespace ct {
-
-// Cross-CTA chain check in one CTA: bitonic-sort the (key, first) list in shared memory
-// and validate consecutive same-key entries.  Lists longer than kChainSortMax set
-// F_CHAIN_BIG and the host falls back to CUB radix sorts + chain_check_kernel.
-__global__ void __launch_bounds__(1024) chain_sort_check_kernel(const ct_record* recs, uint64_t n,
-                                                                const ChainEntry* chain, GlobalState* st) {
-  extern __shared__ __align__(16) unsigned char sm[];
-  uint64_t* key = reinterpret_cast<uint64_t*>(sm);
-  uint64_t* first = key + kChainSortMax;
-  uint32_t* idx = reinterpret_cast<uint32_t*>(first + kChainSortMax);
-  const uint32_t E = st->n_chain;
-  if (E <= 1 || (st->flags & F_NONCANON)) return;
-  if (E > kChainSortMax) {
-    if (threadIdx.x == 0) atomicOr(&st->flags, F_CHAIN_BIG);
+// Cross-range seq-order check, one thread per (warp range, item): items [0, kCS) are the
+// collective comm slots (nranks equal and per-rank seq strictly increasing from the last
+// block of the nearest earlier range holding the comm to this range's first block), items
+// [kCS, kCS + kPC) the p2p channels (send and recv seqs non-decreasing across ranges).
+__global__ void range_check_kernel(const ct_record* recs, const WarpSlot* slots, const P2PEntry* chans,
+                                   uint32_t total_warps, GlobalState* st) {
+  const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  const uint32_t per = kCS + kPC;
+  if (t >= (uint64_t)total_warps * per) return;
+  const uint32_t w = (uint32_t)(t / per), item = (uint32_t)(t % per);
+  if (w == 0) return;
+  if (item < (uint32_t)kCS) {
+    const WarpSlot& me = slots[(size_t)w * kCS + item];
+    if (me.comm == kEmptyTag || me.n == 0) return;
+    for (int32_t v = (int32_t)w - 1; v >= 0; v--)
+      for (int q = 0; q < kCS; q++) {
+        const WarpSlot& o = slots[(size_t)v * kCS + q];
+        if (o.comm != me.comm || o.n == 0) continue;
+        bool ok = o.n == me.n;
+        for (uint32_t r = 0; ok && r < me.n; r++) ok = recs[o.coll_last + r].seq < recs[me.coll_first + r].seq;
+        if (!ok) atomicOr(&st->flags, F_NONCANON);
+        return;
+      }
     return;
   }
-  uint32_t P = 1;
-  while (P < E) P <<= 1;
-  for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) {
-    key[i] = i < E ? chain[i].key : ~0ull;
-    first[i] = i < E ? chain[i].first : ~0ull;
-    idx[i] = i;
-  }
-  __syncthreads();
-  for (uint32_t k = 2; k <= P; k <<= 1) {
-    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-      for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) {
-        const uint32_t l = i ^ j;
-        if (l > i) {
-          const bool up = (i & k) == 0;
-          const bool gt = key[i] > key[l] || (key[i] == key[l] && first[i] > first[l]);
-          if (gt == up) {
-            uint64_t tk = key[i]; key[i] = key[l]; key[l] = tk;
-            uint64_t tf = first[i]; first[i] = first[l]; first[l] = tf;
-            uint32_t ti = idx[i]; idx[i] = idx[l]; idx[l] = ti;
-          }
-        }
-      }
-      __syncthreads();
+  const P2PEntry& me = chans[(size_t)w * kPC + (item - kCS)];
+  if (me.key == kNone) return;
+  for (int32_t v = (int32_t)w - 1; v >= 0; v--)
+    for (int q = 0; q < kPC; q++) {
+      const P2PEntry& o = chans[(size_t)v * kPC + q];
+      if (o.key != me.key) continue;
+      if (me.first_s < o.last_s || me.first_r < o.last_r) atomicOr(&st->flags, F_NONCANON);
+      return;
     }
-  }
-  View v{recs, recs, 0, 0, n};
-  for (uint32_t i = threadIdx.x + 1; i < E; i += blockDim.x) {
-    if (key[i] != key[i - 1]) continue;
-    if (!chain_ok(v, chain[idx[i - 1]].last, chain[idx[i]].first)) atomicOr(&st->flags, F_NONCANON);
-  }
 }
 
 }  // namespace ct

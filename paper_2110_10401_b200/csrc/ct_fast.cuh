@@ -1,41 +1,37 @@
-// The fused expand + accumulate kernel (fast path) and its parameters.
+// The fused layout-check + join + expand + accumulate kernel (fast path).
 //
-// One persistent CTA per SM streams a contiguous range of the packed trace through
-// shared memory with 1-D TMA bulk copies (cp.async.bulk + mbarrier, STAGES deep).
-// Per sub-tile of SUB records:
-//   A1  decode; verify the canonical layout locally (collective records form blocks
-//       of ranks 0..n-1 on one comm; every send is followed by its recv); block heads
-//       compute instance validity (grouping.py:144-167); sends compute pair status.
-//   A2  compact chain elements (block heads, sends) in position order.
-//   A3  chain check, partitioned across warps by key hash: consecutive blocks of one
-//       comm must have strictly increasing seq per rank and equal nranks, consecutive
-//       pairs of one (comm, src, dst) channel non-decreasing seqs — exactly the
-//       conditions under which the reference's seq-sorted grouping/matching
-//       (grouping.py:118-131, decompose.py:357-361) coincides with file order.
-//   B   per-record expansion (ct_common.cuh) into a per-thread register cache of
-//       (cell, bytes, count) entries; evictions go to a shared-memory histogram.
-// At the end each CTA flushes its caches and merges its histogram and statistics into
-// global memory once.  Chain first/last elements per CTA go to a small list that
-// ct_chain_check validates across CTAs.  Any failed precondition raises F_NONCANON and
-// the host reruns through the exact (sort-based) path.
+// Warp-autonomous streaming design (no block-wide barriers in the main loop):
+//   * every warp owns a contiguous range of the packed trace, cut at element starts
+//     (a collective rank-0 record, a send, or a copy), and streams it through its own
+//     ring of 1 KB TMA bulk copies (cp.async.bulk + mbarrier, kRing slots deep);
+//   * it walks the range in 64-record windows: elements starting in the first 32
+//     positions are processed whole (n <= 32 keeps every element inside the window),
+//     the window then slides by 32 and the carry skips the records already consumed;
+//   * element structure, instance validity (signature equality, distinct devices,
+//     grouping.py:132-167), pair matching and the seq-order preconditions are decided
+//     with ballots over the window and broadcast shared-memory reads of the heads;
+//   * per-(comm, rank) state of the last block (seq, device) lives in a small per-warp
+//     table, so a block is validated against its predecessor in O(1) per record;
+//   * transfers go into a per-thread register cache and spill to a per-CTA shared
+//     histogram; each CTA merges into global memory once at the end.
+// Seq-order preconditions (exactly when the reference's seq-sorted grouping and FIFO
+// matching coincide with file order, grouping.py:118-131, decompose.py:357-361):
+//   collectives: per (comm, rank) strictly increasing seq, constant nranks per comm;
+//   p2p:         per (comm, src, dst) channel non-decreasing send seqs and recv seqs.
+// Violations (and anything else non-canonical) raise F_NONCANON; the host then runs the
+// exact sort-based join (ct_exact.cu) and feeds its canonical stream back through here.
 #pragma once
 #include "ct_expand.cuh"
 
 namespace ct {
 
-constexpr int kSub = 1024;      // records per sub-tile (32 KB)
-constexpr int kStages = 3;      // TMA ring depth
-constexpr int kThreads = 512;
+constexpr int kThreads = 512;   // 16 warps, one CTA per SM
 constexpr int kWarps = kThreads / 32;
-constexpr int kPer = kSub / kThreads;
+constexpr int kRing = 5;        // per-warp TMA ring slots of 32 records (1 KB each)
+constexpr int kCS = 8;          // collective communicator slots per warp
+constexpr int kPC = 64;         // p2p channel table entries per warp
+constexpr int kMaxN = 32;       // largest communicator the fast path handles
 constexpr int kCacheE = 4;      // register cache entries per thread
-constexpr int kChainW = 32;     // chain-table entries per warp
-constexpr int kCommSm = 64;     // comms tracked in shared memory for first-occurrence keys
-constexpr uint32_t kChainSortMax = 4096;  // single-CTA cross-CTA chain sort capacity
-
-struct ChainEntry {
-  uint64_t key, first, last;
-};
 
 struct GlobalState {
   uint32_t flags;
@@ -52,10 +48,23 @@ struct GlobalState {
   unsigned long long of_cell;   // min internal cell index whose 64-bit sum wrapped
 };
 
+// Per (warp range, comm slot) summary for the cross-range seq-order check.
+struct WarpSlot {
+  uint32_t comm;        // ~0u: unused
+  uint32_t n;           // collective nranks (0: no collectives)
+  uint64_t coll_first;  // first / last collective block head of this comm in the range
+  uint64_t coll_last;
+};
+
+// Per (warp range, p2p channel) summary: first / last send and recv seq in the range.
+struct P2PEntry {
+  uint64_t key;         // comm << 32 | src << 16 | dst; ~0: unused
+  uint64_t first_s, first_r, last_s, last_r;
+};
+
 struct FastParams {
   const ct_record* recs;      // analyzed array (device)
   uint64_t n;                 // records
-  uint64_t base;              // global index of recs[0] (multi-GPU shards)
   int gcap;                   // GPUs covered by the histogram
   int g2;                     // gcap + 2
   int explicit_d;             // 1: gcap == d, gpu >= d raises EndpointOutOfRange
@@ -67,10 +76,10 @@ struct FastParams {
   unsigned long long* freq;   // [kTypes][g2][g2]
   unsigned long long* type_comm_first;  // [5][n_comms] first valid head per (type, comm)
   unsigned long long* comm_first;       // [n_comms] first collective head per comm
-  ChainEntry* chain;          // cross-CTA chain list
-  uint32_t chain_cap;
-  uint32_t subs_per_cta;
-  uint32_t n_subs;
+  WarpSlot* slots;            // [total warps][kCS]
+  P2PEntry* chans;            // [total warps][kPC]
+  uint32_t total_warps;
+  uint64_t n_chunks;          // ceil(n / 32)
 };
 
 size_t fast_smem_bytes(int g2, int smem_hist);
