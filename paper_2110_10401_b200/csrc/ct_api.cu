@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -17,6 +18,7 @@
 #include "ct_fast.cuh"
 
 namespace ct {
+template <bool SH>
 __global__ void fast_kernel(FastParams P);
 __global__ void range_check_kernel(const ct_record* recs, const WarpSlot* slots, const P2PEntry* chans,
                                    uint32_t total_warps, GlobalState* st);
@@ -148,12 +150,14 @@ int run_fast(ct_context* c, const ct_record* recs, uint64_t n, int gcap, bool ex
   P.chans = c->chans;
   P.total_warps = total_warps;
   P.n_chunks = n_chunks;
+  P.dbg = getenv("CT_DEBUG_MODE") ? atoi(getenv("CT_DEBUG_MODE")) : 0;
   uint32_t launches = 0;  // kernels launched (cudaMemset/Memcpy are copy-engine work)
   out->ms_kernel = 0;
   if (n) {
-    CTX_TRY(c, cudaFuncSetAttribute(fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    auto kern = P.smem_hist ? fast_kernel<true> : fast_kernel<false>;
+    CTX_TRY(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     CTX_TRY(c, cudaEventRecord(c->ev[0], st));
-    fast_kernel<<<grid, kThreads, smem, st>>>(P);
+    kern<<<grid, kThreads, smem, st>>>(P);
     CTX_TRY(c, cudaGetLastError());
     CTX_TRY(c, cudaEventRecord(c->ev[1], st));
     const uint64_t threads = (uint64_t)total_warps * (kCS + kPC);

@@ -46,13 +46,33 @@ __device__ void expand_collective(const ExpandParams& P, const DevOf& v, Sink& a
   }
   if (n == 1 || s == 0) return;
   if (algo == CT_ALGO_TREE) {
+    // T1 carries ceil(S/2), T2 floor(S/2) (skipped when 0); an edge present in both
+    // trees is one transfer carrying S (decompose.py:242-255).  Scalars only, so the
+    // neighbour lists stay in registers.
     const U share1 = s - s / 2, share2 = s / 2;
-    TreeEdges te;
-    tree_edges(n, r, share2 != 0, te);
-#pragma unroll 1
-    for (int e = 0; e < te.n; e++) {
-      const U b = ((te.trees[e] & 1) ? share1 : (U)0) + ((te.trees[e] & 2) ? share2 : (U)0);
-      acc.edge(type, me, (int)v.dev_of(head + te.dst[e]), (unsigned __int128)b, te.dst[e]);
+    int a0, a1, a2, b0, b1, b2;
+    tree_links(n, r, a0, a1, a2);  // T1: rank == position
+    if (share2 != 0) {
+      int q0, q1, q2;
+      tree_links(n, r == 0 ? n - 1 : r - 1, q0, q1, q2);  // T2: rank at position q is (q + 1) % n
+      b0 = q0 < 0 ? -1 : (q0 + 1 == n ? 0 : q0 + 1);
+      b1 = q1 < 0 ? -1 : (q1 + 1 == n ? 0 : q1 + 1);
+      b2 = q2 < 0 ? -1 : (q2 + 1 == n ? 0 : q2 + 1);
+    } else {
+      b0 = b1 = b2 = -1;
+    }
+#pragma unroll
+    for (int i = 0; i < 3; i++) {
+      const int x = i == 0 ? a0 : i == 1 ? a1 : a2;
+      if (x < 0) continue;
+      const bool both = x == b0 || x == b1 || x == b2;
+      acc.edge(type, me, (int)v.dev_of(head + x), (unsigned __int128)(both ? share1 + share2 : share1), x);
+    }
+#pragma unroll
+    for (int i = 0; i < 3; i++) {
+      const int y = i == 0 ? b0 : i == 1 ? b1 : b2;
+      if (y < 0 || y == a0 || y == a1 || y == a2) continue;
+      acc.edge(type, me, (int)v.dev_of(head + y), (unsigned __int128)share2, y);
     }
     return;
   }

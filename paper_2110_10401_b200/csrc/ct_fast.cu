@@ -14,7 +14,6 @@ struct __align__(16) WarpMem {
   ct_record ring[kRing][32];                 // TMA ring: chunk k lives in slot (k - k0) % kRing
   unsigned long long bar[kRing];
   unsigned long long cseq[kCS][kMaxN];       // last collective block: seq per rank
-  P2PEntry chan[kPC];                        // p2p channels: first / last send and recv seq
   unsigned long long cfirst[kCS], clast[kCS];
   unsigned long long tfirst[kCS][5];
   uint16_t cdev[kCS][kMaxN];                 // last collective block: device per rank
@@ -95,6 +94,7 @@ __device__ uint64_t first_start(const ct_record* g, uint64_t n, uint64_t x, bool
 }
 
 // ------------------------------------------------------------ accumulation
+template <bool SH>  // SH: CTA histogram in shared memory (else global atomics)
 struct Acc {
   // two small register caches: transfer cells and per-type statistics; a miss evicts the
   // older entry into the CTA histogram (shared-memory atomics)
@@ -120,14 +120,14 @@ struct Acc {
     rec_key = 0; oor_key = kNone; of_cell = kNone;
   }
 
-  __device__ void flush_cell(uint32_t key, unsigned long long v, uint32_t c) {
+  __device__ __forceinline__ void flush_cell(uint32_t key, unsigned long long v, uint32_t c) {
     const unsigned long long old = atomicAdd(hb + key, v);
     if (old + v < old) { flags |= F_OVERFLOW; if (key < of_cell) of_cell = key; }
-    if (smem) atomicAdd(static_cast<unsigned int*>(hf) + key, c);
+    if (SH) atomicAdd(static_cast<unsigned int*>(hf) + key, c);
     else atomicAdd(static_cast<unsigned long long*>(hf) + key, (unsigned long long)c);
   }
 
-  __device__ void flush_stat(uint32_t t, unsigned long long v, uint32_t c) {
+  __device__ __forceinline__ void flush_stat(uint32_t t, unsigned long long v, uint32_t c) {
     const unsigned long long old = atomicAdd(&C->pay_lo[t], v);
     if (old + v < old) atomicAdd(&C->pay_hi[t], 1ull);
     atomicAdd(&C->calls[t], (unsigned long long)c);
@@ -164,7 +164,7 @@ struct Acc {
     }
   }
 
-  __device__ void drain() {
+  __device__ __forceinline__ void drain() {
     if (ctag[0] != kEmptyTag) flush_cell(ctag[0], csum[0], ccnt[0]);
     if (ctag[1] != kEmptyTag) flush_cell(ctag[1], csum[1], ccnt[1]);
     if (stag[0] != kEmptyTag) flush_stat(stag[0], ssum[0], scnt[0]);
@@ -175,10 +175,6 @@ struct Acc {
   // stats: calls += 1, payload += s (128-bit capable)
   __device__ __forceinline__ void stat(int type, unsigned __int128 s) {
     if ((s >> 63) == 0) { add_stat((uint32_t)type, (unsigned long long)s); return; }
-    stat_big(type, s);
-  }
-
-  __device__ __noinline__ void stat_big(int type, unsigned __int128 s) {
     const unsigned long long lo = (unsigned long long)s;
     unsigned long long hi = (unsigned long long)(s >> 64);
     const unsigned long long old = atomicAdd(&C->pay_lo[type], lo);
@@ -187,7 +183,7 @@ struct Acc {
     atomicAdd(&C->calls[type], 1ull);
   }
 
-  __device__ __noinline__ void out_of_range(unsigned long long k) {
+  __device__ __forceinline__ void out_of_range(unsigned long long k) {
     flags |= explicit_d ? F_OOR : F_CAP;
     if (k < oor_key) oor_key = k;
   }
@@ -239,6 +235,146 @@ __device__ __forceinline__ void note_min_smem(unsigned long long* slot, unsigned
   if (v < *slot) atomicMin(slot, v);
 }
 
+// Predecessor check of a non-start element member.  q0..q4 are the predecessor's words
+// (comm | nranks, rank | kc, ad, aux | count lo | count hi); w2 is the member's own kc/ad/aux.
+// Collective members must continue their block (same comm and nranks, rank + 1); the
+// signature (coll, algo, count, dtype, root; grouping.py:78-79) must match, otherwise the
+// block is incompatible.  A recv must follow its counterpart send (decompose.py:323-330);
+// count/dtype disagreement makes the pair mismatched (decompose.py:362-372).
+__device__ __forceinline__ void member_check(const Rec& me, uint32_t w2, uint32_t q0, uint32_t q1, uint32_t q2,
+                                             uint32_t q3, uint32_t q4, bool& sfail, bool& gfail, bool& mis) {
+  const int kind = me.kind();
+  const uint32_t pk = q2 & 7;
+  if (kind == CT_KIND_COLLECTIVE) {
+    if (pk != CT_KIND_COLLECTIVE || q0 != me.comm || (q1 & 0xFFFF) != me.nranks || (q1 >> 16) + 1 != me.rank) {
+      sfail = true;
+      return;
+    }
+    const uint32_t m = 0x3F78u | (me.has_root() ? 0xFFFF0000u : 0u);
+    if (((q2 ^ w2) & m) != 0 || q3 != (uint32_t)me.count || q4 != (uint32_t)(me.count >> 32)) gfail = true;
+  } else if (kind == CT_KIND_RECV) {
+    if (pk != CT_KIND_SEND || q0 != me.comm || (q1 >> 16) != me.aux || (q2 >> 16) != me.rank) {
+      sfail = true;
+      return;
+    }
+    if (q3 != (uint32_t)me.count || q4 != (uint32_t)(me.count >> 32) || ((q2 >> 10) & 15) != (uint32_t)me.dtype())
+      mis = true;
+  } else {
+    sfail = true;  // sends, copies and unknown kinds never continue an element
+  }
+}
+
+// seq order of a collective member against the same rank of the comm's previous block
+// (in-window ``pseq`` or the per-warp table) and device inheritance from the table
+__device__ __forceinline__ void order_check(const WarpMem& W, const Rec& me, uint32_t info, uint64_t pseq,
+                                            uint32_t& wflags, bool& devf) {
+  const int s = info & 15;
+  const uint32_t r = me.rank;
+  bool have = (info & (1u << 10)) != 0;
+  if (!have && (info & (1u << 11))) { pseq = W.cseq[s][r]; have = true; }
+  if (have && !(pseq < me.seq)) wflags |= F_NONCANON;  // strictly increasing per (comm, rank)
+  devf = !((info & (1u << 12)) && W.cdev[s][r] == me.dev);
+}
+
+// pairwise-distinct devices of the block of n records starting at window position h
+__device__ __noinline__ bool devices_distinct(const ct_record* A, const ct_record* B, uint32_t h, uint32_t n) {
+  uint64_t seen0 = 0, seen1 = 0, seen2 = 0, seen3 = 0;
+  for (uint32_t m = 0; m < n; m++) {
+    const uint32_t p = h + m;
+    const uint32_t d = (p < 32 ? A[p] : B[p - 32]).dev;
+    if (d < 256) {
+      const uint64_t bit = 1ull << (d & 63);
+      const uint32_t wi = d >> 6;
+      const uint64_t wd = wi == 0 ? seen0 : wi == 1 ? seen1 : wi == 2 ? seen2 : seen3;
+      if (wd & bit) return false;
+      if (wi == 0) seen0 |= bit; else if (wi == 1) seen1 |= bit; else if (wi == 2) seen2 |= bit; else seen3 |= bit;
+    } else {
+      for (uint32_t m2 = 0; m2 < m; m2++) {
+        const uint32_t p2 = h + m2;
+        if ((p2 < 32 ? A[p2] : B[p2 - 32]).dev == d) return false;
+      }
+    }
+  }
+  return true;
+}
+
+// p2p order: per (comm, src, dst) channel, send seqs and recv seqs non-decreasing in file
+// order (then FIFO-by-position pairing equals the reference's seq-sorted pairing)
+__device__ __forceinline__ void p2p_order(P2PEntry* chan, const ct_record* A, const ct_record* B, const Rec& ra,
+                                          bool sendA, int lane, unsigned lt, unsigned gt, uint32_t& wflags) {
+  uint64_t key = 0xFFFFFFFF00000000ull | lane, sseq = 0, rseq = 0;
+  if (sendA) {
+    const Rec rv = lane + 1 < 32 ? load_shared(A + lane + 1) : load_shared(B);
+    key = ((uint64_t)ra.comm << 32) | ((uint64_t)ra.rank << 16) | ra.aux;
+    sseq = ra.seq;
+    rseq = rv.seq;
+  }
+  const unsigned m = __match_any_sync(kFull, key);
+  const unsigned lower = m & lt;
+  const int pl = lower ? 31 - __clz(lower) : -1;  // in-window previous pair of the channel
+  const uint64_t ps = __shfl_sync(kFull, sseq, pl < 0 ? lane : pl);
+  const uint64_t pr = __shfl_sync(kFull, rseq, pl < 0 ? lane : pl);
+  int e = -1;
+  if (sendA && !lower) {  // first pair of the channel in this window: channel table
+    uint32_t h = (uint32_t)((key * 0x9E3779B97F4A7C15ull) >> 58) % kPC;
+    for (int probe = 0; probe < kPC; probe++, h = (h + 1) % kPC) {
+      const unsigned long long old = atomicCAS(reinterpret_cast<unsigned long long*>(&chan[h].key), kNone, key);
+      if (old == kNone) {  // first pair of the channel in this range
+        chan[h].first_s = sseq; chan[h].first_r = rseq;
+        chan[h].last_s = sseq; chan[h].last_r = rseq;
+        e = (int)h;
+        break;
+      }
+      if (old == key) {
+        if (sseq < chan[h].last_s || rseq < chan[h].last_r) wflags |= F_NONCANON;
+        e = (int)h;
+        break;
+      }
+    }
+    if (e < 0) wflags |= F_NONCANON;  // more channels than the table holds
+  }
+  if (sendA && pl >= 0 && (sseq < ps || rseq < pr)) wflags |= F_NONCANON;
+  const int e_grp = __shfl_sync(kFull, e, sendA ? __ffs(m) - 1 : lane);
+  __syncwarp();
+  if (sendA && (m & gt) == 0 && e_grp >= 0) { chan[e_grp].last_s = sseq; chan[e_grp].last_r = rseq; }
+  __syncwarp();
+}
+
+// expansion + accumulation of one record of a processed element (status ``st``)
+template <bool SH>
+__device__ __forceinline__ void expand_record(const FastParams& P, Acc<SH>& acc, const WinDev& wdv, const Rec& me,
+                                              uint64_t abs, uint32_t st, uint64_t head, int& max_dev,
+                                              unsigned long long& cf0, unsigned long long& cf1,
+                                              unsigned long long& cf2) {
+  const int kind = me.kind();
+  max_dev = max(max_dev, (int)me.dev);
+  if (kind == CT_KIND_COLLECTIVE) {
+    if (st != ST_VALID) return;
+    acc.rec_key = (min((unsigned long long)head, (1ull << 41) - 1) << 21) | ((unsigned long long)min(me.rank, 1023u) << 11);
+    if ((me.count >> 40) == 0) expand_collective<uint64_t>(P.ex, wdv, acc, me, head);
+    else expand_collective<unsigned __int128>(P.ex, wdv, acc, me, head);
+  } else if (kind == CT_KIND_SEND) {
+    if (st != ST_VALID) return;
+    const unsigned __int128 nb = (unsigned __int128)me.count * (unsigned)dtype_width(me.dtype());
+    acc.stat(CT_T_SENDRECV, nb);
+    acc.rec_key = (1ull << 62) | (min((unsigned long long)abs, (1ull << 41) - 1) << 21);
+    const int rdev = (int)wdv.dev_of(abs + 1);
+    if (rdev != (int)me.dev) acc.edge(CT_T_SENDRECV, (int)me.dev, rdev, nb);
+  } else if (kind >= CT_KIND_MEMCPY) {
+    const int ck = me.ckind();
+    if (ck != CT_CKIND_H2D) max_dev = max(max_dev, (int)me.aux);
+    if (ck != CT_CKIND_D2H) max_dev = max(max_dev, (int)me.aux2);
+    const int t = CT_T_EXPLICIT + (kind - CT_KIND_MEMCPY);
+    acc.stat(t, (unsigned __int128)me.count);
+    acc.rec_key = (2ull << 62) | (min((unsigned long long)abs, (1ull << 41) - 1) << 21);
+    acc.edge(t, ck == CT_CKIND_H2D ? -1 : (int)me.aux, ck == CT_CKIND_D2H ? -1 : (int)me.aux2,
+             (unsigned __int128)me.count);
+    if (kind == CT_KIND_MEMCPY) cf0 = min(cf0, (unsigned long long)abs);
+    else if (kind == CT_KIND_UM) cf1 = min(cf1, (unsigned long long)abs);
+    else cf2 = min(cf2, (unsigned long long)abs);
+  }
+}
+
 }  // namespace
 
 size_t fast_smem_bytes(int g2, int smem_hist) {
@@ -247,6 +383,7 @@ size_t fast_smem_bytes(int g2, int smem_hist) {
   return b;
 }
 
+template <bool SH>
 __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   WarpMem* WM = reinterpret_cast<WarpMem*>(smem_raw);
@@ -260,7 +397,7 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
   const unsigned gt = lane == 31 ? 0u : ~((2u << lane) - 1);
 
   // ---- init
-  if (P.smem_hist)
+  if (SH)
     for (int c = tid; c < ncell; c += kThreads) { shb[c] = 0; shf[c] = 0; }
   if (tid < kTypes) { C.calls[tid] = 0; C.pay_lo[tid] = 0; C.pay_hi[tid] = 0; }
   if (tid < 3) C.copy_first[tid] = kNone;
@@ -271,18 +408,21 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
     W.cfirst[lane] = kNone; W.clast[lane] = kNone;
     for (int t = 0; t < 5; t++) W.tfirst[lane][t] = kNone;
   }
-  for (int e = lane; e < kPC; e += 32) W.chan[e].key = kNone;
+  P2PEntry* chan = P.chans + (size_t)(blockIdx.x * kWarps + warp) * kPC;  // this warp's channel table
+  for (int e = lane; e < kPC; e += 32) chan[e].key = kNone;
   if (lane < kRing) mbar_init(&W.bar[lane], 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
 
-  Acc acc;
-  acc.init(&C, P.smem_hist ? shb : P.cells, P.smem_hist ? (void*)shf : (void*)P.freq, P.smem_hist != 0, P.g2,
-           P.gcap, P.explicit_d != 0);
+  Acc<SH> acc;
+  acc.init(&C, SH ? shb : P.cells, SH ? (void*)shf : (void*)P.freq, SH, P.g2, P.gcap, P.explicit_d != 0);
   int my_max_dev = -1;
   uint32_t n_incompat = 0, n_dupdev = 0, n_mismatch = 0;
   unsigned long long cf0 = kNone, cf1 = kNone, cf2 = kNone;  // first record of each copy kind
   uint32_t wflags = 0;
+  unsigned long long tf_pend = ~0ull;  // (slot, type) pairs whose first valid instance is not yet recorded
+  uint32_t sc_comm = kEmptyTag;  // last (comm, slot) pair looked up (warp-uniform)
+  int sc_slot = -1;
 
   // ---- this warp's range, cut at element starts
   const uint32_t gw = blockIdx.x * kWarps + warp;
@@ -316,7 +456,6 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
       const uint64_t k = b / 32;
       mbar_wait(&W.bar[(k - k0) % kRing], (uint32_t)(((k - k0) / kRing) & 1));
       const bool has_b = k + 1 < last_chunk;
-      if (has_b) mbar_wait(&W.bar[(k + 1 - k0) % kRing], (uint32_t)(((k + 1 - k0) / kRing) & 1));
       const ct_record* A = W.ring[(k - k0) % kRing];
       const ct_record* B = W.ring[(k + 1 - k0) % kRing];
       const uint64_t wa = b + lane;
@@ -325,255 +464,229 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
       Rec ra{};
       int kindA = 7;
       if (wa < P.n) { ra = load_swz(A, lane); kindA = ra.kind(); }
+      if (P.dbg & 4) {  // diagnostic: stream only (roofline experiments)
+        my_max_dev = max(my_max_dev, (int)(ra.dev ^ ra.rank));
+        __syncwarp();
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue_upto(k + 1 + kRing);
+        b += 32;
+        carry = 0;
+        continue;
+      }
       const bool mineA = (uint32_t)lane >= carry && wa < end;
       const bool stA = mineA && is_start(kindA, ra.rank);
+      const bool collA = stA && kindA == CT_KIND_COLLECTIVE;
+      const bool sendA = stA && kindA == CT_KIND_SEND;
       const unsigned S = __ballot_sync(kFull, stA);
+      const unsigned Scoll = __ballot_sync(kFull, collA);
+      const unsigned Ssend = __ballot_sync(kFull, sendA);
       uint32_t len = 0;
-      if (stA) {
-        if (kindA == CT_KIND_COLLECTIVE) {
-          len = ra.nranks;
-          if (len > (uint32_t)kMaxN || len == 0) { wflags |= F_NONCANON; len = 1; }
-        } else {
-          len = kindA == CT_KIND_SEND ? 2 : 1;
-        }
-      }
-      const uint32_t carry_new = __reduce_max_sync(kFull, stA ? (uint32_t)max((int)(lane + len) - 32, 0) : 0u);
+      if (stA) len = kindA == CT_KIND_COLLECTIVE ? ra.nranks : (kindA == CT_KIND_SEND ? 2u : 1u);
+      if (collA && (len > (uint32_t)kMaxN || len == 0)) { wflags |= F_NONCANON; len = 1; }
+      const int hLast = S ? 31 - __clz(S) : 0;
+      const uint32_t lenLast = __shfl_sync(kFull, len, hLast);
+      const uint32_t carry_new = S ? (uint32_t)max((int)(hLast + lenLast) - 32, 0) : 0u;
+      const bool spill = carry_new != 0;  // warp-uniform: does the last element reach into B?
+      if (spill && has_b) mbar_wait(&W.bar[(k + 1 - k0) % kRing], (uint32_t)(((k + 1 - k0) / kRing) & 1));
       const unsigned below = S & (lt | (1u << lane));
       const int hA = below ? 31 - __clz(below) : -1;
       const uint32_t lenA = __shfl_sync(kFull, len, hA < 0 ? 0 : hA);
       const bool memA = mineA && hA >= 0 && (uint32_t)lane < (uint32_t)hA + lenA;
       if (mineA && !memA) wflags |= F_NONCANON;  // a record no element covers
-      const int hLast = S ? 31 - __clz(S) : 0;
+      if (stA && !range_clear((unsigned long long)S, (uint32_t)lane + 1, len - 1))
+        wflags |= F_NONCANON;  // another element starts inside this one (e.g. a send without its recv)
       const uint64_t wb = b + 32 + lane;
-      const bool memB = (uint32_t)lane < carry_new;
+      const bool memB = spill && (uint32_t)lane < carry_new;
       if (memB && (!has_b || wb >= P.n)) wflags |= F_NONCANON;  // element runs past the trace
       Rec rb{};
       if (memB && has_b) rb = load_swz(B, lane);
 
-      // ---------------- member checks against the element head (broadcast smem reads)
-      bool sigfA = false, sigfB = false, structf = false;
-      auto check = [&](const Rec& me, uint32_t pos, int h, bool& sigf) {
-        const Rec hd = load_shared(A + h);
-        const uint32_t off = pos - (uint32_t)h;
-        if (off == 0) return;
-        if (hd.kind() == CT_KIND_COLLECTIVE) {
-          if (me.kind() != CT_KIND_COLLECTIVE || me.comm != hd.comm || me.nranks != hd.nranks || me.rank != off)
-            structf = true;
-          else if (!same_sig(me, hd))
-            sigf = true;
-        } else if (hd.kind() == CT_KIND_SEND) {
-          if (off != 1 || me.kind() != CT_KIND_RECV || me.comm != hd.comm || me.rank != hd.aux || me.aux != hd.rank)
-            structf = true;
-        } else {
-          structf = true;  // copies have no members
-        }
-      };
-      if (memA) check(ra, (uint32_t)lane, hA, sigfA);
-      if (memB) check(rb, 32u + lane, hLast, sigfB);
-      if (__any_sync(kFull, structf)) wflags |= F_NONCANON;
-      const unsigned long long sigmask =
-          (unsigned long long)__ballot_sync(kFull, sigfA) | ((unsigned long long)__ballot_sync(kFull, sigfB) << 32);
-
-      // ---------------- heads: comm slot, in-window predecessor block of the same comm
-      const bool collA = stA && kindA == CT_KIND_COLLECTIVE;
-      const bool sendA = stA && kindA == CT_KIND_SEND;
-      const unsigned Scoll = __ballot_sync(kFull, collA);
-      const unsigned Ssend = __ballot_sync(kFull, sendA);
-      const bool keyed = collA;
-      if (sendA && ra.comm >= P.n_comms) wflags |= F_COMM_RANGE | F_NONCANON;
-      int slot = -1;
-      if (keyed) {
-        if (ra.comm >= P.n_comms) wflags |= F_COMM_RANGE | F_NONCANON;
-        slot = find_slot(W, ra.comm);
-      }
-      while (true) {  // allocate slots for unseen comms (rare, warp-serial)
-        const unsigned miss = __ballot_sync(kFull, keyed && slot < 0);
-        if (!miss) break;
-        const uint32_t cm = __shfl_sync(kFull, ra.comm, __ffs(miss) - 1);
-        int free_s = -1;
-        for (int s = kCS - 1; s >= 0; s--)
-          if (W.tag[s] == kEmptyTag) free_s = s;
-        __syncwarp();
-        if (free_s < 0) { wflags |= F_NONCANON; break; }  // more comms than slots in one range
-        if (lane == 0) W.tag[free_s] = cm;
-        __syncwarp();
-        if (keyed && slot < 0 && ra.comm == cm) slot = free_s;
-      }
-      unsigned same;
+      // ---------------- member checks against the predecessor record (lane shuffles)
+      // words: comm | nranks, rank | kc, ad, aux | count lo | count hi
+      const uint32_t a0 = ra.comm, a1 = ra.nranks | (ra.rank << 16), a2 = ra.kc | (ra.ad << 8) | (ra.aux << 16);
+      const uint32_t a3 = (uint32_t)ra.count, a4 = (uint32_t)(ra.count >> 32);
+      bool sfail = false, gfailA = false, gfailB = false, misA = false, misB = false;
       {
-        const uint32_t c_first = __shfl_sync(kFull, ra.comm, Scoll ? __ffs(Scoll) - 1 : 0);
-        if (__all_sync(kFull, !collA || ra.comm == c_first)) same = collA ? Scoll : 0u;
-        else same = __match_any_sync(kFull, collA ? (unsigned long long)ra.comm : (0xFFFFFFFF00000000ull | lane)) & Scoll;
+        const uint32_t q0 = __shfl_up_sync(kFull, a0, 1), q1 = __shfl_up_sync(kFull, a1, 1);
+        const uint32_t q2 = __shfl_up_sync(kFull, a2, 1), q3 = __shfl_up_sync(kFull, a3, 1);
+        const uint32_t q4 = __shfl_up_sync(kFull, a4, 1);
+        if (memA && !stA) member_check(ra, a2, q0, q1, q2, q3, q4, sfail, gfailA, misA);
       }
-      const unsigned lowerSame = same & lt;
-      const int ph = lowerSame ? 31 - __clz(lowerSame) : -1;
-      const bool lastOfComm = collA && (same & gt) == 0;
-      const int hs = slot < 0 ? 0 : slot;
-      const bool hist = collA && slot >= 0 && W.sn[hs] != 0;
+      if (spill) {
+        const uint32_t b0 = rb.comm, b1 = rb.nranks | (rb.rank << 16), b2 = rb.kc | (rb.ad << 8) | (rb.aux << 16);
+        const uint32_t b3 = (uint32_t)rb.count, b4 = (uint32_t)(rb.count >> 32);
+        uint32_t q0 = __shfl_up_sync(kFull, b0, 1), q1 = __shfl_up_sync(kFull, b1, 1);
+        uint32_t q2 = __shfl_up_sync(kFull, b2, 1), q3 = __shfl_up_sync(kFull, b3, 1);
+        uint32_t q4 = __shfl_up_sync(kFull, b4, 1);
+        const uint32_t t0 = __shfl_sync(kFull, a0, 31), t1 = __shfl_sync(kFull, a1, 31);
+        const uint32_t t2 = __shfl_sync(kFull, a2, 31), t3 = __shfl_sync(kFull, a3, 31);
+        const uint32_t t4 = __shfl_sync(kFull, a4, 31);
+        if (lane == 0) { q0 = t0; q1 = t1; q2 = t2; q3 = t3; q4 = t4; }
+        if (memB) member_check(rb, b2, q0, q1, q2, q3, q4, sfail, gfailB, misB);
+      }
+      if (__any_sync(kFull, sfail)) wflags |= F_NONCANON;
+      const unsigned long long sigmask =
+          (unsigned long long)__ballot_sync(kFull, gfailA) | (spill ? (unsigned long long)__ballot_sync(kFull, gfailB) << 32 : 0ull);
+      const unsigned long long mismask =
+          Ssend ? ((unsigned long long)__ballot_sync(kFull, misA) | ((unsigned long long)__ballot_sync(kFull, misB) << 32)) : 0ull;
+
+      // ---------------- per-comm predecessor block, comm slot (uniform fast case)
+      const int fc = Scoll ? __ffs(Scoll) - 1 : 0;
+      const uint32_t c_first = __shfl_sync(kFull, ra.comm, fc);
+      const bool uni = __all_sync(kFull, !collA || ra.comm == c_first);
+      uint32_t infoA = 0, infoB = 0;  // slot | ph << 4 | has_ph << 10 | hist << 11 | ver << 12 | last << 13
+      int slot = -1;
+      if (uni) {
+        if (Scoll) {
+          int su = c_first == sc_comm ? sc_slot : find_slot(W, c_first);
+          if (su < 0) {  // new comm in this range
+            for (int s = kCS - 1; s >= 0; s--)
+              if (W.tag[s] == kEmptyTag) su = s;
+            __syncwarp();
+            if (su < 0) wflags |= F_NONCANON;  // more comms than slots in one range
+            else if (lane == 0) W.tag[su] = c_first;
+            __syncwarp();
+          }
+          if (c_first >= P.n_comms) wflags |= F_COMM_RANGE | F_NONCANON;
+          sc_comm = c_first;
+          sc_slot = su;
+          slot = su < 0 ? 0 : su;
+          const uint32_t base = (uint32_t)slot | (W.sn[slot] ? 1u << 11 : 0u) | (W.sn[slot] && W.sver[slot] ? 1u << 12 : 0u);
+          auto info_of = [&](int h) -> uint32_t {
+            const unsigned lower = Scoll & ((1u << h) - 1);
+            const int ph = lower ? 31 - __clz(lower) : -1;
+            const bool last = (Scoll >> h) == 1u;
+            return base | ((uint32_t)(ph & 63) << 4) | (ph >= 0 ? 1u << 10 : 0u) | (last ? 1u << 13 : 0u);
+          };
+          if (hA >= 0) infoA = info_of(hA);
+          if (spill) infoB = info_of(hLast);
+        }
+      } else {
+        // several comms start blocks in this window: per-head slots, MATCH for predecessors
+        if (collA) {
+          if (ra.comm >= P.n_comms) wflags |= F_COMM_RANGE | F_NONCANON;
+          slot = ra.comm == sc_comm ? sc_slot : find_slot(W, ra.comm);
+        }
+        while (true) {  // allocate slots for unseen comms (rare, warp-serial)
+          const unsigned miss = __ballot_sync(kFull, collA && slot < 0);
+          if (!miss) break;
+          const uint32_t cm = __shfl_sync(kFull, ra.comm, __ffs(miss) - 1);
+          int free_s = -1;
+          for (int s = kCS - 1; s >= 0; s--)
+            if (W.tag[s] == kEmptyTag) free_s = s;
+          __syncwarp();
+          if (free_s < 0) { wflags |= F_NONCANON; break; }
+          if (lane == 0) W.tag[free_s] = cm;
+          __syncwarp();
+          if (collA && slot < 0 && ra.comm == cm) slot = free_s;
+        }
+        const unsigned same =
+            __match_any_sync(kFull, collA ? (unsigned long long)ra.comm : (0xFFFFFFFF00000000ull | lane)) & Scoll;
+        const unsigned lower = same & lt;
+        const int ph = lower ? 31 - __clz(lower) : -1;
+        const int hs = slot < 0 ? 0 : slot;
+        const bool hist = collA && W.sn[hs] != 0;
+        const uint32_t hinfo = (uint32_t)hs | ((uint32_t)(ph & 63) << 4) | (ph >= 0 ? 1u << 10 : 0u) |
+                               (hist ? 1u << 11 : 0u) | (hist && W.sver[hs] ? 1u << 12 : 0u) |
+                               ((same & gt) == 0 ? 1u << 13 : 0u);
+        infoA = __shfl_sync(kFull, hinfo, hA < 0 ? 0 : hA);
+        infoB = spill ? __shfl_sync(kFull, hinfo, hLast) : 0u;
+        if (collA) slot = hs;
+      }
       if (collA) {  // nranks constant per comm (grouping.py:104-108)
-        const uint32_t pn = ph >= 0 ? A[ph].nranks : (hist ? W.sn[hs] : ra.nranks);
+        const uint32_t hi = infoA;  // a head is its own A member
+        const int s = hi & 15;
+        const uint32_t pn = (hi & (1u << 10)) ? A[(hi >> 4) & 63].nranks : ((hi & (1u << 11)) ? W.sn[s] : ra.nranks);
         if (pn != ra.nranks) wflags |= F_NONCANON;
       }
-      const uint32_t hinfo = (uint32_t)(hs & 15) | ((uint32_t)(ph & 63) << 4) | (ph >= 0 ? 1u << 10 : 0u) |
-                             (hist ? 1u << 11 : 0u) | (hist && W.sver[hs] ? 1u << 12 : 0u) |
-                             (lastOfComm ? 1u << 13 : 0u);
-      const uint32_t infoA = __shfl_sync(kFull, hinfo, hA < 0 ? 0 : hA);
-      const uint32_t infoB = __shfl_sync(kFull, hinfo, hLast);
 
       // ---------------- per-member seq order and device inheritance from the last block
+      const uint32_t sqlo = (uint32_t)ra.seq, sqhi = (uint32_t)(ra.seq >> 32);
       bool devfA = false, devfB = false;
-      auto order_check = [&](const Rec& me, uint32_t info, bool& devf) {
-        const int s = info & 15;
-        const uint32_t r = me.rank;
-        bool have = false;
-        uint64_t pseq = 0;
-        if (info & (1u << 10)) { pseq = A[((info >> 4) & 63) + r].seq; have = true; }
-        else if (info & (1u << 11)) { pseq = W.cseq[s][r]; have = true; }
-        if (have && !(pseq < me.seq)) wflags |= F_NONCANON;  // strictly increasing per (comm, rank)
-        devf = !((info & (1u << 12)) && W.cdev[s][r] == me.dev);
-      };
       const bool cmA = memA && kindA == CT_KIND_COLLECTIVE;
       const bool cmB = memB && has_b && ((Scoll >> hLast) & 1) && rb.kind() == CT_KIND_COLLECTIVE;
-      if (cmA) order_check(ra, infoA, devfA);
-      if (cmB) order_check(rb, infoB, devfB);
+      {
+        const int src = (cmA && (infoA & (1u << 10))) ? ((((infoA >> 4) & 63) + (int)ra.rank) & 31) : lane;
+        const uint64_t pseq = ((uint64_t)__shfl_sync(kFull, sqhi, src) << 32) | __shfl_sync(kFull, sqlo, src);
+        if (cmA) order_check(W, ra, infoA, pseq, wflags, devfA);
+      }
+      if (spill) {
+        const int src = (cmB && (infoB & (1u << 10))) ? ((((infoB >> 4) & 63) + (int)rb.rank) & 31) : lane;
+        const uint64_t pseq = ((uint64_t)__shfl_sync(kFull, sqhi, src) << 32) | __shfl_sync(kFull, sqlo, src);
+        if (cmB) order_check(W, rb, infoB, pseq, wflags, devfB);
+      }
       const unsigned long long devmask =
-          (unsigned long long)__ballot_sync(kFull, devfA) | ((unsigned long long)__ballot_sync(kFull, devfB) << 32);
+          (unsigned long long)__ballot_sync(kFull, devfA) | (spill ? (unsigned long long)__ballot_sync(kFull, devfB) << 32 : 0ull);
 
-      // ---------------- element status at the heads
-      uint32_t status = ST_NONE;
+      // ---------------- element status (every member derives its element's status)
+      // collective: incompatible if any member's signature differs (grouping.py:144-155),
+      // duplicate device if devices are not pairwise distinct (grouping.py:156-167)
+      const unsigned needs_full = __ballot_sync(kFull, collA && !range_clear(devmask, (uint32_t)lane, ra.nranks));
       bool dist = true;
-      if (collA) {
-        const uint32_t n = ra.nranks;
-        if (!range_clear(devmask, (uint32_t)lane, n)) {
-          // pairwise-distinct devices over the members (grouping.py:156-157)
-          uint64_t seen0 = 0, seen1 = 0, seen2 = 0, seen3 = 0;
-          for (uint32_t m = 0; m < n && dist; m++) {
-            const uint32_t p = lane + m;
-            const uint32_t d = (p < 32 ? A[p] : B[p - 32]).dev;
-            if (d < 256) {
-              const uint64_t bit = 1ull << (d & 63);
-              const uint32_t wi = d >> 6;
-              const uint64_t wd = wi == 0 ? seen0 : wi == 1 ? seen1 : wi == 2 ? seen2 : seen3;
-              if (wd & bit) dist = false;
-              if (wi == 0) seen0 |= bit; else if (wi == 1) seen1 |= bit; else if (wi == 2) seen2 |= bit; else seen3 |= bit;
-            } else {
-              for (uint32_t m2 = 0; m2 < m; m2++) {
-                const uint32_t p2 = lane + m2;
-                if ((p2 < 32 ? A[p2] : B[p2 - 32]).dev == d) { dist = false; break; }
-              }
-            }
-          }
+      if (needs_full) {  // devices changed since the comm's last block: full pairwise check
+        if ((needs_full >> lane) & 1) dist = devices_distinct(A, B, (uint32_t)lane, ra.nranks);
+      }
+      const unsigned dupmask = __ballot_sync(kFull, !dist);  // heads with duplicate devices
+      auto status_of = [&](int h, uint32_t kindh) -> uint32_t {
+        if (kindh == CT_KIND_COLLECTIVE) {
+          const uint32_t n = h == hA ? lenA : lenLast;
+          if (!range_clear(sigmask, (uint32_t)h + 1, n - 1)) return ST_INCOMPAT;
+          return ((dupmask >> h) & 1) ? ST_DUPDEV : ST_VALID;
         }
-        const bool sig_ok = range_clear(sigmask, (uint32_t)lane + 1, n - 1);
-        status = !sig_ok ? ST_INCOMPAT : (!dist ? ST_DUPDEV : ST_VALID);
-        n_incompat += status == ST_INCOMPAT;
-        n_dupdev += status == ST_DUPDEV;
-      } else if (sendA) {
-        const Rec rv = lane + 1 < 32 ? load_shared(A + lane + 1) : load_shared(B);
-        const bool mis = rv.count != ra.count || rv.dtype() != ra.dtype();
-        status = mis ? ST_MISMATCH : ST_VALID;
-        n_mismatch += mis;
-      } else if (stA) {
-        status = ST_VALID;  // copies
+        if (kindh == CT_KIND_SEND) return ((mismask >> (h + 1)) & 1) ? ST_MISMATCH : ST_VALID;
+        return ST_VALID;
+      };
+      const uint32_t kindHA = __shfl_sync(kFull, (uint32_t)kindA, hA < 0 ? 0 : hA);
+      const uint32_t kindHL = __shfl_sync(kFull, (uint32_t)kindA, hLast);
+      const uint32_t stA_m = memA ? status_of(hA, kindHA) : ST_NONE;
+      const uint32_t stB_m = memB ? status_of(hLast, kindHL) : ST_NONE;
+      if (stA) {
+        n_incompat += stA_m == ST_INCOMPAT;
+        n_dupdev += stA_m == ST_DUPDEV;
+        n_mismatch += stA_m == ST_MISMATCH;
       }
 
       // ---------------- p2p order: per (comm, src, dst) channel non-decreasing send and
       // recv seqs (decompose.py:359-361 sorts each side by seq; FIFO pairs by position)
-      if (Ssend) {
-        uint64_t key = 0xFFFFFFFF00000000ull | lane, sseq = 0, rseq = 0;
-        if (sendA) {
-          const Rec rv = lane + 1 < 32 ? load_shared(A + lane + 1) : load_shared(B);
-          key = ((uint64_t)ra.comm << 32) | ((uint64_t)ra.rank << 16) | ra.aux;
-          sseq = ra.seq;
-          rseq = rv.seq;
-        }
-        const unsigned m = __match_any_sync(kFull, key);
-        const unsigned lower = m & lt;
-        const int pl = lower ? 31 - __clz(lower) : -1;      // in-window previous pair
-        const uint64_t ps = __shfl_sync(kFull, sseq, pl < 0 ? lane : pl);
-        const uint64_t pr = __shfl_sync(kFull, rseq, pl < 0 ? lane : pl);
-        int e = -1;
-        if (sendA && !lower) {  // first pair of the channel in this window: channel table
-          uint32_t h = (uint32_t)((key * 0x9E3779B97F4A7C15ull) >> 58) % kPC;
-          for (int probe = 0; probe < kPC; probe++, h = (h + 1) % kPC) {
-            const unsigned long long old =
-                atomicCAS(reinterpret_cast<unsigned long long*>(&W.chan[h].key), kNone, key);
-            if (old == kNone) {  // first pair of the channel in this range
-              W.chan[h].first_s = sseq; W.chan[h].first_r = rseq;
-              W.chan[h].last_s = sseq; W.chan[h].last_r = rseq;
-              e = (int)h;
-              break;
-            }
-            if (old == key) {
-              if (sseq < W.chan[h].last_s || rseq < W.chan[h].last_r) wflags |= F_NONCANON;
-              e = (int)h;
-              break;
-            }
-          }
-          if (e < 0) wflags |= F_NONCANON;  // more channels than the table holds
-        }
-        if (sendA && pl >= 0 && (sseq < ps || rseq < pr)) wflags |= F_NONCANON;
-        const int e_grp = __shfl_sync(kFull, e, sendA ? __ffs(m) - 1 : lane);
-        __syncwarp();
-        if (sendA && (m & gt) == 0 && e_grp >= 0) { W.chan[e_grp].last_s = sseq; W.chan[e_grp].last_r = rseq; }
-        __syncwarp();
-      }
+      if (Ssend) p2p_order(chan, A, B, ra, sendA, lane, lt, gt, wflags);
 
       // ---------------- table update with the last block of each comm in the window
-      const uint32_t sinfo = status | (dist ? 0x100u : 0u);
-      const uint32_t stA_m = __shfl_sync(kFull, sinfo, hA < 0 ? 0 : hA);
-      const uint32_t stB_m = __shfl_sync(kFull, sinfo, hLast);
       __syncwarp();
       if (cmA && (infoA & (1u << 13))) { W.cseq[infoA & 15][ra.rank] = ra.seq; W.cdev[infoA & 15][ra.rank] = (uint16_t)ra.dev; }
       if (cmB && (infoB & (1u << 13))) { W.cseq[infoB & 15][rb.rank] = rb.seq; W.cdev[infoB & 15][rb.rank] = (uint16_t)rb.dev; }
       if (collA) {
+        const int hs = infoA & 15;
         const uint64_t gi = b + lane;
-        if (!hist && ph < 0) W.cfirst[hs] = gi;  // first block of this comm in the range
-        if (lastOfComm) { W.sn[hs] = ra.nranks; W.sver[hs] = dist; W.clast[hs] = gi; }
-        if (status == ST_VALID) note_min_smem(&W.tfirst[hs][ra.coll()], gi);
+        if (!(infoA & (3u << 10))) W.cfirst[hs] = gi;  // first block of this comm in the range
+        if (infoA & (1u << 13)) { W.sn[hs] = ra.nranks; W.sver[hs] = dist; W.clast[hs] = gi; }
+      }
+      if (Scoll) {  // first valid instance per (comm slot, type): only until recorded once
+        const unsigned long long bit = (collA && stA_m == ST_VALID) ? 1ull << ((infoA & 15) * 5 + ra.coll()) : 0ull;
+        const bool rec = (bit & tf_pend) != 0;
+        if (rec) note_min_smem(&W.tfirst[infoA & 15][ra.coll()], b + lane);
+        const unsigned lo = __reduce_or_sync(kFull, rec ? (unsigned)bit : 0u);
+        const unsigned hi = __reduce_or_sync(kFull, rec ? (unsigned)(bit >> 32) : 0u);
+        tf_pend &= ~(((unsigned long long)hi << 32) | lo);
       }
       __syncwarp();
 
       // ---------------- expansion + accumulation
       const WinDev wdv{A, B, b};
-      auto expand = [&](const Rec& me, uint64_t abs, uint32_t st, int h) {
-        const int kind = me.kind();
-        my_max_dev = max(my_max_dev, (int)me.dev);
-        if (kind == CT_KIND_COLLECTIVE) {
-          if ((st & 0xFF) != ST_VALID) return;
-          const uint64_t head = b + (uint64_t)h;
-          acc.rec_key = (min((unsigned long long)head, (1ull << 41) - 1) << 21) |
-                        ((unsigned long long)min(me.rank, 1023u) << 11);
-          if ((me.count >> 40) == 0) expand_collective<uint64_t>(P.ex, wdv, acc, me, head);
-          else expand_collective<unsigned __int128>(P.ex, wdv, acc, me, head);
-        } else if (kind == CT_KIND_SEND) {
-          if ((st & 0xFF) != ST_VALID) return;
-          const unsigned __int128 nb = (unsigned __int128)me.count * (unsigned)dtype_width(me.dtype());
-          acc.stat(CT_T_SENDRECV, nb);
-          acc.rec_key = (1ull << 62) | (min((unsigned long long)abs, (1ull << 41) - 1) << 21);
-          const int rdev = (int)wdv.dev_of(abs + 1);
-          if (rdev != (int)me.dev) acc.edge(CT_T_SENDRECV, (int)me.dev, rdev, nb);
-        } else if (kind >= CT_KIND_MEMCPY) {
-          const int ck = me.ckind();
-          if (ck != CT_CKIND_H2D) my_max_dev = max(my_max_dev, (int)me.aux);
-          if (ck != CT_CKIND_D2H) my_max_dev = max(my_max_dev, (int)me.aux2);
-          const int t = CT_T_EXPLICIT + (kind - CT_KIND_MEMCPY);
-          acc.stat(t, (unsigned __int128)me.count);
-          acc.rec_key = (2ull << 62) | (min((unsigned long long)abs, (1ull << 41) - 1) << 21);
-          acc.edge(t, ck == CT_CKIND_H2D ? -1 : (int)me.aux, ck == CT_CKIND_D2H ? -1 : (int)me.aux2,
-                   (unsigned __int128)me.count);
-          if (kind == CT_KIND_MEMCPY) cf0 = min(cf0, (unsigned long long)abs);
-          else if (kind == CT_KIND_UM) cf1 = min(cf1, (unsigned long long)abs);
-          else cf2 = min(cf2, (unsigned long long)abs);
-        }
-      };
-      if (memA) expand(ra, wa, stA_m, hA);
-      if (memB && has_b) expand(rb, wb, stB_m, hLast);
+      if (!(P.dbg & 1)) {
+        if (memA) expand_record(P, acc, wdv, ra, wa, stA_m, b + (uint64_t)hA, my_max_dev, cf0, cf1, cf2);
+        if (memB && has_b) expand_record(P, acc, wdv, rb, wb, stB_m, b + (uint64_t)hLast, my_max_dev, cf0, cf1, cf2);
+      }
 
       // ---------------- slide the window
       __syncwarp();
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue_upto(k + 1 + kRing);  // chunk k's slot is free again
+      if (k + kRing < last_chunk) {  // chunk k's slot is free again: refill it
+        if (lane == 0)
+          bulk_load(W.ring[(k - k0) % kRing], P.recs + (k + kRing) * 32,
+                    (uint32_t)min((uint64_t)32, P.n - (k + kRing) * 32) * (uint32_t)sizeof(ct_record),
+                    &W.bar[(k - k0) % kRing]);
+        issued = k + kRing + 1;
+      }
       b += 32;
       carry = carry_new;
     }
@@ -596,7 +709,6 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
         if (W.tfirst[lane][t] != kNone) atomicMin(&P.type_comm_first[(size_t)t * P.n_comms + cm], W.tfirst[lane][t]);
     }
   }
-  for (int e = lane; e < kPC; e += 32) P.chans[(size_t)gw * kPC + e] = W.chan[e];
 
   // ---- CTA epilogue: drain caches, one global merge
   acc.drain();
@@ -613,7 +725,7 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
   __syncthreads();
 
   GlobalState* G = P.st;
-  if (P.smem_hist) {
+  if (SH) {
     uint32_t of = 0;
     for (int c = tid; c < ncell; c += kThreads) {
       const unsigned int f = shf[c];
@@ -641,6 +753,9 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
     atomicMax(&G->max_dev, C.max_dev);
   }
 }
+
+template __global__ void fast_kernel<true>(FastParams);
+template __global__ void fast_kernel<false>(FastParams);
 
 // Cross-range seq-order check, one thread per (warp range, item): items [0, kCS) are the
 // collective comm slots (nranks equal and per-rank seq strictly increasing from the last

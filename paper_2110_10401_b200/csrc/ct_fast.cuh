@@ -27,7 +27,10 @@ namespace ct {
 
 constexpr int kThreads = 512;   // 16 warps, one CTA per SM
 constexpr int kWarps = kThreads / 32;
-constexpr int kRing = 5;        // per-warp TMA ring slots of 32 records (1 KB each)
+#ifndef CT_RING_SLOTS
+#define CT_RING_SLOTS 8
+#endif
+constexpr int kRing = CT_RING_SLOTS;  // per-warp TMA ring slots of 32 records (1 KB each)
 constexpr int kCS = 8;          // collective communicator slots per warp
 constexpr int kPC = 64;         // p2p channel table entries per warp
 constexpr int kMaxN = 32;       // largest communicator the fast path handles
@@ -80,6 +83,7 @@ struct FastParams {
   P2PEntry* chans;            // [total warps][kPC]
   uint32_t total_warps;
   uint64_t n_chunks;          // ceil(n / 32)
+  int dbg;                    // diagnostic knobs (CT_DEBUG_MODE): 1 skip expansion, 4 stream only
 };
 
 size_t fast_smem_bytes(int g2, int smem_hist);
