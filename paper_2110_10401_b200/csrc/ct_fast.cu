@@ -473,8 +473,10 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
         carry = 0;
         continue;
       }
-      const bool mineA = (uint32_t)lane >= carry && wa < end;
-      const bool stA = mineA && is_start(kindA, ra.rank);
+      const bool liveA = (uint32_t)lane >= carry && wa < P.n;   // not consumed by the previous window
+      const bool mineA = liveA && wa < end;                      // must be covered by this range
+      const bool anyS = liveA && is_start(kindA, ra.rank);
+      const bool stA = anyS && wa < end;
       const bool collA = stA && kindA == CT_KIND_COLLECTIVE;
       const bool sendA = stA && kindA == CT_KIND_SEND;
       const unsigned S = __ballot_sync(kFull, stA);
@@ -491,9 +493,11 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
       const unsigned below = S & (lt | (1u << lane));
       const int hA = below ? 31 - __clz(below) : -1;
       const uint32_t lenA = __shfl_sync(kFull, len, hA < 0 ? 0 : hA);
-      const bool memA = mineA && hA >= 0 && (uint32_t)lane < (uint32_t)hA + lenA;
+      const bool memA = liveA && hA >= 0 && (uint32_t)lane < (uint32_t)hA + lenA;
       if (mineA && !memA) wflags |= F_NONCANON;  // a record no element covers
-      if (stA && !range_clear((unsigned long long)S, (uint32_t)lane + 1, len - 1))
+      if (stA && wa + len > P.n) wflags |= F_NONCANON;  // element runs past the end of the trace
+      const unsigned Sall = __ballot_sync(kFull, anyS);
+      if (stA && !range_clear((unsigned long long)Sall, (uint32_t)lane + 1, len - 1))
         wflags |= F_NONCANON;  // another element starts inside this one (e.g. a send without its recv)
       const uint64_t wb = b + 32 + lane;
       const bool memB = spill && (uint32_t)lane < carry_new;

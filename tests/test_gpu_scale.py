@@ -1,0 +1,143 @@
+"""GPU parity at workload scale: the device generators' traces analysed
+on the B200 versus the C restatement of the reference (oracle/ct_oracle.c) on the same
+records, cell for cell; size-independent properties at the full C4 size; and the
+multi-GPU partial/merge path simulated as shards on one device."""
+
+import ctypes as C
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+KINDS = {"c2": (2, 1), "c3": (3, 3), "c4": (4, 1), "c5": (5, 7)}
+
+
+def _gen(kind, first, n, seed=7):
+    import torch
+    from paper_2110_10401_b200 import _lib
+    ctx = _lib.context(0)
+    buf = torch.empty(n * 32, dtype=torch.uint8, device="cuda")
+    assert ctx.lib.ct_generate(ctx.handle, kind, seed, first, n, C.c_void_p(buf.data_ptr()), None) == 0
+    return buf
+
+
+def _gpu_analyze(buf, n, n_comms, d=None, dev_hint=8, force=0):
+    from paper_2110_10401_b200 import _lib
+    ctx = _lib.context(0)
+    cfg = _lib.make_config(d=d, dev_hint=dev_hint, n_comms=n_comms, force_path=force)
+    s = _lib.CtSummary()
+    rc = ctx.lib.ct_analyze(ctx.handle, C.c_void_p(buf.data_ptr()), n, 1, C.byref(cfg), C.byref(s), None)
+    assert rc == 0, ctx.error()
+    g2 = s.g_cap + 2
+    cells = np.zeros(9 * g2 * g2, np.uint64)
+    freq = np.zeros(9 * g2 * g2, np.uint64)
+    assert ctx.lib.ct_result_cells(ctx.handle, cells.ctypes.data, freq.ctypes.data, cells.size) == 0
+    return s, cells, freq
+
+
+def _host(buf):
+    from paper_2110_10401_b200.packed import RECORD_DTYPE
+    return buf.cpu().numpy().view(RECORD_DTYPE)
+
+
+@pytest.mark.parametrize("name,n", [("c2", 10_000_000), ("c3", 2_000_000), ("c4", 2_000_000), ("c5", 2_000_000)])
+def test_generated_trace_matches_c_oracle(name, n):
+    import os
+    from oracle import c_oracle as CO
+    from paper_2110_10401_b200 import _lib
+
+    kind, n_comms = KINDS[name]
+    lib = _lib.load()
+    n = lib.ct_generate_boundary(kind, n)
+    buf = _gen(kind, 0, n)
+    s, cells, freq = _gpu_analyze(buf, n, n_comms)
+    assert s.path == 1  # the generators emit the canonical layout
+    recs = _host(buf)
+    threads = os.cpu_count() or 4
+    bounds = sorted({0, n} | {lib.ct_generate_boundary(kind, n * k // threads) for k in range(1, threads)})
+    want = CO.analyze_threads(recs, bounds, threads, gcap=s.g_cap)
+    assert want["status"] == 0
+    assert s.d == want["d"]
+    assert np.array_equal(cells.astype(object), np.array(want["cells"], dtype=object))
+    assert np.array_equal(freq, want["freq"])
+    for t in range(9):
+        assert s.calls[t] == int(want["calls"][t])
+        assert s.payload_lo[t] + (s.payload_hi[t] << 64) == want["payload"][t]
+    assert [int(x) for x in s.diag] == [int(x) for x in want["diag"]]
+
+
+def test_exact_path_equals_fast_path_at_scale():
+    buf = _gen(3, 0, 1_000_000)
+    n = 1_000_000
+    a = _gpu_analyze(buf, n, 3, force=1)
+    b = _gpu_analyze(buf, n, 3, force=2)
+    assert a[0].path == 1 and b[0].path == 2
+    assert np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2])
+    assert list(a[0].calls) == list(b[0].calls)
+
+
+def test_c4_full_size_properties():
+    """1B-record C4 is the benchmark trace; check size-independent invariants there:
+    combined == sum of types, ring conservation, closed-form instance counts."""
+    from paper_2110_10401_b200 import _lib
+    lib = _lib.load()
+    n = lib.ct_generate_boundary(4, 200_000_000)
+    buf = _gen(4, 0, n, seed=2)
+    s, cells, freq = _gpu_analyze(buf, n, 1)
+    nt, nb = C.c_uint64(), C.c_uint64()
+    bb = (C.c_uint64 * 64)()
+    lib.ct_c4_shape(C.byref(nt), C.byref(nb), bb)
+    init = 8 * nt.value
+    per_iter = 8 + 8 * nb.value
+    iters, rem = divmod(n - init, per_iter)
+    copies = 8 * iters + min(8, rem)
+    ar = iters * nb.value + max(0, rem - 8) // 8
+    assert s.calls[1] == nt.value              # one init broadcast per tensor
+    assert s.calls[0] == ar                    # allreduce instances
+    assert s.calls[6] == copies                # explicit h2d copies
+    g2 = s.g_cap + 2
+    ar_plane = cells[:g2 * g2].reshape(g2, g2)
+    # ring: every GPU sends exactly what it receives; only successor edges are used
+    for g in range(8):
+        assert ar_plane[g + 2].sum() == ar_plane[:, g + 2].sum()
+        nz = {j - 2 for j in np.nonzero(ar_plane[g + 2])[0]}
+        assert nz == {(g + 1) % 8}
+    assert s.diag[0] == s.diag[1] == s.diag[2] == 0
+
+
+def test_sharded_merge_equals_single():
+    """Multi-GPU path on one device: analyze shards, export partials, merge on device."""
+    import torch
+    from paper_2110_10401_b200 import _lib
+    lib = _lib.load()
+    ctx = _lib.context(0)
+    kind, n_comms = 3, 3
+    n = lib.ct_generate_boundary(kind, 3_000_000)
+    buf = _gen(kind, 0, n)
+    s, cells, freq = _gpu_analyze(buf, n, n_comms)
+    world = 4
+    cuts = [0] + [lib.ct_generate_boundary(kind, n * k // world) for k in range(1, world)] + [n]
+    parts = []
+    words = C.c_uint64()
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        sub = buf[a * 32:b * 32]
+        cfg = _lib.make_config(dev_hint=8, n_comms=n_comms)
+        ss = _lib.CtSummary()
+        assert ctx.lib.ct_analyze(ctx.handle, C.c_void_p(sub.data_ptr()), b - a, 1, C.byref(cfg), C.byref(ss), None) == 0
+        assert ctx.lib.ct_partial_size(ctx.handle, C.byref(words)) == 0
+        p = torch.empty(words.value, dtype=torch.int64, device="cuda")
+        assert ctx.lib.ct_partial_export(ctx.handle, C.c_void_p(p.data_ptr()), words.value, None) == 0
+        torch.cuda.synchronize()
+        parts.append(p)
+    allp = torch.cat(parts)
+    m = _lib.CtSummary()
+    rc = ctx.lib.ct_partial_merge(ctx.handle, C.c_void_p(allp.data_ptr()), world, words.value, C.byref(m), None)
+    assert rc == 0, ctx.error()
+    g2 = m.g_cap + 2
+    mc = np.zeros(9 * g2 * g2, np.uint64)
+    mf = np.zeros(9 * g2 * g2, np.uint64)
+    assert ctx.lib.ct_result_cells(ctx.handle, mc.ctypes.data, mf.ctypes.data, mc.size) == 0
+    assert np.array_equal(mc, cells) and np.array_equal(mf, freq)
+    assert list(m.calls) == list(s.calls) and list(m.diag) == list(s.diag)
+    assert m.d == s.d and list(m.type_first) == list(s.type_first)
