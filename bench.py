@@ -50,7 +50,8 @@ def parse():
     ap.add_argument("--seed", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-sample", type=int, default=2_000_000)
+    ap.add_argument("--cpu-sample", type=int, default=64_000_000)
+    ap.add_argument("--ref-sample", type=int, default=2_000_000)
     return ap.parse_args()
 
 
@@ -152,7 +153,7 @@ def run_reference(a):
     if rank != 0:
         return
     procs = os.cpu_count() or 1
-    sample = a.cpu_sample
+    sample = a.ref_sample
     for _ in range(max(a.warmup, 0) and 1):
         cpu_reference(min(sample, 80_000), procs)
     rates = []
@@ -188,15 +189,21 @@ def main():
     import torch.distributed as dist
 
     from paper_2110_10401_b200 import _lib
+    from paper_2110_10401_b200.dist import gather_partials
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    device = local % max(torch.cuda.device_count(), 1)
+    torch.cuda.set_device(device)
+    backend = os.environ.get("CT_DIST_BACKEND", "nccl")  # gloo: plumbing tests with ranks sharing a GPU
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", device))
+        else:
+            dist.init_process_group(backend)
     kind, n_comms, desc = WORKLOADS[a.workload]
-    ctx = _lib.context(local)
+    ctx = _lib.context(device)
     lib = ctx.lib
     total = lib.ct_generate_boundary(kind, a.records)
     lo = lib.ct_generate_boundary(kind, total * rank // world)
@@ -209,11 +216,13 @@ def main():
     torch.cuda.synchronize()
     cfg = _lib.make_config(d=None, dev_hint=8, n_comms=n_comms)
     summ = _lib.CtSummary()
+    merged = _lib.CtSummary()
 
-    pbuf = gbuf = None
+    pbuf = None
 
     def step(ptr, on_device):
-        nonlocal pbuf, gbuf
+        """One pass of the path over this rank's shard (+ the partial exchange)."""
+        nonlocal pbuf
         rc = lib.ct_analyze(ctx.handle, C.c_void_p(ptr), n, on_device, C.byref(cfg), C.byref(summ),
                             C.c_void_p(stream.cuda_stream))
         if rc != 0:
@@ -225,17 +234,20 @@ def main():
             lib.ct_partial_size(ctx.handle, C.byref(words))
             if pbuf is None:
                 pbuf = torch.empty(words.value, dtype=torch.int64, device="cuda")
-                gbuf = torch.empty(world * words.value, dtype=torch.int64, device="cuda")
             rc = lib.ct_partial_export(ctx.handle, C.c_void_p(pbuf.data_ptr()), words.value,
                                        C.c_void_p(stream.cuda_stream))
             assert rc == 0, ctx.error()
-            dist.all_gather_into_tensor(gbuf, pbuf)
-            m = _lib.CtSummary()
-            rc = lib.ct_partial_merge(ctx.handle, C.c_void_p(gbuf.data_ptr()), world, words.value, C.byref(m),
-                                      C.c_void_p(stream.cuda_stream))
+            launches += 2
+            if backend == "nccl":
+                gbuf = gather_partials(pbuf)
+            else:
+                torch.cuda.synchronize()
+                gbuf = gather_partials(pbuf.cpu()).cuda()
+            rc = lib.ct_partial_merge(ctx.handle, C.c_void_p(gbuf.data_ptr()), world, words.value,
+                                      C.byref(merged), C.c_void_p(stream.cuda_stream))
             if rc != 0:
                 raise RuntimeError(f"ct_partial_merge status {rc}: {ctx.error()}")
-            launches += m.n_launches
+            launches += merged.n_launches
         return ms_k, launches
 
     def timed(ptr, on_device, steps):
@@ -246,7 +258,7 @@ def main():
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         kms, launches = [], 0
-        with ClockSampler(local) as clk:
+        with ClockSampler(device) as clk:
             e0.record(stream)
             for _ in range(steps):
                 k, l = step(ptr, on_device)
@@ -257,7 +269,7 @@ def main():
         if world > 1:
             dist.barrier()
         ms = e0.elapsed_time(e1) / steps
-        t = torch.tensor([ms], device="cuda")
+        t = torch.tensor([ms], device="cuda" if backend == "nccl" else "cpu")
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item()), statistics.mean(kms), launches, clk.summary()
@@ -266,6 +278,13 @@ def main():
     value = total / (ms / 1e3)
     peak, peak_kind = peaks()
     achieved = n * RECORD_BYTES / (kms / 1e3) / 1e9 if kms else None
+    result = merged if world > 1 else summ
+    check = {"instances": int(sum(result.calls[t] for t in range(5))), "diagnostics": int(sum(result.diag)),
+             "d": int(result.d), "path": int(summ.path)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu:
+        cpu = cpu_baseline_c(buf, min(n, a.cpu_sample), kind, lib)
 
     e2e = None
     if not a.no_e2e:
@@ -275,17 +294,10 @@ def main():
         torch.cuda.empty_cache()
         e_steps = max(1, min(a.steps, 5))
         ems, _, _, _ = timed(host.data_ptr(), 0, e_steps)
-        d2h = (9 * 10 * 10 * 8 * 2 + 6 * n_comms * 8 + 512) * world
+        d2h = (2 * 9 * 10 * 10 * 8 + 6 * n_comms * 8 + 512) * world
         e2e = {"value": total / (ems / 1e3), "unit": "records/s", "h2d_bytes_per_step": total * RECORD_BYTES,
-               "d2h_bytes_per_step": d2h, "ms_per_step": ems, "steps": e_steps, "source": "pinned host"}
-
-    cpu = None
-    if rank == 0 and world == 1 and not a.no_cpu and a.workload == "c4":
-        procs = os.cpu_count() or 1
-        r, busy, ns = cpu_reference(a.cpu_sample, procs)
-        cpu = {"value": r, "unit": "records/s", "cores": procs, "kind": "port",
-               "sample": f"first {ns} C4 records, oracle/commtrace_oracle.py over {procs} processes "
-                         f"(instance-aligned shards), {busy:.1f}s of analysis"}
+               "d2h_bytes_per_step": d2h, "ms_per_step": ems, "steps": e_steps,
+               "source": "pinned host buffers through ct_analyze (H2D inside the timed region)"}
 
     if rank == 0:
         line = {
@@ -294,7 +306,7 @@ def main():
             "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "int64", "data": "synthetic",
             "config": {"workload": desc, "records": total, "record_bytes": RECORD_BYTES,
-                       "sharding": "record range, element-aligned", "l2": "inputs larger than L2 (32 GB)",
+                       "sharding": "record range, element-aligned", "l2": "inputs larger than L2 (32 GB at 1B records)",
                        "seed": a.seed},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak if achieved else None, "traffic": ncu_traffic(a.workload),
@@ -304,11 +316,30 @@ def main():
             "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clocks,
-            "path": int(summ.path),
+            "result_check": check,
         }
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
+
+
+def cpu_baseline_c(buf, sample, kind, lib):
+    """C restatement of the reference path (oracle/ct_oracle.c) on all host cores over
+    element-aligned shards of the first ``sample`` records of the same trace."""
+    from oracle import c_oracle as CO
+    from paper_2110_10401_b200.packed import RECORD_DTYPE
+
+    sample = lib.ct_generate_boundary(kind, sample)
+    recs = buf[: sample * RECORD_BYTES].cpu().numpy().view(RECORD_DTYPE)
+    threads = os.cpu_count() or 1
+    bounds = sorted({0, sample} | {lib.ct_generate_boundary(kind, sample * k // threads) for k in range(1, threads)})
+    CO.analyze_threads(recs[: min(sample, 1 << 20)], [0, min(sample, 1 << 20)], 1, gcap=8)  # warm-up
+    t0 = time.perf_counter()
+    CO.analyze_threads(recs, bounds, threads, gcap=8)
+    dt = time.perf_counter() - t0
+    return {"value": sample / dt, "unit": "records/s", "cores": threads, "kind": "port",
+            "sample": f"first {sample} records of the same trace, oracle/ct_oracle.c (C restatement of the "
+                      f"reference path) on {threads} host threads over element-aligned shards, {dt:.2f}s"}
 
 
 if __name__ == "__main__":
