@@ -63,12 +63,14 @@ def peaks():
         return 6650.0, "fallback"
 
 
-def ncu_traffic(workload):
-    """dram bytes/launch of the fast kernel from the committed ncu capture, if any."""
+def ncu_traffic(workload, records):
+    """dram bytes/launch of the fast kernel (dram__bytes_read.sum + dram__bytes_write.sum from
+    the committed ``ncu --set full`` capture, per record, scaled to this launch), if any."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as fh:
-            return json.load(fh).get(workload)
+            e = json.load(fh).get(workload)
+        return None if e is None else e["bytes_per_record"] * records
     except Exception:
         return None
 
@@ -309,7 +311,7 @@ def main():
                        "sharding": "record range, element-aligned", "l2": "inputs larger than L2 (32 GB at 1B records)",
                        "seed": a.seed},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak if achieved else None, "traffic": ncu_traffic(a.workload),
+                         "frac": achieved / peak if achieved else None, "traffic": ncu_traffic(a.workload, n),
                          "kernel": "ct::fast_kernel", "kernel_ms": kms, "peak_source": peak_kind,
                          "algorithmic_bytes_per_launch": n * RECORD_BYTES},
             "cpu_baseline": cpu,

@@ -205,15 +205,14 @@ struct Acc {
   }
 };
 
-// device of a window position (absolute record index) for the expansion rules
+constexpr uint32_t kRM = kRing * 32 - 1;  // ring index mask (kRing is a power of two)
+static_assert((kRing & (kRing - 1)) == 0, "kRing must be a power of two");
+
+// device of a trace record (absolute index) held in the warp's ring
 struct WinDev {
-  const ct_record* A;
-  const ct_record* B;
-  uint64_t wbase;
-  __device__ __forceinline__ uint32_t dev_of(uint64_t abs) const {
-    const uint32_t p = (uint32_t)(abs - wbase);
-    return (p < 32 ? A[p] : B[p - 32]).dev;
-  }
+  const ct_record* R;
+  uint64_t rb0;  // record index of ring position 0
+  __device__ __forceinline__ uint32_t dev_of(uint64_t abs) const { return R[(uint32_t)(abs - rb0) & kRM].dev; }
 };
 
 __device__ __forceinline__ int find_slot(const WarpMem& W, uint32_t comm) {
@@ -276,12 +275,11 @@ __device__ __forceinline__ void order_check(const WarpMem& W, const Rec& me, uin
   devf = !((info & (1u << 12)) && W.cdev[s][r] == me.dev);
 }
 
-// pairwise-distinct devices of the block of n records starting at window position h
-__device__ __noinline__ bool devices_distinct(const ct_record* A, const ct_record* B, uint32_t h, uint32_t n) {
+// pairwise-distinct devices of the block of n records starting at ring index i0
+__device__ __noinline__ bool devices_distinct(const ct_record* R, uint32_t i0, uint32_t n) {
   uint64_t seen0 = 0, seen1 = 0, seen2 = 0, seen3 = 0;
   for (uint32_t m = 0; m < n; m++) {
-    const uint32_t p = h + m;
-    const uint32_t d = (p < 32 ? A[p] : B[p - 32]).dev;
+    const uint32_t d = R[(i0 + m) & kRM].dev;
     if (d < 256) {
       const uint64_t bit = 1ull << (d & 63);
       const uint32_t wi = d >> 6;
@@ -289,10 +287,8 @@ __device__ __noinline__ bool devices_distinct(const ct_record* A, const ct_recor
       if (wd & bit) return false;
       if (wi == 0) seen0 |= bit; else if (wi == 1) seen1 |= bit; else if (wi == 2) seen2 |= bit; else seen3 |= bit;
     } else {
-      for (uint32_t m2 = 0; m2 < m; m2++) {
-        const uint32_t p2 = h + m2;
-        if ((p2 < 32 ? A[p2] : B[p2 - 32]).dev == d) return false;
-      }
+      for (uint32_t m2 = 0; m2 < m; m2++)
+        if (R[(i0 + m2) & kRM].dev == d) return false;
     }
   }
   return true;
@@ -300,14 +296,13 @@ __device__ __noinline__ bool devices_distinct(const ct_record* A, const ct_recor
 
 // p2p order: per (comm, src, dst) channel, send seqs and recv seqs non-decreasing in file
 // order (then FIFO-by-position pairing equals the reference's seq-sorted pairing)
-__device__ __forceinline__ void p2p_order(P2PEntry* chan, const ct_record* A, const ct_record* B, const Rec& ra,
-                                          bool sendA, int lane, unsigned lt, unsigned gt, uint32_t& wflags) {
+__device__ __forceinline__ void p2p_order(P2PEntry* chan, const Rec& ra, uint64_t next_seq, bool sendA, int lane,
+                                          unsigned lt, unsigned gt, uint32_t& wflags) {
   uint64_t key = 0xFFFFFFFF00000000ull | lane, sseq = 0, rseq = 0;
-  if (sendA) {
-    const Rec rv = lane + 1 < 32 ? load_shared(A + lane + 1) : load_shared(B);
+  if (sendA) {  // the recv is the next record (elements are whole inside a window)
     key = ((uint64_t)ra.comm << 32) | ((uint64_t)ra.rank << 16) | ra.aux;
     sseq = ra.seq;
-    rseq = rv.seq;
+    rseq = next_seq;
   }
   const unsigned m = __match_any_sync(kFull, key);
   const unsigned lower = m & lt;
@@ -433,268 +428,238 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
   const uint64_t end = c1 >= NC ? P.n : first_start(P.recs, P.n, c1 * 32, bad);
   if (bad) wflags |= F_NONCANON;
   if (start < end && !bad) {
-    uint64_t b = start & ~31ull;
-    uint32_t carry = (uint32_t)(start - b);
-    const uint64_t last_chunk = min(NC, (end + 31) / 32 + 1);  // chunks below this may be read
-    const uint64_t k0 = b / 32;  // first chunk of the range: ring slot / mbarrier phase origin
-    uint64_t issued = k0;
-    auto issue_upto = [&](uint64_t lim) {
-      lim = min(lim, last_chunk);
-      while (issued < lim) {
-        if (lane == 0) {
-          const uint64_t first = issued * 32;
-          const uint32_t cnt = (uint32_t)min((uint64_t)32, P.n - first);
-          bulk_load(W.ring[(issued - k0) % kRing], P.recs + first, cnt * (uint32_t)sizeof(ct_record),
+    // The warp slides a 32-record window over its range.  A window always begins at an
+    // element start and consumes exactly the elements that lie whole inside it (n <= 32
+    // guarantees progress); the next window begins where the last one ended.  Chunk k of
+    // the range lives in ring slot (k - k0) % kRing; a window touches at most two chunks.
+    const uint64_t k0 = start / 32;
+    const uint64_t rb0 = k0 * 32;                                  // record at ring index 0
+    const uint64_t last_chunk = min(NC, (end + 31) / 32 + 1);      // chunks below this may be read
+    const ct_record* R = &W.ring[0][0];
+    const WinDev wdv{R, rb0};
+    uint64_t issued = k0, ready = k0, freed = k0;
+    {
+      const uint64_t lim = min(k0 + kRing, last_chunk);
+      for (; issued < lim; issued++)
+        if (lane == 0)
+          bulk_load(W.ring[(issued - k0) % kRing], P.recs + issued * 32,
+                    (uint32_t)min((uint64_t)32, P.n - issued * 32) * (uint32_t)sizeof(ct_record),
                     &W.bar[(issued - k0) % kRing]);
-        }
-        issued++;
+    }
+
+    uint64_t b = start;
+    while (b < end) {
+      const uint64_t kB = min((b + 31) / 32, last_chunk - 1);
+      while (ready <= kB) {
+        mbar_wait(&W.bar[(ready - k0) % kRing], (uint32_t)(((ready - k0) / kRing) & 1));
+        ready++;
       }
-    };
-    issue_upto(b / 32 + kRing);
-
-    while (b + carry < end) {
-      const uint64_t k = b / 32;
-      mbar_wait(&W.bar[(k - k0) % kRing], (uint32_t)(((k - k0) / kRing) & 1));
-      const bool has_b = k + 1 < last_chunk;
-      const ct_record* A = W.ring[(k - k0) % kRing];
-      const ct_record* B = W.ring[(k + 1 - k0) % kRing];
-      const uint64_t wa = b + lane;
-
-      // ---------------- element starts in [carry, 32) below the range end
+      const uint32_t ri0 = (uint32_t)(b - rb0);                    // ring index of the window start
+      const uint32_t nval = (uint32_t)min((uint64_t)32, P.n - b);  // records that exist
+      const uint32_t lim = (uint32_t)min((uint64_t)32, end - b);   // heads this range owns
+      const bool valid = (uint32_t)lane < nval;
       Rec ra{};
-      int kindA = 7;
-      if (wa < P.n) { ra = load_swz(A, lane); kindA = ra.kind(); }
+      int kind = 7;
+      if (valid) { ra = load_swz(R, (ri0 + lane) & kRM); kind = ra.kind(); }
+      uint64_t nb;
       if (P.dbg & 4) {  // diagnostic: stream only (roofline experiments)
         my_max_dev = max(my_max_dev, (int)(ra.dev ^ ra.rank));
+        nb = b + 32;
+      } else {
+        // ---------------- elements: starts, lengths, whole-in-window heads, coverage
+        const bool isS = valid && is_start(kind, ra.rank);
+        uint32_t len = 0;
+        bool badl = false;
+        if (isS) {
+          len = kind == CT_KIND_COLLECTIVE ? ra.nranks : (kind == CT_KIND_SEND ? 2u : 1u);
+          if (len == 0 || len > (uint32_t)kMaxN) { badl = true; len = 1; }
+        }
+        const unsigned Sall = __ballot_sync(kFull, isS);
+        const unsigned Sown = lim >= 32 ? Sall : Sall & ((1u << lim) - 1);
+        const unsigned Inc = __ballot_sync(kFull, ((Sown >> lane) & 1) && (uint32_t)lane + len > 32);
+        const unsigned H = Inc ? Sown & ((1u << (__ffs(Inc) - 1)) - 1) : Sown;  // heads processed now
+        const bool head = (H >> lane) & 1;
+        if (!(H & 1)) badl = true;  // the window must begin with an element start
+        const int hL = H ? 31 - __clz(H) : 0;
+        const uint32_t Pw = hL + __shfl_sync(kFull, len, hL);      // records consumed
+        const bool mem = (uint32_t)lane < Pw;
+        const unsigned below = H & (lt | (1u << lane));
+        const int hA = below ? 31 - __clz(below) : 0;
+        const uint32_t lenA = __shfl_sync(kFull, len, hA);
+        if (mem && (uint32_t)lane >= (uint32_t)hA + lenA) badl = true;  // a record no element covers
+        if (head && ((uint32_t)lane + len > nval || !range_clear((unsigned long long)Sall, (uint32_t)lane + 1, len - 1)))
+          badl = true;  // runs past the trace, or another element starts inside this one
+
+        // ---------------- member checks against the predecessor record (lane shuffles)
+        // words: comm | nranks, rank | kc, ad, aux | count lo | count hi
+        const uint32_t a2 = ra.kc | (ra.ad << 8) | (ra.aux << 16);
+        bool gfail = false, mis = false;
+        {
+          const uint32_t q0 = __shfl_up_sync(kFull, ra.comm, 1);
+          const uint32_t q1 = __shfl_up_sync(kFull, ra.nranks | (ra.rank << 16), 1);
+          const uint32_t q2 = __shfl_up_sync(kFull, a2, 1);
+          const uint32_t q3 = __shfl_up_sync(kFull, (uint32_t)ra.count, 1);
+          const uint32_t q4 = __shfl_up_sync(kFull, (uint32_t)(ra.count >> 32), 1);
+          if (mem && !head) member_check(ra, a2, q0, q1, q2, q3, q4, badl, gfail, mis);
+        }
+        if (__any_sync(kFull, badl)) { wflags |= F_NONCANON; break; }  // host re-runs the exact path
+        const bool collH = head && kind == CT_KIND_COLLECTIVE;
+        const bool sendH = head && kind == CT_KIND_SEND;
+        const unsigned Hc = __ballot_sync(kFull, collH);
+        const unsigned Hs = __ballot_sync(kFull, sendH);
+        const unsigned sigmask = __ballot_sync(kFull, gfail);
+        const unsigned mismask = Hs ? __ballot_sync(kFull, mis) : 0u;
+
+        // ---------------- per-comm predecessor block, comm slot (uniform fast case)
+        uint32_t info = 0;  // slot | ph << 4 | has_ph << 10 | hist << 11 | ver << 12 | last << 13
+        if (Hc) {
+          const uint32_t c_first = __shfl_sync(kFull, ra.comm, __ffs(Hc) - 1);
+          if (__all_sync(kFull, !collH || ra.comm == c_first)) {
+            int su = c_first == sc_comm ? sc_slot : find_slot(W, c_first);
+            if (su < 0) {  // new comm in this range
+              for (int s = kCS - 1; s >= 0; s--)
+                if (W.tag[s] == kEmptyTag) su = s;
+              __syncwarp();
+              if (su < 0) wflags |= F_NONCANON;  // more comms than slots in one range
+              else if (lane == 0) W.tag[su] = c_first;
+              __syncwarp();
+            }
+            if (c_first >= P.n_comms) wflags |= F_COMM_RANGE | F_NONCANON;
+            sc_comm = c_first;
+            sc_slot = su;
+            const int slot = su < 0 ? 0 : su;
+            const uint32_t sn = W.sn[slot];
+            const uint32_t base = (uint32_t)slot | (sn ? 1u << 11 : 0u) | (sn && W.sver[slot] ? 1u << 12 : 0u);
+            const unsigned lower = Hc & ((1u << hA) - 1);
+            const int ph = lower ? 31 - __clz(lower) : -1;
+            info = base | ((uint32_t)(ph & 63) << 4) | (ph >= 0 ? 1u << 10 : 0u) | ((Hc >> hA) == 1u ? 1u << 13 : 0u);
+          } else {
+            // several comms start blocks in this window: per-head slots, MATCH for predecessors
+            int slot = -1;
+            if (collH) {
+              if (ra.comm >= P.n_comms) wflags |= F_COMM_RANGE | F_NONCANON;
+              slot = ra.comm == sc_comm ? sc_slot : find_slot(W, ra.comm);
+            }
+            while (true) {  // allocate slots for unseen comms (rare, warp-serial)
+              const unsigned miss = __ballot_sync(kFull, collH && slot < 0);
+              if (!miss) break;
+              const uint32_t cm = __shfl_sync(kFull, ra.comm, __ffs(miss) - 1);
+              int free_s = -1;
+              for (int s = kCS - 1; s >= 0; s--)
+                if (W.tag[s] == kEmptyTag) free_s = s;
+              __syncwarp();
+              if (free_s < 0) { wflags |= F_NONCANON; break; }
+              if (lane == 0) W.tag[free_s] = cm;
+              __syncwarp();
+              if (collH && slot < 0 && ra.comm == cm) slot = free_s;
+            }
+            const unsigned same =
+                __match_any_sync(kFull, collH ? (unsigned long long)ra.comm : (0xFFFFFFFF00000000ull | lane)) & Hc;
+            const unsigned lower = same & lt;
+            const int ph = lower ? 31 - __clz(lower) : -1;
+            const int hs = slot < 0 ? 0 : slot;
+            const bool hist = collH && W.sn[hs] != 0;
+            const uint32_t hinfo = (uint32_t)hs | ((uint32_t)(ph & 63) << 4) | (ph >= 0 ? 1u << 10 : 0u) |
+                                   (hist ? 1u << 11 : 0u) | (hist && W.sver[hs] ? 1u << 12 : 0u) |
+                                   ((same & gt) == 0 ? 1u << 13 : 0u);
+            info = __shfl_sync(kFull, hinfo, hA);
+          }
+        }
+        if (collH) {  // nranks constant per comm (grouping.py:104-108)
+          const uint32_t pn = (info & (1u << 10)) ? R[(ri0 + ((info >> 4) & 63)) & kRM].nranks
+                                                  : ((info & (1u << 11)) ? W.sn[info & 15] : ra.nranks);
+          if (pn != ra.nranks) wflags |= F_NONCANON;
+        }
+
+        // ---------------- per-member seq order and device inheritance from the last block
+        bool devf = false;
+        const bool cm = mem && kind == CT_KIND_COLLECTIVE;
+        {
+          const int src = (cm && (info & (1u << 10))) ? ((((info >> 4) & 63) + (int)ra.rank) & 31) : lane;
+          const uint64_t pseq = ((uint64_t)__shfl_sync(kFull, (uint32_t)(ra.seq >> 32), src) << 32) |
+                                __shfl_sync(kFull, (uint32_t)ra.seq, src);
+          if (cm) order_check(W, ra, info, pseq, wflags, devf);
+        }
+        const unsigned devmask = __ballot_sync(kFull, devf);
+
+        // ---------------- element status (every member derives its element's status)
+        // collective: incompatible if any member's signature differs (grouping.py:144-155),
+        // duplicate device if devices are not pairwise distinct (grouping.py:156-167)
+        const unsigned needs_full = __ballot_sync(kFull, collH && !range_clear(devmask, (uint32_t)lane, ra.nranks));
+        bool dist = true;
+        if (needs_full) {  // devices changed since the comm's last block: full pairwise check
+          if ((needs_full >> lane) & 1) dist = devices_distinct(R, ri0 + lane, ra.nranks);
+        }
+        const unsigned dupmask = __ballot_sync(kFull, !dist);  // heads with duplicate devices
+        const uint32_t kindH = __shfl_sync(kFull, (uint32_t)kind, hA);
+        uint32_t st = ST_NONE;
+        if (mem) {
+          if (kindH == CT_KIND_COLLECTIVE)
+            st = !range_clear(sigmask, (uint32_t)hA + 1, lenA - 1) ? ST_INCOMPAT
+                                                                   : (((dupmask >> hA) & 1) ? ST_DUPDEV : ST_VALID);
+          else if (kindH == CT_KIND_SEND)
+            st = ((mismask >> (hA + 1)) & 1) ? ST_MISMATCH : ST_VALID;
+          else
+            st = ST_VALID;
+        }
+        if (head) {
+          n_incompat += st == ST_INCOMPAT;
+          n_dupdev += st == ST_DUPDEV;
+          n_mismatch += st == ST_MISMATCH;
+        }
+
+        // ---------------- p2p order: per (comm, src, dst) channel non-decreasing send and
+        // recv seqs (decompose.py:359-361 sorts each side by seq; FIFO pairs by position)
+        if (Hs) {
+          const uint64_t nseq = ((uint64_t)__shfl_down_sync(kFull, (uint32_t)(ra.seq >> 32), 1) << 32) |
+                                __shfl_down_sync(kFull, (uint32_t)ra.seq, 1);
+          p2p_order(chan, ra, nseq, sendH, lane, lt, gt, wflags);
+        }
+
+        // ---------------- table update with the last block of each comm in the window
+        __syncwarp();
+        if (cm && (info & (1u << 13))) { W.cseq[info & 15][ra.rank] = ra.seq; W.cdev[info & 15][ra.rank] = (uint16_t)ra.dev; }
+        if (collH) {
+          const int hs = info & 15;
+          const uint64_t gi = b + lane;
+          if (!(info & (3u << 10))) W.cfirst[hs] = gi;  // first block of this comm in the range
+          if (info & (1u << 13)) { W.sn[hs] = ra.nranks; W.sver[hs] = dist; W.clast[hs] = gi; }
+        }
+        if (Hc) {  // first valid instance per (comm slot, type): only until recorded once
+          const unsigned long long bit = (collH && st == ST_VALID) ? 1ull << ((info & 15) * 5 + ra.coll()) : 0ull;
+          const bool rec = (bit & tf_pend) != 0;
+          if (rec) note_min_smem(&W.tfirst[info & 15][ra.coll()], b + lane);
+          const unsigned lo = __reduce_or_sync(kFull, rec ? (unsigned)bit : 0u);
+          const unsigned hi = __reduce_or_sync(kFull, rec ? (unsigned)(bit >> 32) : 0u);
+          tf_pend &= ~(((unsigned long long)hi << 32) | lo);
+        }
+        __syncwarp();
+
+        // ---------------- expansion + accumulation
+        if (mem && !(P.dbg & 1)) expand_record(P, acc, wdv, ra, b + lane, st, b + (uint64_t)hA, my_max_dev, cf0, cf1, cf2);
+        nb = b + Pw;
+      }
+
+      // ---------------- slide: chunks wholly behind the next window refill their slots
+      const uint64_t kf = nb / 32;
+      if (kf > freed) {
         __syncwarp();
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        issue_upto(k + 1 + kRing);
-        b += 32;
-        carry = 0;
-        continue;
-      }
-      const bool liveA = (uint32_t)lane >= carry && wa < P.n;   // not consumed by the previous window
-      const bool mineA = liveA && wa < end;                      // must be covered by this range
-      const bool anyS = liveA && is_start(kindA, ra.rank);
-      const bool stA = anyS && wa < end;
-      const bool collA = stA && kindA == CT_KIND_COLLECTIVE;
-      const bool sendA = stA && kindA == CT_KIND_SEND;
-      const unsigned S = __ballot_sync(kFull, stA);
-      const unsigned Scoll = __ballot_sync(kFull, collA);
-      const unsigned Ssend = __ballot_sync(kFull, sendA);
-      uint32_t len = 0;
-      if (stA) len = kindA == CT_KIND_COLLECTIVE ? ra.nranks : (kindA == CT_KIND_SEND ? 2u : 1u);
-      if (collA && (len > (uint32_t)kMaxN || len == 0)) { wflags |= F_NONCANON; len = 1; }
-      const int hLast = S ? 31 - __clz(S) : 0;
-      const uint32_t lenLast = __shfl_sync(kFull, len, hLast);
-      const uint32_t carry_new = S ? (uint32_t)max((int)(hLast + lenLast) - 32, 0) : 0u;
-      const bool spill = carry_new != 0;  // warp-uniform: does the last element reach into B?
-      if (spill && has_b) mbar_wait(&W.bar[(k + 1 - k0) % kRing], (uint32_t)(((k + 1 - k0) / kRing) & 1));
-      const unsigned below = S & (lt | (1u << lane));
-      const int hA = below ? 31 - __clz(below) : -1;
-      const uint32_t lenA = __shfl_sync(kFull, len, hA < 0 ? 0 : hA);
-      const bool memA = liveA && hA >= 0 && (uint32_t)lane < (uint32_t)hA + lenA;
-      if (mineA && !memA) wflags |= F_NONCANON;  // a record no element covers
-      if (stA && wa + len > P.n) wflags |= F_NONCANON;  // element runs past the end of the trace
-      const unsigned Sall = __ballot_sync(kFull, anyS);
-      if (stA && !range_clear((unsigned long long)Sall, (uint32_t)lane + 1, len - 1))
-        wflags |= F_NONCANON;  // another element starts inside this one (e.g. a send without its recv)
-      const uint64_t wb = b + 32 + lane;
-      const bool memB = spill && (uint32_t)lane < carry_new;
-      if (memB && (!has_b || wb >= P.n)) wflags |= F_NONCANON;  // element runs past the trace
-      Rec rb{};
-      if (memB && has_b) rb = load_swz(B, lane);
-
-      // ---------------- member checks against the predecessor record (lane shuffles)
-      // words: comm | nranks, rank | kc, ad, aux | count lo | count hi
-      const uint32_t a0 = ra.comm, a1 = ra.nranks | (ra.rank << 16), a2 = ra.kc | (ra.ad << 8) | (ra.aux << 16);
-      const uint32_t a3 = (uint32_t)ra.count, a4 = (uint32_t)(ra.count >> 32);
-      bool sfail = false, gfailA = false, gfailB = false, misA = false, misB = false;
-      {
-        const uint32_t q0 = __shfl_up_sync(kFull, a0, 1), q1 = __shfl_up_sync(kFull, a1, 1);
-        const uint32_t q2 = __shfl_up_sync(kFull, a2, 1), q3 = __shfl_up_sync(kFull, a3, 1);
-        const uint32_t q4 = __shfl_up_sync(kFull, a4, 1);
-        if (memA && !stA) member_check(ra, a2, q0, q1, q2, q3, q4, sfail, gfailA, misA);
-      }
-      if (spill) {
-        const uint32_t b0 = rb.comm, b1 = rb.nranks | (rb.rank << 16), b2 = rb.kc | (rb.ad << 8) | (rb.aux << 16);
-        const uint32_t b3 = (uint32_t)rb.count, b4 = (uint32_t)(rb.count >> 32);
-        uint32_t q0 = __shfl_up_sync(kFull, b0, 1), q1 = __shfl_up_sync(kFull, b1, 1);
-        uint32_t q2 = __shfl_up_sync(kFull, b2, 1), q3 = __shfl_up_sync(kFull, b3, 1);
-        uint32_t q4 = __shfl_up_sync(kFull, b4, 1);
-        const uint32_t t0 = __shfl_sync(kFull, a0, 31), t1 = __shfl_sync(kFull, a1, 31);
-        const uint32_t t2 = __shfl_sync(kFull, a2, 31), t3 = __shfl_sync(kFull, a3, 31);
-        const uint32_t t4 = __shfl_sync(kFull, a4, 31);
-        if (lane == 0) { q0 = t0; q1 = t1; q2 = t2; q3 = t3; q4 = t4; }
-        if (memB) member_check(rb, b2, q0, q1, q2, q3, q4, sfail, gfailB, misB);
-      }
-      if (__any_sync(kFull, sfail)) wflags |= F_NONCANON;
-      const unsigned long long sigmask =
-          (unsigned long long)__ballot_sync(kFull, gfailA) | (spill ? (unsigned long long)__ballot_sync(kFull, gfailB) << 32 : 0ull);
-      const unsigned long long mismask =
-          Ssend ? ((unsigned long long)__ballot_sync(kFull, misA) | ((unsigned long long)__ballot_sync(kFull, misB) << 32)) : 0ull;
-
-      // ---------------- per-comm predecessor block, comm slot (uniform fast case)
-      const int fc = Scoll ? __ffs(Scoll) - 1 : 0;
-      const uint32_t c_first = __shfl_sync(kFull, ra.comm, fc);
-      const bool uni = __all_sync(kFull, !collA || ra.comm == c_first);
-      uint32_t infoA = 0, infoB = 0;  // slot | ph << 4 | has_ph << 10 | hist << 11 | ver << 12 | last << 13
-      int slot = -1;
-      if (uni) {
-        if (Scoll) {
-          int su = c_first == sc_comm ? sc_slot : find_slot(W, c_first);
-          if (su < 0) {  // new comm in this range
-            for (int s = kCS - 1; s >= 0; s--)
-              if (W.tag[s] == kEmptyTag) su = s;
-            __syncwarp();
-            if (su < 0) wflags |= F_NONCANON;  // more comms than slots in one range
-            else if (lane == 0) W.tag[su] = c_first;
-            __syncwarp();
+        do {
+          const uint64_t q = freed + kRing;
+          if (q < last_chunk) {
+            if (lane == 0)
+              bulk_load(W.ring[(freed - k0) % kRing], P.recs + q * 32,
+                        (uint32_t)min((uint64_t)32, P.n - q * 32) * (uint32_t)sizeof(ct_record),
+                        &W.bar[(freed - k0) % kRing]);
+            issued = q + 1;
           }
-          if (c_first >= P.n_comms) wflags |= F_COMM_RANGE | F_NONCANON;
-          sc_comm = c_first;
-          sc_slot = su;
-          slot = su < 0 ? 0 : su;
-          const uint32_t base = (uint32_t)slot | (W.sn[slot] ? 1u << 11 : 0u) | (W.sn[slot] && W.sver[slot] ? 1u << 12 : 0u);
-          auto info_of = [&](int h) -> uint32_t {
-            const unsigned lower = Scoll & ((1u << h) - 1);
-            const int ph = lower ? 31 - __clz(lower) : -1;
-            const bool last = (Scoll >> h) == 1u;
-            return base | ((uint32_t)(ph & 63) << 4) | (ph >= 0 ? 1u << 10 : 0u) | (last ? 1u << 13 : 0u);
-          };
-          if (hA >= 0) infoA = info_of(hA);
-          if (spill) infoB = info_of(hLast);
-        }
-      } else {
-        // several comms start blocks in this window: per-head slots, MATCH for predecessors
-        if (collA) {
-          if (ra.comm >= P.n_comms) wflags |= F_COMM_RANGE | F_NONCANON;
-          slot = ra.comm == sc_comm ? sc_slot : find_slot(W, ra.comm);
-        }
-        while (true) {  // allocate slots for unseen comms (rare, warp-serial)
-          const unsigned miss = __ballot_sync(kFull, collA && slot < 0);
-          if (!miss) break;
-          const uint32_t cm = __shfl_sync(kFull, ra.comm, __ffs(miss) - 1);
-          int free_s = -1;
-          for (int s = kCS - 1; s >= 0; s--)
-            if (W.tag[s] == kEmptyTag) free_s = s;
-          __syncwarp();
-          if (free_s < 0) { wflags |= F_NONCANON; break; }
-          if (lane == 0) W.tag[free_s] = cm;
-          __syncwarp();
-          if (collA && slot < 0 && ra.comm == cm) slot = free_s;
-        }
-        const unsigned same =
-            __match_any_sync(kFull, collA ? (unsigned long long)ra.comm : (0xFFFFFFFF00000000ull | lane)) & Scoll;
-        const unsigned lower = same & lt;
-        const int ph = lower ? 31 - __clz(lower) : -1;
-        const int hs = slot < 0 ? 0 : slot;
-        const bool hist = collA && W.sn[hs] != 0;
-        const uint32_t hinfo = (uint32_t)hs | ((uint32_t)(ph & 63) << 4) | (ph >= 0 ? 1u << 10 : 0u) |
-                               (hist ? 1u << 11 : 0u) | (hist && W.sver[hs] ? 1u << 12 : 0u) |
-                               ((same & gt) == 0 ? 1u << 13 : 0u);
-        infoA = __shfl_sync(kFull, hinfo, hA < 0 ? 0 : hA);
-        infoB = spill ? __shfl_sync(kFull, hinfo, hLast) : 0u;
-        if (collA) slot = hs;
+          freed++;
+        } while (freed < kf);
       }
-      if (collA) {  // nranks constant per comm (grouping.py:104-108)
-        const uint32_t hi = infoA;  // a head is its own A member
-        const int s = hi & 15;
-        const uint32_t pn = (hi & (1u << 10)) ? A[(hi >> 4) & 63].nranks : ((hi & (1u << 11)) ? W.sn[s] : ra.nranks);
-        if (pn != ra.nranks) wflags |= F_NONCANON;
-      }
-
-      // ---------------- per-member seq order and device inheritance from the last block
-      const uint32_t sqlo = (uint32_t)ra.seq, sqhi = (uint32_t)(ra.seq >> 32);
-      bool devfA = false, devfB = false;
-      const bool cmA = memA && kindA == CT_KIND_COLLECTIVE;
-      const bool cmB = memB && has_b && ((Scoll >> hLast) & 1) && rb.kind() == CT_KIND_COLLECTIVE;
-      {
-        const int src = (cmA && (infoA & (1u << 10))) ? ((((infoA >> 4) & 63) + (int)ra.rank) & 31) : lane;
-        const uint64_t pseq = ((uint64_t)__shfl_sync(kFull, sqhi, src) << 32) | __shfl_sync(kFull, sqlo, src);
-        if (cmA) order_check(W, ra, infoA, pseq, wflags, devfA);
-      }
-      if (spill) {
-        const int src = (cmB && (infoB & (1u << 10))) ? ((((infoB >> 4) & 63) + (int)rb.rank) & 31) : lane;
-        const uint64_t pseq = ((uint64_t)__shfl_sync(kFull, sqhi, src) << 32) | __shfl_sync(kFull, sqlo, src);
-        if (cmB) order_check(W, rb, infoB, pseq, wflags, devfB);
-      }
-      const unsigned long long devmask =
-          (unsigned long long)__ballot_sync(kFull, devfA) | (spill ? (unsigned long long)__ballot_sync(kFull, devfB) << 32 : 0ull);
-
-      // ---------------- element status (every member derives its element's status)
-      // collective: incompatible if any member's signature differs (grouping.py:144-155),
-      // duplicate device if devices are not pairwise distinct (grouping.py:156-167)
-      const unsigned needs_full = __ballot_sync(kFull, collA && !range_clear(devmask, (uint32_t)lane, ra.nranks));
-      bool dist = true;
-      if (needs_full) {  // devices changed since the comm's last block: full pairwise check
-        if ((needs_full >> lane) & 1) dist = devices_distinct(A, B, (uint32_t)lane, ra.nranks);
-      }
-      const unsigned dupmask = __ballot_sync(kFull, !dist);  // heads with duplicate devices
-      auto status_of = [&](int h, uint32_t kindh) -> uint32_t {
-        if (kindh == CT_KIND_COLLECTIVE) {
-          const uint32_t n = h == hA ? lenA : lenLast;
-          if (!range_clear(sigmask, (uint32_t)h + 1, n - 1)) return ST_INCOMPAT;
-          return ((dupmask >> h) & 1) ? ST_DUPDEV : ST_VALID;
-        }
-        if (kindh == CT_KIND_SEND) return ((mismask >> (h + 1)) & 1) ? ST_MISMATCH : ST_VALID;
-        return ST_VALID;
-      };
-      const uint32_t kindHA = __shfl_sync(kFull, (uint32_t)kindA, hA < 0 ? 0 : hA);
-      const uint32_t kindHL = __shfl_sync(kFull, (uint32_t)kindA, hLast);
-      const uint32_t stA_m = memA ? status_of(hA, kindHA) : ST_NONE;
-      const uint32_t stB_m = memB ? status_of(hLast, kindHL) : ST_NONE;
-      if (stA) {
-        n_incompat += stA_m == ST_INCOMPAT;
-        n_dupdev += stA_m == ST_DUPDEV;
-        n_mismatch += stA_m == ST_MISMATCH;
-      }
-
-      // ---------------- p2p order: per (comm, src, dst) channel non-decreasing send and
-      // recv seqs (decompose.py:359-361 sorts each side by seq; FIFO pairs by position)
-      if (Ssend) p2p_order(chan, A, B, ra, sendA, lane, lt, gt, wflags);
-
-      // ---------------- table update with the last block of each comm in the window
-      __syncwarp();
-      if (cmA && (infoA & (1u << 13))) { W.cseq[infoA & 15][ra.rank] = ra.seq; W.cdev[infoA & 15][ra.rank] = (uint16_t)ra.dev; }
-      if (cmB && (infoB & (1u << 13))) { W.cseq[infoB & 15][rb.rank] = rb.seq; W.cdev[infoB & 15][rb.rank] = (uint16_t)rb.dev; }
-      if (collA) {
-        const int hs = infoA & 15;
-        const uint64_t gi = b + lane;
-        if (!(infoA & (3u << 10))) W.cfirst[hs] = gi;  // first block of this comm in the range
-        if (infoA & (1u << 13)) { W.sn[hs] = ra.nranks; W.sver[hs] = dist; W.clast[hs] = gi; }
-      }
-      if (Scoll) {  // first valid instance per (comm slot, type): only until recorded once
-        const unsigned long long bit = (collA && stA_m == ST_VALID) ? 1ull << ((infoA & 15) * 5 + ra.coll()) : 0ull;
-        const bool rec = (bit & tf_pend) != 0;
-        if (rec) note_min_smem(&W.tfirst[infoA & 15][ra.coll()], b + lane);
-        const unsigned lo = __reduce_or_sync(kFull, rec ? (unsigned)bit : 0u);
-        const unsigned hi = __reduce_or_sync(kFull, rec ? (unsigned)(bit >> 32) : 0u);
-        tf_pend &= ~(((unsigned long long)hi << 32) | lo);
-      }
-      __syncwarp();
-
-      // ---------------- expansion + accumulation
-      const WinDev wdv{A, B, b};
-      if (!(P.dbg & 1)) {
-        if (memA) expand_record(P, acc, wdv, ra, wa, stA_m, b + (uint64_t)hA, my_max_dev, cf0, cf1, cf2);
-        if (memB && has_b) expand_record(P, acc, wdv, rb, wb, stB_m, b + (uint64_t)hLast, my_max_dev, cf0, cf1, cf2);
-      }
-
-      // ---------------- slide the window
-      __syncwarp();
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      if (k + kRing < last_chunk) {  // chunk k's slot is free again: refill it
-        if (lane == 0)
-          bulk_load(W.ring[(k - k0) % kRing], P.recs + (k + kRing) * 32,
-                    (uint32_t)min((uint64_t)32, P.n - (k + kRing) * 32) * (uint32_t)sizeof(ct_record),
-                    &W.bar[(k - k0) % kRing]);
-        issued = k + kRing + 1;
-      }
-      b += 32;
-      carry = carry_new;
+      b = nb;
     }
-    for (uint64_t q = b / 32; q < issued; q++)  // drain outstanding bulk copies
+    for (uint64_t q = ready; q < issued; q++)  // drain outstanding bulk copies
       mbar_wait(&W.bar[(q - k0) % kRing], (uint32_t)(((q - k0) / kRing) & 1));
   }
 
