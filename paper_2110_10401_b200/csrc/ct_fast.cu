@@ -10,8 +10,20 @@ constexpr uint64_t kNone = ~0ull;
 constexpr uint32_t kEmptyTag = 0xFFFFFFFFu;
 constexpr unsigned kFull = 0xFFFFFFFFu;
 
+// A block signature seen valid in the warp's steady communicator, and how many later
+// blocks repeated it exactly (same signature and devices) without being expanded yet.
+struct __align__(16) Tpl {
+  unsigned long long count;
+  uint32_t sig;   // coll_sig(); 0 = empty entry
+  uint32_t ndef;  // deferred repeats
+};
+constexpr int kTSets = 16;          // 2-way set-associative template table
+constexpr int kTE = 2 * kTSets;
+static_assert(kTE == 32, "one template entry per lane");
+
 struct __align__(16) WarpMem {
   ct_record ring[kRing][32];                 // TMA ring: chunk k lives in slot (k - k0) % kRing
+  Tpl tpl[kTE];
   unsigned long long bar[kRing];
   unsigned long long cseq[kCS][kMaxN];       // last collective block: seq per rank
   unsigned long long cfirst[kCS], clast[kCS];
@@ -25,10 +37,25 @@ struct __align__(16) WarpMem {
 struct __align__(16) CtaMem {
   unsigned long long calls[kTypes], pay_lo[kTypes], pay_hi[kTypes];
   unsigned long long copy_first[3];
+  unsigned long long oor_key;   // min out-of-range ordering key seen by the CTA
+  unsigned long long of_cell;   // min cell index whose 64-bit sum wrapped
   unsigned int diag[CT_NDIAG];
   uint32_t flags;
   int max_dev;
 };
+static_assert(sizeof(CtaMem) % 16 == 0, "histogram after CtaMem must stay aligned");
+// the shared-memory histogram must fit for d <= 16 (g2 = 18), else the kernel falls back
+// to global atomics
+static_assert(sizeof(WarpMem) * kWarps + sizeof(CtaMem) + kTypes * 18 * 18 * 12 <= 227 * 1024,
+              "shared memory budget: CTA histogram no longer fits for d <= 16");
+
+constexpr uint32_t kRM = kRing * 32 - 1;  // ring index mask (kRing is a power of two)
+static_assert((kRing & (kRing - 1)) == 0, "kRing must be a power of two");
+
+__device__ __forceinline__ CtaMem& cta_mem() {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  return *reinterpret_cast<CtaMem*>(smem_raw + sizeof(WarpMem) * kWarps);
+}
 
 // ------------------------------------------------------------ TMA bulk ring
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -94,53 +121,63 @@ __device__ uint64_t first_start(const ct_record* g, uint64_t n, uint64_t x, bool
 }
 
 // ------------------------------------------------------------ accumulation
+// Histogram location: the CTA's shared-memory copy right after CtaMem (SH), else global.
+template <bool SH>
+__device__ __forceinline__ unsigned long long* hist_bytes(const FastParams& P) {
+  return SH ? reinterpret_cast<unsigned long long*>(&cta_mem() + 1) : P.cells;
+}
+template <bool SH>
+__device__ __forceinline__ void* hist_freq(const FastParams& P) {
+  return SH ? static_cast<void*>(hist_bytes<SH>(P) + kTypes * P.g2 * P.g2) : static_cast<void*>(P.freq);
+}
+
+__device__ __forceinline__ void note_overflow(uint32_t& flags, unsigned long long key) {
+  flags |= F_OVERFLOW;
+  if (key < cta_mem().of_cell) atomicMin(&cta_mem().of_cell, key);
+}
+
 template <bool SH>  // SH: CTA histogram in shared memory (else global atomics)
 struct Acc {
   // two small register caches: transfer cells and per-type statistics; a miss evicts the
-  // older entry into the CTA histogram (shared-memory atomics)
+  // older entry into the CTA histogram (shared-memory atomics).  Everything else (the
+  // histogram, limits, first-error keys) comes from the kernel parameters / shared memory.
   uint32_t ctag[2], stag[2];
   unsigned long long csum[2], ssum[2];
   uint32_t ccnt[2], scnt[2];
   uint32_t flags;
-  unsigned long long* hb;
-  void* hf;
-  bool smem;
-  CtaMem* C;
-  int g2, gcap;
-  bool explicit_d;
   unsigned long long rec_key;  // (class << 62) | (element << 21) | (src rank << 11) for oor ordering
-  unsigned long long oor_key;
-  unsigned long long of_cell;
+  const FastParams& P;
 
-  __device__ void init(CtaMem* c, unsigned long long* b, void* f, bool sm, int g2_, int gcap_, bool ex) {
+  __device__ __forceinline__ explicit Acc(const FastParams& p) : P(p) {
     ctag[0] = ctag[1] = stag[0] = stag[1] = kEmptyTag;
     csum[0] = csum[1] = ssum[0] = ssum[1] = 0;
     ccnt[0] = ccnt[1] = scnt[0] = scnt[1] = 0;
-    flags = 0; hb = b; hf = f; smem = sm; C = c; g2 = g2_; gcap = gcap_; explicit_d = ex;
-    rec_key = 0; oor_key = kNone; of_cell = kNone;
+    flags = 0;
+    rec_key = 0;
   }
 
   __device__ __forceinline__ void flush_cell(uint32_t key, unsigned long long v, uint32_t c) {
-    const unsigned long long old = atomicAdd(hb + key, v);
-    if (old + v < old) { flags |= F_OVERFLOW; if (key < of_cell) of_cell = key; }
-    if (SH) atomicAdd(static_cast<unsigned int*>(hf) + key, c);
-    else atomicAdd(static_cast<unsigned long long*>(hf) + key, (unsigned long long)c);
+    const unsigned long long old = atomicAdd(hist_bytes<SH>(P) + key, v);
+    if (old + v < old) note_overflow(flags, key);
+    if (SH) atomicAdd(static_cast<unsigned int*>(hist_freq<SH>(P)) + key, c);
+    else atomicAdd(static_cast<unsigned long long*>(hist_freq<SH>(P)) + key, (unsigned long long)c);
   }
 
   __device__ __forceinline__ void flush_stat(uint32_t t, unsigned long long v, uint32_t c) {
-    const unsigned long long old = atomicAdd(&C->pay_lo[t], v);
-    if (old + v < old) atomicAdd(&C->pay_hi[t], 1ull);
-    atomicAdd(&C->calls[t], (unsigned long long)c);
+    CtaMem& C = cta_mem();
+    const unsigned long long old = atomicAdd(&C.pay_lo[t], v);
+    if (old + v < old) atomicAdd(&C.pay_hi[t], 1ull);
+    atomicAdd(&C.calls[t], (unsigned long long)c);
   }
 
   __device__ __forceinline__ void add_cell(uint32_t key, unsigned long long v) {
     if (ctag[0] == key) {
       const unsigned long long s = csum[0] + v;
-      if (s < v) { flags |= F_OVERFLOW; if (key < of_cell) of_cell = key; }
+      if (s < v) note_overflow(flags, key);
       csum[0] = s; ccnt[0]++;
     } else if (ctag[1] == key) {
       const unsigned long long s = csum[1] + v;
-      if (s < v) { flags |= F_OVERFLOW; if (key < of_cell) of_cell = key; }
+      if (s < v) note_overflow(flags, key);
       csum[1] = s; ccnt[1]++;
     } else {
       if (ctag[1] != kEmptyTag) flush_cell(ctag[1], csum[1], ccnt[1]);
@@ -175,17 +212,18 @@ struct Acc {
   // stats: calls += 1, payload += s (128-bit capable)
   __device__ __forceinline__ void stat(int type, unsigned __int128 s) {
     if ((s >> 63) == 0) { add_stat((uint32_t)type, (unsigned long long)s); return; }
+    CtaMem& C = cta_mem();
     const unsigned long long lo = (unsigned long long)s;
     unsigned long long hi = (unsigned long long)(s >> 64);
-    const unsigned long long old = atomicAdd(&C->pay_lo[type], lo);
+    const unsigned long long old = atomicAdd(&C.pay_lo[type], lo);
     if (old + lo < old) hi += 1;
-    atomicAdd(&C->pay_hi[type], hi);
-    atomicAdd(&C->calls[type], 1ull);
+    atomicAdd(&C.pay_hi[type], hi);
+    atomicAdd(&C.calls[type], 1ull);
   }
 
   __device__ __forceinline__ void out_of_range(unsigned long long k) {
-    flags |= explicit_d ? F_OOR : F_CAP;
-    if (k < oor_key) oor_key = k;
+    flags |= P.explicit_d ? F_OOR : F_CAP;
+    if (k < cta_mem().oor_key) atomicMin(&cta_mem().oor_key, k);
   }
 
   // endpoint: gpu g (>= 0), -1 host, -2 net.  ``sub`` orders transfers inside one
@@ -194,26 +232,133 @@ struct Acc {
   __device__ __forceinline__ void edge(int type, int src, int dst, unsigned __int128 bytes, int sub = 0) {
     const int a = src == -1 ? kHost : (src == -2 ? kNet : src + 2);
     const int b = dst == -1 ? kHost : (dst == -2 ? kNet : dst + 2);
-    if (src >= gcap || dst >= gcap) {
+    if (src >= P.gcap || dst >= P.gcap) {
       const unsigned long long k = rec_key | ((unsigned long long)min(sub, 1023) << 1);
-      if (src >= gcap) out_of_range(k);
-      if (dst >= gcap) out_of_range(k | 1);
+      if (src >= P.gcap) out_of_range(k);
+      if (dst >= P.gcap) out_of_range(k | 1);
       return;
     }
     if ((bytes >> 63) != 0) { flags |= F_OVERFLOW; return; }
-    add_cell((uint32_t)((type * g2 + a) * g2 + b), (unsigned long long)bytes);
+    add_cell((uint32_t)((type * P.g2 + a) * P.g2 + b), (unsigned long long)bytes);
   }
 };
 
-constexpr uint32_t kRM = kRing * 32 - 1;  // ring index mask (kRing is a power of two)
-static_assert((kRing & (kRing - 1)) == 0, "kRing must be a power of two");
-
-// device of a trace record (absolute index) held in the warp's ring
+// device of a record held in the warp's ring, by position relative to the ring origin
 struct WinDev {
   const ct_record* R;
-  uint64_t rb0;  // record index of ring position 0
-  __device__ __forceinline__ uint32_t dev_of(uint64_t abs) const { return R[(uint32_t)(abs - rb0) & kRM].dev; }
+  __device__ __forceinline__ uint32_t dev_of(uint64_t rel) const { return R[(uint32_t)rel & kRM].dev; }
 };
+
+// signature word of a collective record: coll, has_root, algo, dtype, root when rooted
+// (grouping.py:78-79 without count), bit 7 set so an empty entry (0) never matches
+__device__ __forceinline__ uint32_t coll_sig(uint32_t a2 /* kc | ad << 8 | aux << 16 */) {
+  return (a2 & (0x3F78u | ((a2 & 0x40u) ? 0xFFFF0000u : 0u))) | 0x80u;
+}
+
+__device__ __forceinline__ uint32_t tpl_set(unsigned long long count, uint32_t sig) {
+  const uint32_t h = ((uint32_t)count ^ ((uint32_t)(count >> 32) * 0x85EBCA6Bu) ^ (sig * 0xC2B2AE35u)) * 0x9E3779B1u;
+  return h >> 28;  // kTSets == 16
+}
+
+// ------------------------------------------------------------ out-of-line sinks
+// Sink that adds every transfer ``c`` times straight into the CTA histogram: bytes * c
+// into the cell, c into the frequency, S * c into the 128-bit payload and c calls.  Used
+// for deferred repeats (c identical blocks) and for the rare > 2^40-element records.
+template <bool SH>
+struct DirectSink {
+  unsigned long long* hb;
+  void* hf;
+  int g2, gcap, explicit_d;
+  unsigned long long rec_key;
+  unsigned long long c;
+  uint32_t flags;
+  __device__ __forceinline__ void stat(int type, unsigned __int128 s) {
+    CtaMem& C = cta_mem();
+    const unsigned __int128 v = s * c;
+    const unsigned long long lo = (unsigned long long)v;
+    unsigned long long hi = (unsigned long long)(v >> 64);
+    const unsigned long long old = atomicAdd(&C.pay_lo[type], lo);
+    if (old + lo < old) hi++;
+    if (hi) atomicAdd(&C.pay_hi[type], hi);
+    atomicAdd(&C.calls[type], c);
+  }
+  __device__ __forceinline__ void edge(int type, int src, int dst, unsigned __int128 bytes, int sub) {
+    if (src >= gcap || dst >= gcap) {  // same ordering key as Acc::edge
+      const unsigned long long k = rec_key | ((unsigned long long)min(sub, 1023) << 1);
+      flags |= explicit_d ? F_OOR : F_CAP;
+      const unsigned long long kk = src >= gcap ? k : (k | 1);
+      if (kk < cta_mem().oor_key) atomicMin(&cta_mem().oor_key, kk);
+      return;
+    }
+    const int a = src == -1 ? kHost : (src == -2 ? kNet : src + 2);
+    const int b = dst == -1 ? kHost : (dst == -2 ? kNet : dst + 2);
+    const unsigned long long key = (unsigned long long)((type * g2 + a) * g2 + b);
+    const unsigned __int128 v = bytes * c;
+    if ((v >> 63) != 0) {  // one transfer alone exceeds the cell (as Acc::edge); c repeats do by summing
+      if (c == 1) flags |= F_OVERFLOW;
+      else note_overflow(flags, key);
+      return;
+    }
+    const unsigned long long old = atomicAdd(hb + key, (unsigned long long)v);
+    if (old + (unsigned long long)v < old) note_overflow(flags, key);
+    if (SH) atomicAdd(static_cast<unsigned int*>(hf) + key, (unsigned int)c);
+    else atomicAdd(static_cast<unsigned long long*>(hf) + key, c);
+  }
+};
+
+// a collective record with count >= 2^40 (128-bit byte counts): rare, kept out of line
+template <bool SH>
+__device__ __noinline__ uint32_t expand_wide(ExpandParams ex, unsigned long long* hb, void* hf, int g2, int gcap,
+                                             int explicit_d, unsigned long long rec_key, Rec me, uint32_t head,
+                                             const ct_record* R) {
+  DirectSink<SH> ds{hb, hf, g2, gcap, explicit_d, rec_key, 1ull, 0u};
+  const WinDev wdv{R};
+  expand_collective<unsigned __int128>(ex, wdv, ds, me, head);
+  return ds.flags;
+}
+
+struct TblDev {  // devices of the steady communicator's last block, by rank
+  const uint16_t* cd;
+  __device__ __forceinline__ uint32_t dev_of(uint64_t r) const { return cd[(uint32_t)r]; }
+};
+
+// Expand every template with deferred repeats (lane = rank) and clear the counters;
+// returns error flags.
+template <bool SH>
+__device__ __noinline__ uint32_t flush_templates(ExpandParams ex, unsigned long long* hb, void* hf, int g2, WarpMem& W,
+                                                 int ts, uint32_t tcomm, uint32_t tn) {
+  const int lane = threadIdx.x & 31;
+  uint32_t flags = 0;
+  unsigned todo = __ballot_sync(kFull, W.tpl[lane].ndef != 0);  // kTE == 32
+  while (todo) {
+    const int e = __ffs(todo) - 1;
+    todo &= todo - 1;
+    const unsigned long long c = W.tpl[e].ndef;
+    if ((uint32_t)lane < tn) {
+      const uint32_t sg = W.tpl[e].sig;
+      Rec rc;
+      rc.count = W.tpl[e].count;
+      rc.seq = 0;
+      rc.comm = tcomm;
+      rc.nranks = tn;
+      rc.rank = (uint32_t)lane;
+      rc.dev = W.cdev[ts][lane];
+      rc.aux = sg >> 16;
+      rc.aux2 = 0;
+      rc.kc = sg & 0x78u;
+      rc.ad = (sg >> 8) & 0x3Fu;
+      DirectSink<SH> ds{hb, hf, g2, 1 << 30, 0, 0ull, c, 0u};  // steady devices are < gcap
+      const TblDev td{W.cdev[ts]};
+      if ((rc.count >> 40) == 0) expand_collective<uint64_t>(ex, td, ds, rc, 0);
+      else expand_collective<unsigned __int128>(ex, td, ds, rc, 0);
+      flags |= ds.flags;
+    }
+  }
+  __syncwarp();
+  W.tpl[lane].ndef = 0;
+  __syncwarp();
+  return flags;
+}
 
 __device__ __forceinline__ int find_slot(const WarpMem& W, uint32_t comm) {
   int s = -1;
@@ -297,7 +442,9 @@ __device__ __noinline__ bool devices_distinct(const ct_record* R, uint32_t i0, u
 // p2p order: per (comm, src, dst) channel, send seqs and recv seqs non-decreasing in file
 // order (then FIFO-by-position pairing equals the reference's seq-sorted pairing)
 __device__ __forceinline__ void p2p_order(P2PEntry* chan, const Rec& ra, uint64_t next_seq, bool sendA, int lane,
-                                          unsigned lt, unsigned gt, uint32_t& wflags) {
+                                          uint32_t& wflags) {
+  const unsigned lt = (1u << lane) - 1;
+  const unsigned gt = lane == 31 ? 0u : ~((2u << lane) - 1);
   uint64_t key = 0xFFFFFFFF00000000ull | lane, sseq = 0, rseq = 0;
   if (sendA) {  // the recv is the next record (elements are whole inside a window)
     key = ((uint64_t)ra.comm << 32) | ((uint64_t)ra.rank << 16) | ra.aux;
@@ -335,25 +482,26 @@ __device__ __forceinline__ void p2p_order(P2PEntry* chan, const Rec& ra, uint64_
   __syncwarp();
 }
 
-// expansion + accumulation of one record of a processed element (status ``st``)
+// expansion + accumulation of one record of a processed element (status ``st``); ``rel``
+// and ``head`` are positions relative to the ring origin ``rb0``
 template <bool SH>
 __device__ __forceinline__ void expand_record(const FastParams& P, Acc<SH>& acc, const WinDev& wdv, const Rec& me,
-                                              uint64_t abs, uint32_t st, uint64_t head, int& max_dev,
-                                              unsigned long long& cf0, unsigned long long& cf1,
-                                              unsigned long long& cf2) {
+                                              uint64_t rb0, uint32_t rel, uint32_t st, uint32_t head, int& max_dev,
+                                              uint32_t& copy_seen) {
   const int kind = me.kind();
   max_dev = max(max_dev, (int)me.dev);
   if (kind == CT_KIND_COLLECTIVE) {
     if (st != ST_VALID) return;
-    acc.rec_key = (min((unsigned long long)head, (1ull << 41) - 1) << 21) | ((unsigned long long)min(me.rank, 1023u) << 11);
+    acc.rec_key = (min((unsigned long long)(rb0 + head), (1ull << 41) - 1) << 21) | ((unsigned long long)min(me.rank, 1023u) << 11);
     if ((me.count >> 40) == 0) expand_collective<uint64_t>(P.ex, wdv, acc, me, head);
-    else expand_collective<unsigned __int128>(P.ex, wdv, acc, me, head);
+    else acc.flags |= expand_wide<SH>(P.ex, hist_bytes<SH>(P), hist_freq<SH>(P), P.g2, P.gcap, P.explicit_d,
+                                      acc.rec_key, me, head, wdv.R);
   } else if (kind == CT_KIND_SEND) {
     if (st != ST_VALID) return;
     const unsigned __int128 nb = (unsigned __int128)me.count * (unsigned)dtype_width(me.dtype());
     acc.stat(CT_T_SENDRECV, nb);
-    acc.rec_key = (1ull << 62) | (min((unsigned long long)abs, (1ull << 41) - 1) << 21);
-    const int rdev = (int)wdv.dev_of(abs + 1);
+    acc.rec_key = (1ull << 62) | (min((unsigned long long)(rb0 + rel), (1ull << 41) - 1) << 21);
+    const int rdev = (int)wdv.dev_of(rel + 1);
     if (rdev != (int)me.dev) acc.edge(CT_T_SENDRECV, (int)me.dev, rdev, nb);
   } else if (kind >= CT_KIND_MEMCPY) {
     const int ck = me.ckind();
@@ -361,13 +509,22 @@ __device__ __forceinline__ void expand_record(const FastParams& P, Acc<SH>& acc,
     if (ck != CT_CKIND_D2H) max_dev = max(max_dev, (int)me.aux2);
     const int t = CT_T_EXPLICIT + (kind - CT_KIND_MEMCPY);
     acc.stat(t, (unsigned __int128)me.count);
-    acc.rec_key = (2ull << 62) | (min((unsigned long long)abs, (1ull << 41) - 1) << 21);
+    acc.rec_key = (2ull << 62) | (min((unsigned long long)(rb0 + rel), (1ull << 41) - 1) << 21);
     acc.edge(t, ck == CT_CKIND_H2D ? -1 : (int)me.aux, ck == CT_CKIND_D2H ? -1 : (int)me.aux2,
              (unsigned __int128)me.count);
-    if (kind == CT_KIND_MEMCPY) cf0 = min(cf0, (unsigned long long)abs);
-    else if (kind == CT_KIND_UM) cf1 = min(cf1, (unsigned long long)abs);
-    else cf2 = min(cf2, (unsigned long long)abs);
+    // first record of each copy kind: positions only grow, so a lane's first is its min
+    const uint32_t bit = 1u << (kind - CT_KIND_MEMCPY);
+    if (!(copy_seen & bit)) {
+      copy_seen |= bit;
+      atomicMin(&cta_mem().copy_first[kind - CT_KIND_MEMCPY], rb0 + rel);
+    }
   }
+}
+
+__device__ __forceinline__ void count_diag(uint32_t st) {
+  if (st == ST_INCOMPAT) atomicAdd(&cta_mem().diag[CT_DIAG_INCOMPATIBLE], 1u);
+  else if (st == ST_DUPDEV) atomicAdd(&cta_mem().diag[CT_DIAG_DUPLICATE_DEVICE], 1u);
+  else if (st == ST_MISMATCH) atomicAdd(&cta_mem().diag[CT_DIAG_MISMATCHED_P2P], 1u);
 }
 
 }  // namespace
@@ -382,14 +539,12 @@ template <bool SH>
 __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   WarpMem* WM = reinterpret_cast<WarpMem*>(smem_raw);
-  CtaMem& C = *reinterpret_cast<CtaMem*>(smem_raw + sizeof(WarpMem) * kWarps);
+  CtaMem& C = cta_mem();
   const int ncell = kTypes * P.g2 * P.g2;
-  unsigned long long* shb = reinterpret_cast<unsigned long long*>(smem_raw + sizeof(WarpMem) * kWarps + sizeof(CtaMem));
-  unsigned int* shf = reinterpret_cast<unsigned int*>(shb + ncell);
+  unsigned long long* shb = hist_bytes<true>(P);
+  unsigned int* shf = static_cast<unsigned int*>(hist_freq<true>(P));
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   WarpMem& W = WM[warp];
-  const unsigned lt = (1u << lane) - 1;
-  const unsigned gt = lane == 31 ? 0u : ~((2u << lane) - 1);
 
   // ---- init
   if (SH)
@@ -397,30 +552,30 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
   if (tid < kTypes) { C.calls[tid] = 0; C.pay_lo[tid] = 0; C.pay_hi[tid] = 0; }
   if (tid < 3) C.copy_first[tid] = kNone;
   if (tid < CT_NDIAG) C.diag[tid] = 0;
-  if (tid == 0) { C.flags = 0; C.max_dev = -1; }
+  if (tid == 0) { C.flags = 0; C.max_dev = -1; C.oor_key = kNone; C.of_cell = kNone; }
+  W.tpl[lane].sig = 0;  // kTE == 32
+  W.tpl[lane].ndef = 0;
   if (lane < kCS) {
     W.tag[lane] = kEmptyTag; W.sn[lane] = 0; W.sver[lane] = 0;
     W.cfirst[lane] = kNone; W.clast[lane] = kNone;
     for (int t = 0; t < 5; t++) W.tfirst[lane][t] = kNone;
   }
-  P2PEntry* chan = P.chans + (size_t)(blockIdx.x * kWarps + warp) * kPC;  // this warp's channel table
-  for (int e = lane; e < kPC; e += 32) chan[e].key = kNone;
+  const uint32_t gw = blockIdx.x * kWarps + warp;
+  for (int e = lane; e < kPC; e += 32) P.chans[(size_t)gw * kPC + e].key = kNone;
   if (lane < kRing) mbar_init(&W.bar[lane], 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
 
-  Acc<SH> acc;
-  acc.init(&C, SH ? shb : P.cells, SH ? (void*)shf : (void*)P.freq, SH, P.g2, P.gcap, P.explicit_d != 0);
+  const long long t_start = clock64();
+  Acc<SH> acc(P);
   int my_max_dev = -1;
-  uint32_t n_incompat = 0, n_dupdev = 0, n_mismatch = 0;
-  unsigned long long cf0 = kNone, cf1 = kNone, cf2 = kNone;  // first record of each copy kind
+  uint32_t copy_seen = 0;              // copy kinds this lane has seen (first index noted)
   uint32_t wflags = 0;
   unsigned long long tf_pend = ~0ull;  // (slot, type) pairs whose first valid instance is not yet recorded
-  uint32_t sc_comm = kEmptyTag;  // last (comm, slot) pair looked up (warp-uniform)
+  uint32_t sc_comm = kEmptyTag;        // last (comm, slot) pair looked up (warp-uniform)
   int sc_slot = -1;
 
   // ---- this warp's range, cut at element starts
-  const uint32_t gw = blockIdx.x * kWarps + warp;
   const uint64_t NC = P.n_chunks;
   const uint64_t c0 = NC * gw / P.total_warps, c1 = NC * (gw + 1) / P.total_warps;
   bool bad = false;
@@ -430,41 +585,45 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
   if (start < end && !bad) {
     // The warp slides a 32-record window over its range.  A window always begins at an
     // element start and consumes exactly the elements that lie whole inside it (n <= 32
-    // guarantees progress); the next window begins where the last one ended.  Chunk k of
-    // the range lives in ring slot (k - k0) % kRing; a window touches at most two chunks.
+    // guarantees progress); the next window begins where the last one ended.  Positions
+    // are 32-bit, relative to the ring origin rb0 (chunk k0); relative chunk q lives in
+    // ring slot q % kRing, so record rb0 + x sits at ring index x & kRM.
     const uint64_t k0 = start / 32;
-    const uint64_t rb0 = k0 * 32;                                  // record at ring index 0
-    const uint64_t last_chunk = min(NC, (end + 31) / 32 + 1);      // chunks below this may be read
+    const uint64_t rb0 = k0 * 32;
+    const uint32_t lastc = (uint32_t)(min(NC, (end + 31) / 32 + 1) - k0);  // chunks below this may be read
+    const uint32_t eo = (uint32_t)(end - rb0);
+    const uint32_t no = (uint32_t)min((unsigned long long)(P.n - rb0), 0xFFFFFFFFull);
     const ct_record* R = &W.ring[0][0];
-    const WinDev wdv{R, rb0};
-    uint64_t issued = k0, ready = k0, freed = k0;
-    {
-      const uint64_t lim = min(k0 + kRing, last_chunk);
-      for (; issued < lim; issued++)
-        if (lane == 0)
-          bulk_load(W.ring[(issued - k0) % kRing], P.recs + issued * 32,
-                    (uint32_t)min((uint64_t)32, P.n - issued * 32) * (uint32_t)sizeof(ct_record),
-                    &W.bar[(issued - k0) % kRing]);
-    }
+    const WinDev wdv{R};
+    uint32_t issued = 0, ready = 0, freed = 0;
+    for (; issued < (uint32_t)kRing && issued < lastc; issued++)
+      if (lane == 0) {
+        const uint64_t first = (k0 + issued) * 32;
+        bulk_load(W.ring[issued], P.recs + first, (uint32_t)min((uint64_t)32, P.n - first) * (uint32_t)sizeof(ct_record),
+                  &W.bar[issued]);
+      }
 
-    uint64_t b = start;
-    while (b < end) {
-      const uint64_t kB = min((b + 31) / 32, last_chunk - 1);
+    int ts = -1;                     // steady comm slot (-1: none)
+    uint32_t tcomm = 0, tn = 0;      // its comm id and nranks
+    uint32_t pending = 0;            // deferred blocks not yet expanded
+    uint32_t skip = 0, backoff = 0;  // steady attempts back off after misses
+    uint32_t bo = (uint32_t)(start - rb0);
+    while (bo < eo) {
+      const uint32_t kB = min((bo + 31) / 32, lastc - 1);
       while (ready <= kB) {
-        mbar_wait(&W.bar[(ready - k0) % kRing], (uint32_t)(((ready - k0) / kRing) & 1));
+        mbar_wait(&W.bar[ready % kRing], (ready / kRing) & 1);
         ready++;
       }
-      const uint32_t ri0 = (uint32_t)(b - rb0);                    // ring index of the window start
-      const uint32_t nval = (uint32_t)min((uint64_t)32, P.n - b);  // records that exist
-      const uint32_t lim = (uint32_t)min((uint64_t)32, end - b);   // heads this range owns
+      const uint32_t nval = min(32u, no - bo);  // records that exist
+      const uint32_t lim = min(32u, eo - bo);   // heads this range owns
       const bool valid = (uint32_t)lane < nval;
       Rec ra{};
       int kind = 7;
-      if (valid) { ra = load_swz(R, (ri0 + lane) & kRM); kind = ra.kind(); }
-      uint64_t nb;
+      if (valid) { ra = load_swz(R, (bo + lane) & kRM); kind = ra.kind(); }
+      uint32_t nbo;
       if (P.dbg & 4) {  // diagnostic: stream only (roofline experiments)
         my_max_dev = max(my_max_dev, (int)(ra.dev ^ ra.rank));
-        nb = b + 32;
+        nbo = bo + 32;
       } else {
         // ---------------- elements: starts, lengths, whole-in-window heads, coverage
         const bool isS = valid && is_start(kind, ra.rank);
@@ -483,185 +642,300 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
         const int hL = H ? 31 - __clz(H) : 0;
         const uint32_t Pw = hL + __shfl_sync(kFull, len, hL);      // records consumed
         const bool mem = (uint32_t)lane < Pw;
-        const unsigned below = H & (lt | (1u << lane));
+        const unsigned below = H & (0xFFFFFFFFu >> (31 - lane));
         const int hA = below ? 31 - __clz(below) : 0;
         const uint32_t lenA = __shfl_sync(kFull, len, hA);
         if (mem && (uint32_t)lane >= (uint32_t)hA + lenA) badl = true;  // a record no element covers
         if (head && ((uint32_t)lane + len > nval || !range_clear((unsigned long long)Sall, (uint32_t)lane + 1, len - 1)))
           badl = true;  // runs past the trace, or another element starts inside this one
-
-        // ---------------- member checks against the predecessor record (lane shuffles)
-        // words: comm | nranks, rank | kc, ad, aux | count lo | count hi
         const uint32_t a2 = ra.kc | (ra.ad << 8) | (ra.aux << 16);
-        bool gfail = false, mis = false;
-        {
-          const uint32_t q0 = __shfl_up_sync(kFull, ra.comm, 1);
-          const uint32_t q1 = __shfl_up_sync(kFull, ra.nranks | (ra.rank << 16), 1);
-          const uint32_t q2 = __shfl_up_sync(kFull, a2, 1);
-          const uint32_t q3 = __shfl_up_sync(kFull, (uint32_t)ra.count, 1);
-          const uint32_t q4 = __shfl_up_sync(kFull, (uint32_t)(ra.count >> 32), 1);
-          if (mem && !head) member_check(ra, a2, q0, q1, q2, q3, q4, badl, gfail, mis);
-        }
-        if (__any_sync(kFull, badl)) { wflags |= F_NONCANON; break; }  // host re-runs the exact path
-        const bool collH = head && kind == CT_KIND_COLLECTIVE;
-        const bool sendH = head && kind == CT_KIND_SEND;
-        const unsigned Hc = __ballot_sync(kFull, collH);
-        const unsigned Hs = __ballot_sync(kFull, sendH);
-        const unsigned sigmask = __ballot_sync(kFull, gfail);
-        const unsigned mismask = Hs ? __ballot_sync(kFull, mis) : 0u;
 
-        // ---------------- per-comm predecessor block, comm slot (uniform fast case)
-        uint32_t info = 0;  // slot | ph << 4 | has_ph << 10 | hist << 11 | ver << 12 | last << 13
-        if (Hc) {
-          const uint32_t c_first = __shfl_sync(kFull, ra.comm, __ffs(Hc) - 1);
-          if (__all_sync(kFull, !collH || ra.comm == c_first)) {
-            int su = c_first == sc_comm ? sc_slot : find_slot(W, c_first);
-            if (su < 0) {  // new comm in this range
-              for (int s = kCS - 1; s >= 0; s--)
-                if (W.tag[s] == kEmptyTag) su = s;
-              __syncwarp();
-              if (su < 0) wflags |= F_NONCANON;  // more comms than slots in one range
-              else if (lane == 0) W.tag[su] = c_first;
-              __syncwarp();
-            }
-            if (c_first >= P.n_comms) wflags |= F_COMM_RANGE | F_NONCANON;
-            sc_comm = c_first;
-            sc_slot = su;
-            const int slot = su < 0 ? 0 : su;
-            const uint32_t sn = W.sn[slot];
-            const uint32_t base = (uint32_t)slot | (sn ? 1u << 11 : 0u) | (sn && W.sver[slot] ? 1u << 12 : 0u);
-            const unsigned lower = Hc & ((1u << hA) - 1);
-            const int ph = lower ? 31 - __clz(lower) : -1;
-            info = base | ((uint32_t)(ph & 63) << 4) | (ph >= 0 ? 1u << 10 : 0u) | ((Hc >> hA) == 1u ? 1u << 13 : 0u);
-          } else {
-            // several comms start blocks in this window: per-head slots, MATCH for predecessors
-            int slot = -1;
-            if (collH) {
-              if (ra.comm >= P.n_comms) wflags |= F_COMM_RANGE | F_NONCANON;
-              slot = ra.comm == sc_comm ? sc_slot : find_slot(W, ra.comm);
-            }
-            while (true) {  // allocate slots for unseen comms (rare, warp-serial)
-              const unsigned miss = __ballot_sync(kFull, collH && slot < 0);
-              if (!miss) break;
-              const uint32_t cm = __shfl_sync(kFull, ra.comm, __ffs(miss) - 1);
-              int free_s = -1;
-              for (int s = kCS - 1; s >= 0; s--)
-                if (W.tag[s] == kEmptyTag) free_s = s;
-              __syncwarp();
-              if (free_s < 0) { wflags |= F_NONCANON; break; }
-              if (lane == 0) W.tag[free_s] = cm;
-              __syncwarp();
-              if (collH && slot < 0 && ra.comm == cm) slot = free_s;
-            }
-            const unsigned same =
-                __match_any_sync(kFull, collH ? (unsigned long long)ra.comm : (0xFFFFFFFF00000000ull | lane)) & Hc;
-            const unsigned lower = same & lt;
-            const int ph = lower ? 31 - __clz(lower) : -1;
-            const int hs = slot < 0 ? 0 : slot;
-            const bool hist = collH && W.sn[hs] != 0;
-            const uint32_t hinfo = (uint32_t)hs | ((uint32_t)(ph & 63) << 4) | (ph >= 0 ? 1u << 10 : 0u) |
-                                   (hist ? 1u << 11 : 0u) | (hist && W.sver[hs] ? 1u << 12 : 0u) |
-                                   ((same & gt) == 0 ? 1u << 13 : 0u);
-            info = __shfl_sync(kFull, hinfo, hA);
+        // ---------------- steady window: every element is a copy or a block of the steady
+        // communicator repeating a known-valid signature with the devices of its last block
+        // and increasing seqs.  Such blocks are valid instances with identical transfers:
+        // count them per template and expand once, multiplied, at the next flush.
+        bool steady = false;
+        if (ts >= 0 && skip == 0) {
+          bool okl = !badl;
+          uint32_t ti = 0;
+          const bool cl = mem && kind == CT_KIND_COLLECTIVE;
+          if (cl) {
+            const uint32_t sg = coll_sig(a2);
+            const uint32_t set = tpl_set(ra.count, sg);
+            const Tpl e0 = W.tpl[2 * set], e1 = W.tpl[2 * set + 1];
+            const bool h0 = e0.count == ra.count && e0.sig == sg;
+            const bool h1 = e1.count == ra.count && e1.sig == sg;
+            ti = 2 * set + (h0 ? 0u : 1u);
+            okl = okl && (h0 || h1) && ra.comm == tcomm && ra.nranks == tn && ra.rank == (uint32_t)(lane - hA) &&
+                  ra.dev == W.cdev[ts][ra.rank & 31] && ra.dev < (uint32_t)P.gcap;
+          } else if (mem) {
+            okl = okl && kind >= CT_KIND_MEMCPY && kind <= CT_KIND_ZEROCOPY;
           }
-        }
-        if (collH) {  // nranks constant per comm (grouping.py:104-108)
-          const uint32_t pn = (info & (1u << 10)) ? R[(ri0 + ((info >> 4) & 63)) & kRM].nranks
-                                                  : ((info & (1u << 11)) ? W.sn[info & 15] : ra.nranks);
-          if (pn != ra.nranks) wflags |= F_NONCANON;
-        }
-
-        // ---------------- per-member seq order and device inheritance from the last block
-        bool devf = false;
-        const bool cm = mem && kind == CT_KIND_COLLECTIVE;
-        {
-          const int src = (cm && (info & (1u << 10))) ? ((((info >> 4) & 63) + (int)ra.rank) & 31) : lane;
+          const unsigned Hc = __ballot_sync(kFull, head && kind == CT_KIND_COLLECTIVE);
+          const uint32_t tiH = __shfl_sync(kFull, ti, hA);
+          const unsigned lower = Hc & ((1u << hA) - 1);
+          const int ph = lower ? 31 - __clz(lower) : -1;  // previous block of the comm in the window
+          const int src = ph >= 0 ? ((ph + (int)ra.rank) & 31) : lane;
           const uint64_t pseq = ((uint64_t)__shfl_sync(kFull, (uint32_t)(ra.seq >> 32), src) << 32) |
                                 __shfl_sync(kFull, (uint32_t)ra.seq, src);
-          if (cm) order_check(W, ra, info, pseq, wflags, devf);
+          if (cl) {
+            const uint64_t prev = ph >= 0 ? pseq : W.cseq[ts][ra.rank & 31];
+            okl = okl && ti == tiH && prev < ra.seq;
+          }
+          if ((P.dbg & 8) && !okl) {  // diagnostic: why a steady attempt failed
+            uint32_t why = badl ? 1u : 0u;
+            if (cl) {
+              const uint32_t sg = coll_sig(a2);
+              const uint32_t set = tpl_set(ra.count, sg);
+              const bool hit = (W.tpl[2 * set].count == ra.count && W.tpl[2 * set].sig == sg) ||
+                               (W.tpl[2 * set + 1].count == ra.count && W.tpl[2 * set + 1].sig == sg);
+              if (!hit) why |= 2;
+              if (ra.comm != tcomm || ra.nranks != tn) why |= 4;
+              if (ra.rank != (uint32_t)(lane - hA)) why |= 8;
+              if (ra.dev != W.cdev[ts][ra.rank & 31]) why |= 16;
+              if (ti != tiH) why |= 128;
+              if (!((ph >= 0 ? pseq : W.cseq[ts][ra.rank & 31]) < ra.seq)) why |= 256;
+            } else if (mem) {
+              why |= 64;
+            }
+            atomicOr(&P.st->pad, why);
+          }
+          if (__all_sync(kFull, okl)) {
+            steady = true;
+            backoff = 0;
+            if ((P.dbg & 8) && lane == 0) atomicAdd(&P.st->n_chain, 1u);
+            if (Hc) {
+              const int hLc = 31 - __clz(Hc);
+              if (head && kind == CT_KIND_COLLECTIVE) atomicAdd(&W.tpl[ti].ndef, 1u);
+              pending += __popc(Hc);
+              if (cl && hA == hLc) W.cseq[ts][ra.rank] = ra.seq;
+              if (lane == 0) W.clast[ts] = rb0 + bo + hLc;
+              __syncwarp();
+            }
+            if (Hc != H && mem && kind != CT_KIND_COLLECTIVE && !(P.dbg & 1))
+              expand_record(P, acc, wdv, ra, rb0, bo + lane, ST_VALID, bo + lane, my_max_dev, copy_seen);
+          } else {
+            if (backoff == 63) {  // long miss streak: drop stale templates
+              W.tpl[lane].sig = 0;
+              __syncwarp();
+            }
+            backoff = min(2 * backoff + 1, 63u);
+            skip = backoff;
+          }
+        } else if (skip) {
+          skip--;
         }
-        const unsigned devmask = __ballot_sync(kFull, devf);
 
-        // ---------------- element status (every member derives its element's status)
-        // collective: incompatible if any member's signature differs (grouping.py:144-155),
-        // duplicate device if devices are not pairwise distinct (grouping.py:156-167)
-        const unsigned needs_full = __ballot_sync(kFull, collH && !range_clear(devmask, (uint32_t)lane, ra.nranks));
-        bool dist = true;
-        if (needs_full) {  // devices changed since the comm's last block: full pairwise check
-          if ((needs_full >> lane) & 1) dist = devices_distinct(R, ri0 + lane, ra.nranks);
-        }
-        const unsigned dupmask = __ballot_sync(kFull, !dist);  // heads with duplicate devices
-        const uint32_t kindH = __shfl_sync(kFull, (uint32_t)kind, hA);
-        uint32_t st = ST_NONE;
-        if (mem) {
-          if (kindH == CT_KIND_COLLECTIVE)
-            st = !range_clear(sigmask, (uint32_t)hA + 1, lenA - 1) ? ST_INCOMPAT
-                                                                   : (((dupmask >> hA) & 1) ? ST_DUPDEV : ST_VALID);
-          else if (kindH == CT_KIND_SEND)
-            st = ((mismask >> (hA + 1)) & 1) ? ST_MISMATCH : ST_VALID;
-          else
-            st = ST_VALID;
-        }
-        if (head) {
-          n_incompat += st == ST_INCOMPAT;
-          n_dupdev += st == ST_DUPDEV;
-          n_mismatch += st == ST_MISMATCH;
-        }
+        if (!steady) {
+          if (pending) {  // the general path may change the steady comm's devices: expand first
+            acc.flags |= flush_templates<SH>(P.ex, hist_bytes<SH>(P), hist_freq<SH>(P), P.g2, W, ts, tcomm, tn);
+            pending = 0;
+          }
+          // ---------------- member checks against the predecessor record (lane shuffles)
+          // words: comm | nranks, rank | kc, ad, aux | count lo | count hi
+          bool gfail = false, mis = false;
+          {
+            const uint32_t q0 = __shfl_up_sync(kFull, ra.comm, 1);
+            const uint32_t q1 = __shfl_up_sync(kFull, ra.nranks | (ra.rank << 16), 1);
+            const uint32_t q2 = __shfl_up_sync(kFull, a2, 1);
+            const uint32_t q3 = __shfl_up_sync(kFull, (uint32_t)ra.count, 1);
+            const uint32_t q4 = __shfl_up_sync(kFull, (uint32_t)(ra.count >> 32), 1);
+            if (mem && !head) member_check(ra, a2, q0, q1, q2, q3, q4, badl, gfail, mis);
+          }
+          if (__any_sync(kFull, badl)) { wflags |= F_NONCANON; break; }  // host re-runs the exact path
+          const bool collH = head && kind == CT_KIND_COLLECTIVE;
+          const bool sendH = head && kind == CT_KIND_SEND;
+          const unsigned Hc = __ballot_sync(kFull, collH);
+          const unsigned Hs = __ballot_sync(kFull, sendH);
+          const unsigned sigmask = __ballot_sync(kFull, gfail);
+          const unsigned mismask = Hs ? __ballot_sync(kFull, mis) : 0u;
 
-        // ---------------- p2p order: per (comm, src, dst) channel non-decreasing send and
-        // recv seqs (decompose.py:359-361 sorts each side by seq; FIFO pairs by position)
-        if (Hs) {
-          const uint64_t nseq = ((uint64_t)__shfl_down_sync(kFull, (uint32_t)(ra.seq >> 32), 1) << 32) |
-                                __shfl_down_sync(kFull, (uint32_t)ra.seq, 1);
-          p2p_order(chan, ra, nseq, sendH, lane, lt, gt, wflags);
-        }
+          // ---------------- per-comm predecessor block, comm slot (uniform fast case)
+          uint32_t info = 0;  // slot | ph << 4 | has_ph << 10 | hist << 11 | ver << 12 | last << 13
+          int uslot = -1;     // the single comm slot of the window's blocks (uniform case)
+          if (Hc) {
+            const uint32_t c_first = __shfl_sync(kFull, ra.comm, __ffs(Hc) - 1);
+            if (__all_sync(kFull, !collH || ra.comm == c_first)) {
+              int su = c_first == sc_comm ? sc_slot : find_slot(W, c_first);
+              if (su < 0) {  // new comm in this range
+                for (int s = kCS - 1; s >= 0; s--)
+                  if (W.tag[s] == kEmptyTag) su = s;
+                __syncwarp();
+                if (su < 0) wflags |= F_NONCANON;  // more comms than slots in one range
+                else if (lane == 0) W.tag[su] = c_first;
+                __syncwarp();
+              }
+              if (c_first >= P.n_comms) wflags |= F_COMM_RANGE | F_NONCANON;
+              sc_comm = c_first;
+              sc_slot = su;
+              uslot = su;
+              const int slot = su < 0 ? 0 : su;
+              const uint32_t sn = W.sn[slot];
+              const uint32_t base = (uint32_t)slot | (sn ? 1u << 11 : 0u) | (sn && W.sver[slot] ? 1u << 12 : 0u);
+              const unsigned lower = Hc & ((1u << hA) - 1);
+              const int ph = lower ? 31 - __clz(lower) : -1;
+              info = base | ((uint32_t)(ph & 63) << 4) | (ph >= 0 ? 1u << 10 : 0u) | ((Hc >> hA) == 1u ? 1u << 13 : 0u);
+            } else {
+              // several comms start blocks in this window: per-head slots, MATCH for predecessors
+              int slot = -1;
+              if (collH) {
+                if (ra.comm >= P.n_comms) wflags |= F_COMM_RANGE | F_NONCANON;
+                slot = ra.comm == sc_comm ? sc_slot : find_slot(W, ra.comm);
+              }
+              while (true) {  // allocate slots for unseen comms (rare, warp-serial)
+                const unsigned miss = __ballot_sync(kFull, collH && slot < 0);
+                if (!miss) break;
+                const uint32_t cm = __shfl_sync(kFull, ra.comm, __ffs(miss) - 1);
+                int free_s = -1;
+                for (int s = kCS - 1; s >= 0; s--)
+                  if (W.tag[s] == kEmptyTag) free_s = s;
+                __syncwarp();
+                if (free_s < 0) { wflags |= F_NONCANON; break; }
+                if (lane == 0) W.tag[free_s] = cm;
+                __syncwarp();
+                if (collH && slot < 0 && ra.comm == cm) slot = free_s;
+              }
+              const unsigned lt = (1u << lane) - 1;
+              const unsigned same =
+                  __match_any_sync(kFull, collH ? (unsigned long long)ra.comm : (0xFFFFFFFF00000000ull | lane)) & Hc;
+              const unsigned lower = same & lt;
+              const int ph = lower ? 31 - __clz(lower) : -1;
+              const int hs = slot < 0 ? 0 : slot;
+              const bool hist = collH && W.sn[hs] != 0;
+              const uint32_t hinfo = (uint32_t)hs | ((uint32_t)(ph & 63) << 4) | (ph >= 0 ? 1u << 10 : 0u) |
+                                     (hist ? 1u << 11 : 0u) | (hist && W.sver[hs] ? 1u << 12 : 0u) |
+                                     ((same & ~lt & ~(1u << lane)) == 0 ? 1u << 13 : 0u);
+              info = __shfl_sync(kFull, hinfo, hA);
+            }
+          }
+          if (collH) {  // nranks constant per comm (grouping.py:104-108)
+            const uint32_t pn = (info & (1u << 10)) ? R[(bo + ((info >> 4) & 63)) & kRM].nranks
+                                                    : ((info & (1u << 11)) ? W.sn[info & 15] : ra.nranks);
+            if (pn != ra.nranks) wflags |= F_NONCANON;
+          }
 
-        // ---------------- table update with the last block of each comm in the window
-        __syncwarp();
-        if (cm && (info & (1u << 13))) { W.cseq[info & 15][ra.rank] = ra.seq; W.cdev[info & 15][ra.rank] = (uint16_t)ra.dev; }
-        if (collH) {
-          const int hs = info & 15;
-          const uint64_t gi = b + lane;
-          if (!(info & (3u << 10))) W.cfirst[hs] = gi;  // first block of this comm in the range
-          if (info & (1u << 13)) { W.sn[hs] = ra.nranks; W.sver[hs] = dist; W.clast[hs] = gi; }
-        }
-        if (Hc) {  // first valid instance per (comm slot, type): only until recorded once
-          const unsigned long long bit = (collH && st == ST_VALID) ? 1ull << ((info & 15) * 5 + ra.coll()) : 0ull;
-          const bool rec = (bit & tf_pend) != 0;
-          if (rec) note_min_smem(&W.tfirst[info & 15][ra.coll()], b + lane);
-          const unsigned lo = __reduce_or_sync(kFull, rec ? (unsigned)bit : 0u);
-          const unsigned hi = __reduce_or_sync(kFull, rec ? (unsigned)(bit >> 32) : 0u);
-          tf_pend &= ~(((unsigned long long)hi << 32) | lo);
-        }
-        __syncwarp();
+          // ---------------- per-member seq order and device inheritance from the last block
+          bool devf = false;
+          const bool cm = mem && kind == CT_KIND_COLLECTIVE;
+          {
+            const int src = (cm && (info & (1u << 10))) ? ((((info >> 4) & 63) + (int)ra.rank) & 31) : lane;
+            const uint64_t pseq = ((uint64_t)__shfl_sync(kFull, (uint32_t)(ra.seq >> 32), src) << 32) |
+                                  __shfl_sync(kFull, (uint32_t)ra.seq, src);
+            if (cm) order_check(W, ra, info, pseq, wflags, devf);
+          }
+          const unsigned devmask = __ballot_sync(kFull, devf);
 
-        // ---------------- expansion + accumulation
-        if (mem && !(P.dbg & 1)) expand_record(P, acc, wdv, ra, b + lane, st, b + (uint64_t)hA, my_max_dev, cf0, cf1, cf2);
-        nb = b + Pw;
+          // ---------------- element status (every member derives its element's status)
+          // collective: incompatible if any member's signature differs (grouping.py:144-155),
+          // duplicate device if devices are not pairwise distinct (grouping.py:156-167)
+          const unsigned needs_full = __ballot_sync(kFull, collH && !range_clear(devmask, (uint32_t)lane, ra.nranks));
+          bool dist = true;
+          if (needs_full) {  // devices changed since the comm's last block: full pairwise check
+            if ((needs_full >> lane) & 1) dist = devices_distinct(R, bo + lane, ra.nranks);
+          }
+          const unsigned dupmask = __ballot_sync(kFull, !dist);  // heads with duplicate devices
+          const uint32_t kindH = __shfl_sync(kFull, (uint32_t)kind, hA);
+          uint32_t st = ST_NONE;
+          if (mem) {
+            if (kindH == CT_KIND_COLLECTIVE)
+              st = !range_clear(sigmask, (uint32_t)hA + 1, lenA - 1) ? ST_INCOMPAT
+                                                                     : (((dupmask >> hA) & 1) ? ST_DUPDEV : ST_VALID);
+            else if (kindH == CT_KIND_SEND)
+              st = ((mismask >> (hA + 1)) & 1) ? ST_MISMATCH : ST_VALID;
+            else
+              st = ST_VALID;
+          }
+          if (head && st != ST_VALID) count_diag(st);
+
+          // ---------------- p2p order: per (comm, src, dst) channel non-decreasing send and
+          // recv seqs (decompose.py:359-361 sorts each side by seq; FIFO pairs by position)
+          if (Hs) {
+            const uint64_t nseq = ((uint64_t)__shfl_down_sync(kFull, (uint32_t)(ra.seq >> 32), 1) << 32) |
+                                  __shfl_down_sync(kFull, (uint32_t)ra.seq, 1);
+            p2p_order(P.chans + (size_t)gw * kPC, ra, nseq, sendH, lane, wflags);
+          }
+
+          // ---------------- table update with the last block of each comm in the window
+          __syncwarp();
+          if (cm && (info & (1u << 13))) { W.cseq[info & 15][ra.rank] = ra.seq; W.cdev[info & 15][ra.rank] = (uint16_t)ra.dev; }
+          if (collH) {
+            const int hs = info & 15;
+            const uint64_t gi = rb0 + bo + lane;
+            if (!(info & (3u << 10))) W.cfirst[hs] = gi;  // first block of this comm in the range
+            if (info & (1u << 13)) { W.sn[hs] = ra.nranks; W.sver[hs] = dist; W.clast[hs] = gi; }
+          }
+          if (Hc) {  // first valid instance per (comm slot, type): only until recorded once
+            const unsigned long long bit = (collH && st == ST_VALID) ? 1ull << ((info & 15) * 5 + ra.coll()) : 0ull;
+            const bool rec = (bit & tf_pend) != 0;
+            if (rec) note_min_smem(&W.tfirst[info & 15][ra.coll()], rb0 + bo + lane);
+            const unsigned lo = __reduce_or_sync(kFull, rec ? (unsigned)bit : 0u);
+            const unsigned hi = __reduce_or_sync(kFull, rec ? (unsigned)(bit >> 32) : 0u);
+            tf_pend &= ~(((unsigned long long)hi << 32) | lo);
+          }
+          __syncwarp();
+
+          // ---------------- expansion + accumulation
+          if (mem && !(P.dbg & 1))
+            expand_record(P, acc, wdv, ra, rb0, bo + lane, st, bo + (uint32_t)hA, my_max_dev, copy_seen);
+
+          // ---------------- steady comm and templates: the window's last block, when valid
+          if (ts >= 0 && !W.sver[ts]) ts = -1;  // duplicate devices: repeats are not valid
+          if (Hc && uslot >= 0) {
+            const int hLc = 31 - __clz(Hc);
+            if (__shfl_sync(kFull, st, hLc) == ST_VALID && W.sver[uslot] && uslot != ts) {
+              W.tpl[lane].sig = 0;
+              ts = uslot;
+              tcomm = __shfl_sync(kFull, ra.comm, hLc);
+              tn = __shfl_sync(kFull, ra.nranks, hLc);
+              skip = backoff = 0;
+            }
+            __syncwarp();
+            if (ts == uslot && skip <= 3 && collH && st == ST_VALID) {  // valid signatures before an attempt
+              const uint32_t sg = coll_sig(a2);
+              const uint32_t set = tpl_set(ra.count, sg);
+              Tpl* e = &W.tpl[2 * set];
+              const bool in0 = e[0].count == ra.count && e[0].sig == sg;
+              const bool in1 = e[1].count == ra.count && e[1].sig == sg;
+              if (!in0 && !in1) {  // empty way first, else replace way (seq & 1); racing lanes only cost hits
+                const int way = e[0].sig == 0 ? 0 : (e[1].sig == 0 ? 1 : (int)(ra.seq & 1));
+                e[way].count = ra.count;
+                e[way].sig = sg;
+                e[way].ndef = 0;
+              }
+            }
+            __syncwarp();
+          }
+        }  // general path
+        nbo = bo + Pw;
       }
 
       // ---------------- slide: chunks wholly behind the next window refill their slots
-      const uint64_t kf = nb / 32;
+      const uint32_t kf = nbo / 32;
       if (kf > freed) {
         __syncwarp();
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         do {
-          const uint64_t q = freed + kRing;
-          if (q < last_chunk) {
-            if (lane == 0)
-              bulk_load(W.ring[(freed - k0) % kRing], P.recs + q * 32,
-                        (uint32_t)min((uint64_t)32, P.n - q * 32) * (uint32_t)sizeof(ct_record),
-                        &W.bar[(freed - k0) % kRing]);
+          const uint32_t q = freed + kRing;
+          if (q < lastc) {
+            if (lane == 0) {
+              const uint64_t first = (k0 + q) * 32;
+              bulk_load(W.ring[freed % kRing], P.recs + first,
+                        (uint32_t)min((uint64_t)32, P.n - first) * (uint32_t)sizeof(ct_record), &W.bar[freed % kRing]);
+            }
             issued = q + 1;
           }
           freed++;
         } while (freed < kf);
       }
-      b = nb;
+      bo = nbo;
     }
-    for (uint64_t q = ready; q < issued; q++)  // drain outstanding bulk copies
-      mbar_wait(&W.bar[(q - k0) % kRing], (uint32_t)(((q - k0) / kRing) & 1));
+    if (pending) acc.flags |= flush_templates<SH>(P.ex, hist_bytes<SH>(P), hist_freq<SH>(P), P.g2, W, ts, tcomm, tn);
+    for (uint32_t q = ready; q < issued; q++)  // drain outstanding bulk copies
+      mbar_wait(&W.bar[q % kRing], (q / kRing) & 1);
   }
+
+  if ((P.dbg & 16) && lane == 0)  // diagnostic: slowest warp (cycles << 24 | warp)
+    atomicMax(&P.st->err_index, ((unsigned long long)(clock64() - t_start) << 24) | gw);
 
   // ---- per-warp summaries for the cross-range check and first-occurrence keys
   __syncwarp();
@@ -682,15 +956,7 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
   // ---- CTA epilogue: drain caches, one global merge
   acc.drain();
   atomicMax(&C.max_dev, my_max_dev);
-  if (n_incompat) atomicAdd(&C.diag[CT_DIAG_INCOMPATIBLE], n_incompat);
-  if (n_dupdev) atomicAdd(&C.diag[CT_DIAG_DUPLICATE_DEVICE], n_dupdev);
-  if (n_mismatch) atomicAdd(&C.diag[CT_DIAG_MISMATCHED_P2P], n_mismatch);
-  if (cf0 != kNone) atomicMin(&C.copy_first[0], cf0);
-  if (cf1 != kNone) atomicMin(&C.copy_first[1], cf1);
-  if (cf2 != kNone) atomicMin(&C.copy_first[2], cf2);
   if (acc.flags | wflags) atomicOr(&C.flags, acc.flags | wflags);
-  if (acc.oor_key != kNone) atomicMin(&P.st->oor_key, acc.oor_key);
-  if (acc.of_cell != kNone) atomicMin(&P.st->of_cell, acc.of_cell);
   __syncthreads();
 
   GlobalState* G = P.st;
@@ -720,6 +986,8 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
   if (tid == 0) {
     if (C.flags) atomicOr(&G->flags, C.flags);
     atomicMax(&G->max_dev, C.max_dev);
+    if (C.oor_key != kNone) atomicMin(&G->oor_key, C.oor_key);
+    if (C.of_cell != kNone) atomicMin(&G->of_cell, C.of_cell);
   }
 }
 
