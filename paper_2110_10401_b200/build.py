@@ -11,16 +11,17 @@ import subprocess
 import sys
 
 PKG = os.path.dirname(os.path.abspath(__file__))
+OUT = os.environ.get("CT_BUILD_OUT", "")  # variant builds: alternate output directory
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-LIB = os.path.join(PKG, "libcommtrace_b200.so")
+LIB = os.path.join(OUT or PKG, "libcommtrace_b200.so")
 SOURCES = ["ct_api.cu", "ct_fast.cu", "ct_exact.cu", "ct_emit.cu", "ct_gen.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
     "-I", os.path.join(ROOT, "include"),
-]
+] + os.environ.get("CT_NVCC_EXTRA", "").split()
 
 
 def _stale() -> bool:
@@ -35,12 +36,13 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
     objs = []
-    os.makedirs(os.path.join(PKG, "_obj"), exist_ok=True)
+    obj_dir = os.path.join(OUT or PKG, "_obj")
+    os.makedirs(obj_dir, exist_ok=True)
     for src in SOURCES:
         path = os.path.join(CSRC, src)
         if not os.path.exists(path):
             continue
-        obj = os.path.join(PKG, "_obj", src.replace(".cu", ".o"))
+        obj = os.path.join(obj_dir, src.replace(".cu", ".o"))
         cmd = [NVCC, *FLAGS, "-c", path, "-o", obj]
         if verbose:
             print(" ".join(cmd))

@@ -101,7 +101,7 @@ struct RunOut {
 
 // One pass of the fast kernel + the cross-range order check over ``recs``.
 int run_fast(ct_context* c, const ct_record* recs, uint64_t n, int gcap, bool explicit_d,
-             const ExpandParams& ex, uint32_t n_comms, cudaStream_t st, RunOut* out) {
+                  const ExpandParams& ex, uint32_t n_comms, cudaStream_t st, RunOut* out) {
   const int g2 = gcap + 2;
   const size_t ncell = (size_t)kTypes * g2 * g2;
   if (ensure(c, c->cells, c->cells_cap, 2 * ncell)) return CT_ERR_CUDA;

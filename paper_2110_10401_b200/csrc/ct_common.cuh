@@ -42,9 +42,7 @@ enum : uint32_t {
   F_BAD_RING = 1u << 4,   // invalid ring order used by a ring instance
   F_WRONG_ALGO = 1u << 5,
   F_MISSING_ROOT = 1u << 6,
-  F_CHAIN_CAP = 1u << 7,  // per-CTA chain table full
   F_COMM_RANGE = 1u << 8, // comm id >= n_comms
-  F_CHAIN_BIG = 1u << 9,  // cross-CTA chain list too long for the single-CTA sort
 };
 
 __host__ __device__ inline int dtype_width(int code) {

@@ -1,4 +1,4 @@
-// Fast path: warp-autonomous streaming layout check + join + expand + accumulate
+// Fast path: element-parallel streaming layout check + join + expand + accumulate
 // (design notes in ct_fast.cuh).
 #include "ct_fast.cuh"
 
@@ -9,36 +9,31 @@ namespace {
 constexpr uint64_t kNone = ~0ull;
 constexpr uint32_t kEmptyTag = 0xFFFFFFFFu;
 constexpr unsigned kFull = 0xFFFFFFFFu;
-
-// A block signature seen valid in the warp's steady communicator, and how many later
-// blocks repeated it exactly (same signature and devices) without being expanded yet.
-struct __align__(16) Tpl {
-  unsigned long long count;
-  uint32_t sig;   // coll_sig(); 0 = empty entry
-  uint32_t ndef;  // deferred repeats
-};
-constexpr int kTSets = 16;          // 2-way set-associative template table
-constexpr int kTE = 2 * kTSets;
-static_assert(kTE == 32, "one template entry per lane");
+constexpr uint32_t kQM = kQ - 1;
+static_assert((kQ & (kQ - 1)) == 0 && kQ >= 64, "queue holds < 32 carried + 32 new heads");
 
 struct __align__(16) WarpMem {
-  ct_record ring[kRing][32];                 // TMA ring: chunk k lives in slot (k - k0) % kRing
-  Tpl tpl[kTE];
+  ct_record ring[kRing][32];                 // TMA ring: chunk k lives in slot k % kRing
+  unsigned long long cseq[kCS][kMaxN];       // last collective block of the comm: seq per rank
   unsigned long long bar[kRing];
-  unsigned long long cseq[kCS][kMaxN];       // last collective block: seq per rank
   unsigned long long cfirst[kCS], clast[kCS];
   unsigned long long tfirst[kCS][5];
-  uint16_t cdev[kCS][kMaxN];                 // last collective block: device per rank
+  uint32_t q[kQ];                            // element queue: ring-relative head positions
   uint32_t tag[kCS];                         // comm id of the slot
   uint32_t sn[kCS];                          // collective nranks of the slot (0: none yet)
-  uint32_t sver[kCS];                        // last block's devices pairwise distinct
 };
 
+constexpr int kTreeLut = 16;
+
 struct __align__(16) CtaMem {
-  unsigned long long calls[kTypes], pay_lo[kTypes], pay_hi[kTypes];
+  // per-type statistics: payload = pay_a + pay_b * 2^32 (exact, no return-value atomics)
+  unsigned long long calls[kTypes], pay_a[kTypes], pay_b[kTypes];
   unsigned long long copy_first[3];
   unsigned long long oor_key;   // min out-of-range ordering key seen by the CTA
   unsigned long long of_cell;   // min cell index whose 64-bit sum wrapped
+  // double binary tree peers for n <= kTreeLut (trees.py:57-106): .x = T1 parent, left,
+  // right ranks (bytes, 0xFF none), .y = the same in T2 mapped to ranks
+  uint2 tree_lut[kTreeLut + 1][kTreeLut];
   unsigned int diag[CT_NDIAG];
   uint32_t flags;
   int max_dev;
@@ -49,6 +44,10 @@ static_assert(sizeof(CtaMem) % 16 == 0, "histogram after CtaMem must stay aligne
 static_assert(sizeof(WarpMem) * kWarps + sizeof(CtaMem) + kTypes * 18 * 18 * 12 <= 227 * 1024,
               "shared memory budget: CTA histogram no longer fits for d <= 16");
 
+#ifndef CT_SLACK
+#define CT_SLACK 1
+#endif
+constexpr uint32_t kDrainSlack = CT_SLACK;  // chunks of read-ahead kept free for the TMA ring
 constexpr uint32_t kRM = kRing * 32 - 1;  // ring index mask (kRing is a power of two)
 static_assert((kRing & (kRing - 1)) == 0, "kRing must be a power of two");
 
@@ -87,14 +86,7 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t pari
   }
 }
 
-// conflict-free 32-B record read from shared memory: lanes alternate which 16-B half
-// they fetch first so each quarter-warp covers all 32 banks
-__device__ __forceinline__ Rec load_swz(const ct_record* base, int i) {
-  const uint4* q = reinterpret_cast<const uint4*>(base + i);
-  const int f = (i >> 2) & 1;
-  const uint4 x = q[f], y = q[f ^ 1];
-  return f ? unpack(y, x) : unpack(x, y);
-}
+__device__ __forceinline__ Rec ring_rec(const ct_record* R, uint32_t pos) { return load_shared(R + (pos & kRM)); }
 
 __device__ __forceinline__ bool is_start(int kind, uint32_t rank) {
   return kind == CT_KIND_COLLECTIVE ? rank == 0
@@ -121,243 +113,195 @@ __device__ uint64_t first_start(const ct_record* g, uint64_t n, uint64_t x, bool
 }
 
 // ------------------------------------------------------------ accumulation
-// Histogram location: the CTA's shared-memory copy right after CtaMem (SH), else global.
+// CTA histogram (SH): per cell the byte sum as two 32-bit limbs (lo[ncell], hi[ncell]) and
+// a 32-bit frequency, all updated with native shared-memory atomics (a 64-bit shared
+// atomic add is a CAS loop).  Without SH the cells are the global 64-bit arrays.
 template <bool SH>
-__device__ __forceinline__ unsigned long long* hist_bytes(const FastParams& P) {
-  return SH ? reinterpret_cast<unsigned long long*>(&cta_mem() + 1) : P.cells;
+__device__ __forceinline__ uint32_t* hist_lo(const FastParams& P) {
+  return reinterpret_cast<uint32_t*>(&cta_mem() + 1);
 }
-template <bool SH>
-__device__ __forceinline__ void* hist_freq(const FastParams& P) {
-  return SH ? static_cast<void*>(hist_bytes<SH>(P) + kTypes * P.g2 * P.g2) : static_cast<void*>(P.freq);
+__device__ __forceinline__ void note_min_smem(unsigned long long* slot, unsigned long long v) {
+  if (v < *slot) atomicMin(slot, v);
 }
 
-__device__ __forceinline__ void note_overflow(uint32_t& flags, unsigned long long key) {
-  flags |= F_OVERFLOW;
-  if (key < cta_mem().of_cell) atomicMin(&cta_mem().of_cell, key);
+// an endpoint >= gcap: EndpointOutOfRange with explicit d, else a rerun with a wider table
+__device__ __noinline__ uint32_t oor(unsigned long long rec_key, int sub, bool src_bad, int explicit_d) {
+  const unsigned long long k = rec_key | ((unsigned long long)min(sub, 1023) << 1);
+  note_min_smem(&cta_mem().oor_key, src_bad ? k : (k | 1));
+  return explicit_d ? F_OOR : F_CAP;
 }
 
-template <bool SH>  // SH: CTA histogram in shared memory (else global atomics)
-struct Acc {
-  // two small register caches: transfer cells and per-type statistics; a miss evicts the
-  // older entry into the CTA histogram (shared-memory atomics).  Everything else (the
-  // histogram, limits, first-error keys) comes from the kernel parameters / shared memory.
-  uint32_t ctag[2], stag[2];
-  unsigned long long csum[2], ssum[2];
-  uint32_t ccnt[2], scnt[2];
+__device__ __noinline__ uint32_t note_overflow(unsigned long long key) {
+  note_min_smem(&cta_mem().of_cell, key);
+  return F_OVERFLOW;
+}
+
+__device__ __noinline__ void flush_stat(uint32_t t, unsigned long long v, uint32_t c) {
+  CtaMem& C = cta_mem();
+  atomicAdd(&C.pay_a[t], v & 0xFFFFFFFFull);
+  atomicAdd(&C.pay_b[t], v >> 32);
+  atomicAdd(&C.calls[t], (unsigned long long)c);
+}
+
+// Transfers are added straight into the CTA histogram; statistics of the collective
+// types and sendrecv (types 0..5) accumulate in registers until the end (or a wrap).
+template <bool SH>
+struct Sink {
+  const FastParams& P;
   uint32_t flags;
   unsigned long long rec_key;  // (class << 62) | (element << 21) | (src rank << 11) for oor ordering
-  const FastParams& P;
+  unsigned long long ssum[6];
+  uint32_t scnt[6];
+  uint32_t nc;  // cells per array
 
-  __device__ __forceinline__ explicit Acc(const FastParams& p) : P(p) {
-    ctag[0] = ctag[1] = stag[0] = stag[1] = kEmptyTag;
-    csum[0] = csum[1] = ssum[0] = ssum[1] = 0;
-    ccnt[0] = ccnt[1] = scnt[0] = scnt[1] = 0;
+  __device__ __forceinline__ explicit Sink(const FastParams& p) : P(p) {
+    nc = (uint32_t)(kTypes * p.g2 * p.g2);
     flags = 0;
     rec_key = 0;
+#pragma unroll
+    for (int k = 0; k < 6; k++) { ssum[k] = 0; scnt[k] = 0; }
   }
 
-  __device__ __forceinline__ void flush_cell(uint32_t key, unsigned long long v, uint32_t c) {
-    const unsigned long long old = atomicAdd(hist_bytes<SH>(P) + key, v);
-    if (old + v < old) note_overflow(flags, key);
-    if (SH) atomicAdd(static_cast<unsigned int*>(hist_freq<SH>(P)) + key, c);
-    else atomicAdd(static_cast<unsigned long long*>(hist_freq<SH>(P)) + key, (unsigned long long)c);
-  }
-
-  __device__ __forceinline__ void flush_stat(uint32_t t, unsigned long long v, uint32_t c) {
-    CtaMem& C = cta_mem();
-    const unsigned long long old = atomicAdd(&C.pay_lo[t], v);
-    if (old + v < old) atomicAdd(&C.pay_hi[t], 1ull);
-    atomicAdd(&C.calls[t], (unsigned long long)c);
-  }
-
-  __device__ __forceinline__ void add_cell(uint32_t key, unsigned long long v) {
-    if (ctag[0] == key) {
-      const unsigned long long s = csum[0] + v;
-      if (s < v) note_overflow(flags, key);
-      csum[0] = s; ccnt[0]++;
-    } else if (ctag[1] == key) {
-      const unsigned long long s = csum[1] + v;
-      if (s < v) note_overflow(flags, key);
-      csum[1] = s; ccnt[1]++;
+  __device__ __forceinline__ void add(uint32_t key, unsigned long long v, uint32_t c = 1) {
+    if (SH) {
+      uint32_t* lo = hist_lo<SH>(P);
+      const uint32_t vlo = (uint32_t)v, vhi = (uint32_t)(v >> 32);  // v < 2^63
+      const uint32_t old = atomicAdd(lo + key, vlo);
+      const uint32_t inc = vhi + (old + vlo < old ? 1u : 0u);
+      if (inc) {
+        const uint32_t oh = atomicAdd(lo + nc + key, inc);
+        if (oh + inc < oh) flags |= note_overflow(key);  // the 64-bit cell wrapped
+      }
+      atomicAdd(lo + 2 * nc + key, c);
     } else {
-      if (ctag[1] != kEmptyTag) flush_cell(ctag[1], csum[1], ccnt[1]);
-      ctag[1] = ctag[0]; csum[1] = csum[0]; ccnt[1] = ccnt[0];
-      ctag[0] = key; csum[0] = v; ccnt[0] = 1;
+      const unsigned long long old = atomicAdd(P.cells + key, v);
+      if (old + v < old) flags |= note_overflow(key);
+      atomicAdd(P.freq + key, (unsigned long long)c);
     }
-  }
-
-  // payload sums are 128-bit in the CTA: flush before a register entry would wrap
-  __device__ __forceinline__ void add_stat(uint32_t t, unsigned long long v) {
-    if (stag[0] == t) {
-      if (ssum[0] + v < v) { flush_stat(t, ssum[0], scnt[0]); ssum[0] = v; scnt[0] = 1; }
-      else { ssum[0] += v; scnt[0]++; }
-    } else if (stag[1] == t) {
-      if (ssum[1] + v < v) { flush_stat(t, ssum[1], scnt[1]); ssum[1] = v; scnt[1] = 1; }
-      else { ssum[1] += v; scnt[1]++; }
-    } else {
-      if (stag[1] != kEmptyTag) flush_stat(stag[1], ssum[1], scnt[1]);
-      stag[1] = stag[0]; ssum[1] = ssum[0]; scnt[1] = scnt[0];
-      stag[0] = t; ssum[0] = v; scnt[0] = 1;
-    }
-  }
-
-  __device__ __forceinline__ void drain() {
-    if (ctag[0] != kEmptyTag) flush_cell(ctag[0], csum[0], ccnt[0]);
-    if (ctag[1] != kEmptyTag) flush_cell(ctag[1], csum[1], ccnt[1]);
-    if (stag[0] != kEmptyTag) flush_stat(stag[0], ssum[0], scnt[0]);
-    if (stag[1] != kEmptyTag) flush_stat(stag[1], ssum[1], scnt[1]);
-    ctag[0] = ctag[1] = stag[0] = stag[1] = kEmptyTag;
-  }
-
-  // stats: calls += 1, payload += s (128-bit capable)
-  __device__ __forceinline__ void stat(int type, unsigned __int128 s) {
-    if ((s >> 63) == 0) { add_stat((uint32_t)type, (unsigned long long)s); return; }
-    CtaMem& C = cta_mem();
-    const unsigned long long lo = (unsigned long long)s;
-    unsigned long long hi = (unsigned long long)(s >> 64);
-    const unsigned long long old = atomicAdd(&C.pay_lo[type], lo);
-    if (old + lo < old) hi += 1;
-    atomicAdd(&C.pay_hi[type], hi);
-    atomicAdd(&C.calls[type], 1ull);
-  }
-
-  __device__ __forceinline__ void out_of_range(unsigned long long k) {
-    flags |= P.explicit_d ? F_OOR : F_CAP;
-    if (k < cta_mem().oor_key) atomicMin(&cta_mem().oor_key, k);
   }
 
   // endpoint: gpu g (>= 0), -1 host, -2 net.  ``sub`` orders transfers inside one
   // decomposition (destination rank of a collective edge, transfers are sorted by rank
   // pair, decompose.py:92; 0/1 for collnet) for the EndpointOutOfRange message.
   __device__ __forceinline__ void edge(int type, int src, int dst, unsigned __int128 bytes, int sub = 0) {
-    const int a = src == -1 ? kHost : (src == -2 ? kNet : src + 2);
-    const int b = dst == -1 ? kHost : (dst == -2 ? kNet : dst + 2);
     if (src >= P.gcap || dst >= P.gcap) {
-      const unsigned long long k = rec_key | ((unsigned long long)min(sub, 1023) << 1);
-      if (src >= P.gcap) out_of_range(k);
-      if (dst >= P.gcap) out_of_range(k | 1);
+      flags |= oor(rec_key, sub, src >= P.gcap, P.explicit_d);
       return;
     }
-    if ((bytes >> 63) != 0) { flags |= F_OVERFLOW; return; }
-    add_cell((uint32_t)((type * P.g2 + a) * P.g2 + b), (unsigned long long)bytes);
+    if ((bytes >> 63) != 0) { flags |= F_OVERFLOW; return; }  // one transfer alone exceeds a cell
+    const int a = src == -1 ? kHost : (src == -2 ? kNet : src + 2);
+    const int b = dst == -1 ? kHost : (dst == -2 ? kNet : dst + 2);
+    add((uint32_t)((type * P.g2 + a) * P.g2 + b), (unsigned long long)bytes);
+  }
+
+  // stats: calls += 1, payload += s (128-bit capable; s < 2^72)
+  __device__ __forceinline__ void stat(int type, unsigned __int128 s) {
+    if ((s >> 63) == 0 && type < 6) {
+      const unsigned long long v = (unsigned long long)s;
+#pragma unroll
+      for (int k = 0; k < 6; k++)
+        if (type == k) {
+          if (ssum[k] + v < v) { flush_stat(k, ssum[k], scnt[k]); ssum[k] = 0; scnt[k] = 0; }
+          ssum[k] += v;
+          scnt[k]++;
+        }
+      return;
+    }
+    CtaMem& C = cta_mem();
+    atomicAdd(&C.pay_a[type], (unsigned long long)s & 0xFFFFFFFFull);
+    atomicAdd(&C.pay_b[type], (unsigned long long)(s >> 32));
+    atomicAdd(&C.calls[type], 1ull);
+  }
+
+  __device__ __forceinline__ void drain() {
+#pragma unroll
+    for (int k = 0; k < 6; k++)
+      if (scnt[k]) flush_stat(k, ssum[k], scnt[k]);
   }
 };
 
-// device of a record held in the warp's ring, by position relative to the ring origin
+// Register accumulator for uniform ring-family instances over an identity ring whose
+// devices (n <= 8, packed one per byte) are all < gcap.  The edge leaving position q
+// carries gen + dlt * ([q == n-2] + [q == n-3]) (mod n): ring allreduce with every block
+// but the last full (gen = 2S - 2 chunk, dlt = chunk - last block), allgather /
+// reduce-scatter (gen = (n-1) * block, dlt = 0).  Instances with the same (type, n,
+// devices) add into 128-bit sums; the n cells are written when the key changes.
+template <bool SH>
+__device__ __noinline__ uint32_t flush_ring(const FastParams& P, int g2, uint32_t nc, uint32_t tag,
+                                            unsigned long long devs, unsigned long long g_lo, uint32_t g_hi,
+                                            unsigned long long d_lo, uint32_t d_hi, uint32_t cnt) {
+  Sink<SH> sk(P);
+  const int coll = tag & 0xFF, n = (int)(tag >> 8);
+  const int a = n - 2, b = n >= 3 ? n - 3 : n - 1;
+  for (int q = 0; q < n; q++) {
+    const int qn = q + 1 == n ? 0 : q + 1;
+    const uint32_t k = (uint32_t)(q == a) + (uint32_t)(q == b);
+    // v = g + k * d as 128 bits
+    unsigned long long lo = g_lo;
+    unsigned __int128 hi = g_hi;
+    for (uint32_t t = 0; t < k; t++) {
+      const unsigned long long x = lo + d_lo;
+      hi += (unsigned __int128)d_hi + (x < lo ? 1u : 0u);
+      lo = x;
+    }
+    const uint32_t key = (uint32_t)((coll * g2 + (int)((devs >> (8 * q)) & 0xFF) + 2) * g2 +
+                                    (int)((devs >> (8 * qn)) & 0xFF) + 2);
+    if (hi != 0 || (lo >> 63) != 0) sk.flags |= note_overflow(key);  // the cell exceeds 2^63 - 1
+    else sk.add(key, lo, cnt);
+  }
+  return sk.flags;
+}
+
+struct RingAcc {
+  uint32_t tag;                 // coll | n << 8 (0: empty)
+  unsigned long long devs;
+  unsigned long long g_lo, d_lo;
+  uint32_t g_hi, d_hi, cnt;
+  uint32_t miss;                // consecutive instances that did not match the key
+
+  template <bool SH>
+  __device__ __forceinline__ void flush(Sink<SH>& sk, int g2) {
+    sk.flags |= flush_ring<SH>(sk.P, g2, sk.nc, tag, devs, g_lo, g_hi, d_lo, d_hi, cnt);
+  }
+
+  // false: the key differs and is kept (the caller expands the instance itself); after a
+  // streak of misses the accumulator is flushed and re-keyed
+  template <bool SH>
+  __device__ __forceinline__ bool add(Sink<SH>& sk, int g2, uint32_t t, unsigned long long dv, unsigned long long g,
+                                      unsigned long long d) {
+    if (t != tag || dv != devs) {
+      if (tag && ++miss < 8) return false;
+      if (tag) flush(sk, g2);
+      tag = t; devs = dv;
+      g_lo = d_lo = 0; g_hi = d_hi = cnt = 0;
+    }
+    miss = 0;
+    const unsigned long long x = g_lo + g, y = d_lo + d;
+    g_hi += x < g ? 1u : 0u;
+    d_hi += y < d ? 1u : 0u;
+    g_lo = x; d_lo = y;
+    cnt++;
+    if (cnt == 0xFFFFFFFFu) { flush(sk, g2); tag = 0; }
+    return true;
+  }
+};
+
+// device of a record held in the warp's ring, by ring-relative position
 struct WinDev {
   const ct_record* R;
   __device__ __forceinline__ uint32_t dev_of(uint64_t rel) const { return R[(uint32_t)rel & kRM].dev; }
 };
 
-// signature word of a collective record: coll, has_root, algo, dtype, root when rooted
-// (grouping.py:78-79 without count), bit 7 set so an empty entry (0) never matches
-__device__ __forceinline__ uint32_t coll_sig(uint32_t a2 /* kc | ad << 8 | aux << 16 */) {
-  return (a2 & (0x3F78u | ((a2 & 0x40u) ? 0xFFFF0000u : 0u))) | 0x80u;
-}
-
-__device__ __forceinline__ uint32_t tpl_set(unsigned long long count, uint32_t sig) {
-  const uint32_t h = ((uint32_t)count ^ ((uint32_t)(count >> 32) * 0x85EBCA6Bu) ^ (sig * 0xC2B2AE35u)) * 0x9E3779B1u;
-  return h >> 28;  // kTSets == 16
-}
-
-// ------------------------------------------------------------ out-of-line sinks
-// Sink that adds every transfer ``c`` times straight into the CTA histogram: bytes * c
-// into the cell, c into the frequency, S * c into the 128-bit payload and c calls.  Used
-// for deferred repeats (c identical blocks) and for the rare > 2^40-element records.
-template <bool SH>
-struct DirectSink {
-  unsigned long long* hb;
-  void* hf;
-  int g2, gcap, explicit_d;
-  unsigned long long rec_key;
-  unsigned long long c;
-  uint32_t flags;
-  __device__ __forceinline__ void stat(int type, unsigned __int128 s) {
-    CtaMem& C = cta_mem();
-    const unsigned __int128 v = s * c;
-    const unsigned long long lo = (unsigned long long)v;
-    unsigned long long hi = (unsigned long long)(v >> 64);
-    const unsigned long long old = atomicAdd(&C.pay_lo[type], lo);
-    if (old + lo < old) hi++;
-    if (hi) atomicAdd(&C.pay_hi[type], hi);
-    atomicAdd(&C.calls[type], c);
-  }
-  __device__ __forceinline__ void edge(int type, int src, int dst, unsigned __int128 bytes, int sub) {
-    if (src >= gcap || dst >= gcap) {  // same ordering key as Acc::edge
-      const unsigned long long k = rec_key | ((unsigned long long)min(sub, 1023) << 1);
-      flags |= explicit_d ? F_OOR : F_CAP;
-      const unsigned long long kk = src >= gcap ? k : (k | 1);
-      if (kk < cta_mem().oor_key) atomicMin(&cta_mem().oor_key, kk);
-      return;
-    }
-    const int a = src == -1 ? kHost : (src == -2 ? kNet : src + 2);
-    const int b = dst == -1 ? kHost : (dst == -2 ? kNet : dst + 2);
-    const unsigned long long key = (unsigned long long)((type * g2 + a) * g2 + b);
-    const unsigned __int128 v = bytes * c;
-    if ((v >> 63) != 0) {  // one transfer alone exceeds the cell (as Acc::edge); c repeats do by summing
-      if (c == 1) flags |= F_OVERFLOW;
-      else note_overflow(flags, key);
-      return;
-    }
-    const unsigned long long old = atomicAdd(hb + key, (unsigned long long)v);
-    if (old + (unsigned long long)v < old) note_overflow(flags, key);
-    if (SH) atomicAdd(static_cast<unsigned int*>(hf) + key, (unsigned int)c);
-    else atomicAdd(static_cast<unsigned long long*>(hf) + key, c);
-  }
-};
-
 // a collective record with count >= 2^40 (128-bit byte counts): rare, kept out of line
 template <bool SH>
-__device__ __noinline__ uint32_t expand_wide(ExpandParams ex, unsigned long long* hb, void* hf, int g2, int gcap,
-                                             int explicit_d, unsigned long long rec_key, Rec me, uint32_t head,
-                                             const ct_record* R) {
-  DirectSink<SH> ds{hb, hf, g2, gcap, explicit_d, rec_key, 1ull, 0u};
+__device__ __noinline__ uint32_t expand_wide(const FastParams& P, const ct_record* R, Rec rc, uint32_t head,
+                                             unsigned long long rec_key) {
   const WinDev wdv{R};
-  expand_collective<unsigned __int128>(ex, wdv, ds, me, head);
-  return ds.flags;
-}
-
-struct TblDev {  // devices of the steady communicator's last block, by rank
-  const uint16_t* cd;
-  __device__ __forceinline__ uint32_t dev_of(uint64_t r) const { return cd[(uint32_t)r]; }
-};
-
-// Expand every template with deferred repeats (lane = rank) and clear the counters;
-// returns error flags.
-template <bool SH>
-__device__ __noinline__ uint32_t flush_templates(ExpandParams ex, unsigned long long* hb, void* hf, int g2, WarpMem& W,
-                                                 int ts, uint32_t tcomm, uint32_t tn) {
-  const int lane = threadIdx.x & 31;
-  uint32_t flags = 0;
-  unsigned todo = __ballot_sync(kFull, W.tpl[lane].ndef != 0);  // kTE == 32
-  while (todo) {
-    const int e = __ffs(todo) - 1;
-    todo &= todo - 1;
-    const unsigned long long c = W.tpl[e].ndef;
-    if ((uint32_t)lane < tn) {
-      const uint32_t sg = W.tpl[e].sig;
-      Rec rc;
-      rc.count = W.tpl[e].count;
-      rc.seq = 0;
-      rc.comm = tcomm;
-      rc.nranks = tn;
-      rc.rank = (uint32_t)lane;
-      rc.dev = W.cdev[ts][lane];
-      rc.aux = sg >> 16;
-      rc.aux2 = 0;
-      rc.kc = sg & 0x78u;
-      rc.ad = (sg >> 8) & 0x3Fu;
-      DirectSink<SH> ds{hb, hf, g2, 1 << 30, 0, 0ull, c, 0u};  // steady devices are < gcap
-      const TblDev td{W.cdev[ts]};
-      if ((rc.count >> 40) == 0) expand_collective<uint64_t>(ex, td, ds, rc, 0);
-      else expand_collective<unsigned __int128>(ex, td, ds, rc, 0);
-      flags |= ds.flags;
-    }
-  }
-  __syncwarp();
-  W.tpl[lane].ndef = 0;
-  __syncwarp();
-  return flags;
+  Sink<SH> sk(P);
+  sk.rec_key = rec_key;
+  expand_collective<unsigned __int128>(P.ex, wdv, sk, rc, head);
+  sk.drain();
+  return sk.flags;
 }
 
 __device__ __forceinline__ int find_slot(const WarpMem& W, uint32_t comm) {
@@ -368,96 +312,36 @@ __device__ __forceinline__ int find_slot(const WarpMem& W, uint32_t comm) {
   return s;
 }
 
-// no set bit in [lo, lo + len) of a 64-bit window mask (lo + len <= 64)
-__device__ __forceinline__ bool range_clear(unsigned long long mask64, uint32_t lo, uint32_t len) {
-  if (len == 0) return true;
-  const unsigned long long m = len >= 64 ? ~0ull : ((1ull << len) - 1);
-  return ((mask64 >> lo) & m) == 0;
-}
-
-__device__ __forceinline__ void note_min_smem(unsigned long long* slot, unsigned long long v) {
-  if (v < *slot) atomicMin(slot, v);
-}
-
-// Predecessor check of a non-start element member.  q0..q4 are the predecessor's words
-// (comm | nranks, rank | kc, ad, aux | count lo | count hi); w2 is the member's own kc/ad/aux.
-// Collective members must continue their block (same comm and nranks, rank + 1); the
-// signature (coll, algo, count, dtype, root; grouping.py:78-79) must match, otherwise the
-// block is incompatible.  A recv must follow its counterpart send (decompose.py:323-330);
-// count/dtype disagreement makes the pair mismatched (decompose.py:362-372).
-__device__ __forceinline__ void member_check(const Rec& me, uint32_t w2, uint32_t q0, uint32_t q1, uint32_t q2,
-                                             uint32_t q3, uint32_t q4, bool& sfail, bool& gfail, bool& mis) {
-  const int kind = me.kind();
-  const uint32_t pk = q2 & 7;
-  if (kind == CT_KIND_COLLECTIVE) {
-    if (pk != CT_KIND_COLLECTIVE || q0 != me.comm || (q1 & 0xFFFF) != me.nranks || (q1 >> 16) + 1 != me.rank) {
-      sfail = true;
-      return;
-    }
-    const uint32_t m = 0x3F78u | (me.has_root() ? 0xFFFF0000u : 0u);
-    if (((q2 ^ w2) & m) != 0 || q3 != (uint32_t)me.count || q4 != (uint32_t)(me.count >> 32)) gfail = true;
-  } else if (kind == CT_KIND_RECV) {
-    if (pk != CT_KIND_SEND || q0 != me.comm || (q1 >> 16) != me.aux || (q2 >> 16) != me.rank) {
-      sfail = true;
-      return;
-    }
-    if (q3 != (uint32_t)me.count || q4 != (uint32_t)(me.count >> 32) || ((q2 >> 10) & 15) != (uint32_t)me.dtype())
-      mis = true;
-  } else {
-    sfail = true;  // sends, copies and unknown kinds never continue an element
-  }
-}
-
-// seq order of a collective member against the same rank of the comm's previous block
-// (in-window ``pseq`` or the per-warp table) and device inheritance from the table
-__device__ __forceinline__ void order_check(const WarpMem& W, const Rec& me, uint32_t info, uint64_t pseq,
-                                            uint32_t& wflags, bool& devf) {
-  const int s = info & 15;
-  const uint32_t r = me.rank;
-  bool have = (info & (1u << 10)) != 0;
-  if (!have && (info & (1u << 11))) { pseq = W.cseq[s][r]; have = true; }
-  if (have && !(pseq < me.seq)) wflags |= F_NONCANON;  // strictly increasing per (comm, rank)
-  devf = !((info & (1u << 12)) && W.cdev[s][r] == me.dev);
-}
-
-// pairwise-distinct devices of the block of n records starting at ring index i0
-__device__ __noinline__ bool devices_distinct(const ct_record* R, uint32_t i0, uint32_t n) {
-  uint64_t seen0 = 0, seen1 = 0, seen2 = 0, seen3 = 0;
-  for (uint32_t m = 0; m < n; m++) {
-    const uint32_t d = R[(i0 + m) & kRM].dev;
-    if (d < 256) {
-      const uint64_t bit = 1ull << (d & 63);
-      const uint32_t wi = d >> 6;
-      const uint64_t wd = wi == 0 ? seen0 : wi == 1 ? seen1 : wi == 2 ? seen2 : seen3;
-      if (wd & bit) return false;
-      if (wi == 0) seen0 |= bit; else if (wi == 1) seen1 |= bit; else if (wi == 2) seen2 |= bit; else seen3 |= bit;
-    } else {
-      for (uint32_t m2 = 0; m2 < m; m2++)
-        if (R[(i0 + m2) & kRM].dev == d) return false;
-    }
+// pairwise-distinct devices of the block of n records starting at ring position p
+__device__ __noinline__ bool devices_distinct(const ct_record* R, uint32_t p, uint32_t n) {
+  for (uint32_t m = 1; m < n; m++) {
+    const uint32_t d = R[(p + m) & kRM].dev;
+    for (uint32_t m2 = 0; m2 < m; m2++)
+      if (R[(p + m2) & kRM].dev == d) return false;
   }
   return true;
 }
 
 // p2p order: per (comm, src, dst) channel, send seqs and recv seqs non-decreasing in file
-// order (then FIFO-by-position pairing equals the reference's seq-sorted pairing)
-__device__ __forceinline__ void p2p_order(P2PEntry* chan, const Rec& ra, uint64_t next_seq, bool sendA, int lane,
-                                          uint32_t& wflags) {
+// order (then FIFO-by-position pairing equals the reference's seq-sorted pairing).  Lanes
+// hold send/recv pairs in file order (lane = element).
+__device__ __noinline__ uint32_t p2p_order(P2PEntry* chan, const Rec ra, uint64_t next_seq, bool sendA, int lane) {
+  uint32_t wflags = 0;
   const unsigned lt = (1u << lane) - 1;
   const unsigned gt = lane == 31 ? 0u : ~((2u << lane) - 1);
   uint64_t key = 0xFFFFFFFF00000000ull | lane, sseq = 0, rseq = 0;
-  if (sendA) {  // the recv is the next record (elements are whole inside a window)
+  if (sendA) {
     key = ((uint64_t)ra.comm << 32) | ((uint64_t)ra.rank << 16) | ra.aux;
     sseq = ra.seq;
     rseq = next_seq;
   }
   const unsigned m = __match_any_sync(kFull, key);
   const unsigned lower = m & lt;
-  const int pl = lower ? 31 - __clz(lower) : -1;  // in-window previous pair of the channel
+  const int pl = lower ? 31 - __clz(lower) : -1;  // previous pair of the channel in this batch
   const uint64_t ps = __shfl_sync(kFull, sseq, pl < 0 ? lane : pl);
   const uint64_t pr = __shfl_sync(kFull, rseq, pl < 0 ? lane : pl);
   int e = -1;
-  if (sendA && !lower) {  // first pair of the channel in this window: channel table
+  if (sendA && !lower) {  // first pair of the channel in this batch: channel table
     uint32_t h = (uint32_t)((key * 0x9E3779B97F4A7C15ull) >> 58) % kPC;
     for (int probe = 0; probe < kPC; probe++, h = (h + 1) % kPC) {
       const unsigned long long old = atomicCAS(reinterpret_cast<unsigned long long*>(&chan[h].key), kNone, key);
@@ -480,44 +364,155 @@ __device__ __forceinline__ void p2p_order(P2PEntry* chan, const Rec& ra, uint64_
   __syncwarp();
   if (sendA && (m & gt) == 0 && e_grp >= 0) { chan[e_grp].last_s = sseq; chan[e_grp].last_r = rseq; }
   __syncwarp();
+  return wflags;
 }
 
-// expansion + accumulation of one record of a processed element (status ``st``); ``rel``
-// and ``head`` are positions relative to the ring origin ``rb0``
-template <bool SH>
-__device__ __forceinline__ void expand_record(const FastParams& P, Acc<SH>& acc, const WinDev& wdv, const Rec& me,
-                                              uint64_t rb0, uint32_t rel, uint32_t st, uint32_t head, int& max_dev,
-                                              uint32_t& copy_seen) {
-  const int kind = me.kind();
-  max_dev = max(max_dev, (int)me.dev);
-  if (kind == CT_KIND_COLLECTIVE) {
-    if (st != ST_VALID) return;
-    acc.rec_key = (min((unsigned long long)(rb0 + head), (1ull << 41) - 1) << 21) | ((unsigned long long)min(me.rank, 1023u) << 11);
-    if ((me.count >> 40) == 0) expand_collective<uint64_t>(P.ex, wdv, acc, me, head);
-    else acc.flags |= expand_wide<SH>(P.ex, hist_bytes<SH>(P), hist_freq<SH>(P), P.g2, P.gcap, P.explicit_d,
-                                      acc.rec_key, me, head, wdv.R);
-  } else if (kind == CT_KIND_SEND) {
-    if (st != ST_VALID) return;
-    const unsigned __int128 nb = (unsigned __int128)me.count * (unsigned)dtype_width(me.dtype());
-    acc.stat(CT_T_SENDRECV, nb);
-    acc.rec_key = (1ull << 62) | (min((unsigned long long)(rb0 + rel), (1ull << 41) - 1) << 21);
-    const int rdev = (int)wdv.dev_of(rel + 1);
-    if (rdev != (int)me.dev) acc.edge(CT_T_SENDRECV, (int)me.dev, rdev, nb);
-  } else if (kind >= CT_KIND_MEMCPY) {
-    const int ck = me.ckind();
-    if (ck != CT_CKIND_H2D) max_dev = max(max_dev, (int)me.aux);
-    if (ck != CT_CKIND_D2H) max_dev = max(max_dev, (int)me.aux2);
-    const int t = CT_T_EXPLICIT + (kind - CT_KIND_MEMCPY);
-    acc.stat(t, (unsigned __int128)me.count);
-    acc.rec_key = (2ull << 62) | (min((unsigned long long)(rb0 + rel), (1ull << 41) - 1) << 21);
-    acc.edge(t, ck == CT_CKIND_H2D ? -1 : (int)me.aux, ck == CT_CKIND_D2H ? -1 : (int)me.aux2,
-             (unsigned __int128)me.count);
-    // first record of each copy kind: positions only grow, so a lane's first is its min
-    const uint32_t bit = 1u << (kind - CT_KIND_MEMCPY);
-    if (!(copy_seen & bit)) {
-      copy_seen |= bit;
-      atomicMin(&cta_mem().copy_first[kind - CT_KIND_MEMCPY], rb0 + rel);
+// Peers of position j in the double binary tree (trees.py:57-106, decompose.py:227-255)
+// as ``cnt`` packed 7-bit codes: rank in bits [0,5), bit 5 = T1 edge (ceil(S/2)), bit 6 =
+// T2 edge (floor(S/2), only when t2); an edge present in both trees is one transfer of S.
+__device__ __forceinline__ unsigned long long tree_peers(int n, int j, bool t2, int& cnt) {
+  int a0, a1, a2, b0 = -1, b1 = -1, b2 = -1;
+  if (n <= kTreeLut) {
+    const uint2 e = cta_mem().tree_lut[n][j];
+    a0 = (int)(e.x & 0xFF); a1 = (int)((e.x >> 8) & 0xFF); a2 = (int)((e.x >> 16) & 0xFF);
+    a0 = a0 == 0xFF ? -1 : a0; a1 = a1 == 0xFF ? -1 : a1; a2 = a2 == 0xFF ? -1 : a2;
+    if (t2) {
+      b0 = (int)(e.y & 0xFF); b1 = (int)((e.y >> 8) & 0xFF); b2 = (int)((e.y >> 16) & 0xFF);
+      b0 = b0 == 0xFF ? -1 : b0; b1 = b1 == 0xFF ? -1 : b1; b2 = b2 == 0xFF ? -1 : b2;
     }
+  } else {
+    tree_links(n, j, a0, a1, a2);  // T1: rank == position
+    if (t2) {
+      int q0, q1, q2;
+      tree_links(n, j == 0 ? n - 1 : j - 1, q0, q1, q2);  // T2: rank at position q is (q + 1) % n
+      b0 = q0 < 0 ? -1 : (q0 + 1 == n ? 0 : q0 + 1);
+      b1 = q1 < 0 ? -1 : (q1 + 1 == n ? 0 : q1 + 1);
+      b2 = q2 < 0 ? -1 : (q2 + 1 == n ? 0 : q2 + 1);
+    }
+  }
+  unsigned long long w = 0;
+  cnt = 0;
+  auto put = [&](int r, uint32_t code) {
+    w |= (unsigned long long)((uint32_t)r | (code << 5)) << (7 * cnt);
+    cnt++;
+  };
+  if (a0 >= 0) put(a0, 1u | (a0 == b0 || a0 == b1 || a0 == b2 ? 2u : 0u));
+  if (a1 >= 0) put(a1, 1u | (a1 == b0 || a1 == b1 || a1 == b2 ? 2u : 0u));
+  if (a2 >= 0) put(a2, 1u | (a2 == b0 || a2 == b1 || a2 == b2 ? 2u : 0u));
+  if (b0 >= 0 && b0 != a0 && b0 != a1 && b0 != a2) put(b0, 2u);
+  if (b1 >= 0 && b1 != a0 && b1 != a1 && b1 != a2) put(b1, 2u);
+  if (b2 >= 0 && b2 != a0 && b2 != a1 && b2 != a2) put(b2, 2u);
+  return w;
+}
+
+// Expansion + statistics of one VALID collective instance whose head (rank 0) sits at
+// ring position p; gidx is its global record index.  Rank-attributed rules (ct_common.cuh,
+// SURVEY App. A): ring family -- the record at ring position q (rank order[q]) sends to
+// order[q+1]; tree -- every rank sends to its peers in both trees; collnet -- every rank
+// sends S to NET and receives S from it.  All edges leave through one emission site.
+// Ring lanes start at different positions (j0) so their shared-memory reads spread over
+// the banks.
+template <bool SH>
+__device__ __forceinline__ void expand_block(const FastParams& P, Sink<SH>& sk, const ct_record* R, const Rec& h,
+                                             uint32_t p, uint64_t gidx, uint32_t j0, bool fastdev, bool packed,
+                                             unsigned long long devs, RingAcc& ra) {
+  const int n = (int)h.nranks, coll = h.coll();
+  const unsigned long long base = min((unsigned long long)gidx, (1ull << 41) - 1) << 21;
+  if ((h.count >> 40) != 0) {
+    for (int j = 0; j < n; j++) {
+      Rec rc = h;
+      rc.rank = (uint32_t)j;
+      rc.dev = R[(p + j) & kRM].dev;
+      sk.flags |= expand_wide<SH>(P, R, rc, p, base | ((unsigned long long)j << 11));
+    }
+    return;
+  }
+  const uint64_t blk = h.count * (uint64_t)dtype_width(h.dtype());
+  const bool scatter = coll == CT_COLL_ALLGATHER || coll == CT_COLL_REDUCESCATTER;
+  const uint64_t s = scatter ? blk * (uint64_t)n : blk;
+  int algo = h.algo();
+  if (coll == CT_COLL_ALLREDUCE) {
+    if (algo == CT_ALGO_AUTO) algo = s < P.ex.tree_threshold ? CT_ALGO_TREE : CT_ALGO_RING;
+  } else {
+    if (algo == CT_ALGO_TREE || algo == CT_ALGO_COLLNET) { sk.flags |= F_WRONG_ALGO; return; }
+    algo = CT_ALGO_RING;
+  }
+  sk.stat(coll, (unsigned __int128)s);
+  if (algo == CT_ALGO_COLLNET) {
+    if (s == 0) return;
+  } else {
+    if ((coll == CT_COLL_BROADCAST || coll == CT_COLL_REDUCE) && !h.has_root()) {
+      sk.flags |= F_MISSING_ROOT;
+      return;
+    }
+    if (n == 1 || s == 0) return;
+  }
+  const int g2 = P.g2;
+  const bool ring = algo == CT_ALGO_RING, tree = algo == CT_ALGO_TREE;
+  // ring family
+  const bool rmap = ring && n == P.ex.ring_len;
+  if (rmap && !P.ex.ring_valid) { sk.flags |= F_BAD_RING; return; }
+  const int root_pos = rmap ? (h.has_root() ? (int)P.ex.ring_inv[h.aux] : 0) : (int)h.aux;
+  const int skip_pos = coll == CT_COLL_BROADCAST ? (root_pos == 0 ? n - 1 : root_pos - 1)
+                                                 : (coll == CT_COLL_REDUCE ? root_pos : -1);
+  const uint64_t chunk = ring && coll == CT_COLL_ALLREDUCE ? ceil_div(s, (uint32_t)n) : 0;
+  // allreduce blocks b[i] (decompose.py:104-107): chunk for i < n-1 and the remainder
+  // s - (n-1)*chunk for i = n-1 unless s is tiny (then trailing blocks are empty)
+  const bool simple = ring && coll == CT_COLL_ALLREDUCE && (uint64_t)(n - 1) * chunk < s;
+  const uint64_t gen = 2 * s - 2 * chunk, dlt = chunk - (s - (uint64_t)(n - 1) * chunk);
+  const uint64_t fixed = scatter ? s - blk : s;
+  if (ring && fastdev && packed && !rmap && (simple || scatter)) {  // uniform: register accumulator
+    if (ra.add(sk, g2, (uint32_t)coll | ((uint32_t)n << 8), devs, simple ? gen : fixed, simple ? dlt : 0ull)) return;
+  }
+  // tree shares
+  const uint64_t share1 = s - s / 2, share2 = s / 2;
+  auto devof = [&](int r) -> int {
+    return packed ? (int)((devs >> (8 * r)) & 0xFF) : (int)R[(p + r) & kRM].dev;
+  };
+  int q = ring ? (int)j0 : 0;
+  for (int i = 0; i < n; i++) {
+    const int qn = q + 1 == n ? 0 : q + 1;
+    const int rs = rmap ? (int)P.ex.ring_order[q] : q;  // sending rank
+    int rd = 0, cnt;
+    uint64_t rbytes = 0;
+    unsigned long long w = 0;
+    if (ring) {
+      rd = rmap ? (int)P.ex.ring_order[qn] : qn;
+      if (coll == CT_COLL_ALLREDUCE) {
+        const int q2 = qn + 1 == n ? 0 : qn + 1;
+        rbytes = simple ? gen + (qn == n - 1 ? dlt : 0) + (q2 == n - 1 ? dlt : 0)
+                        : 2 * s - ring_block(s, chunk, qn) - ring_block(s, chunk, q2);
+      } else {
+        rbytes = q == skip_pos ? 0 : fixed;
+      }
+      cnt = rbytes != 0 ? 1 : 0;
+    } else if (tree) {
+      w = tree_peers(n, q, share2 != 0, cnt);
+    } else {
+      cnt = 2;
+    }
+    const int me = devof(rs);
+    for (int x = 0; x < cnt; x++) {
+      int src = me, dst, sub;
+      uint64_t bytes;
+      if (ring) {
+        dst = devof(rd); bytes = rbytes; sub = rd;
+      } else if (tree) {
+        const uint32_t c = (uint32_t)(w >> (7 * x));
+        sub = (int)(c & 31);
+        dst = devof(sub);
+        bytes = (c & 0x60) == 0x60 ? s : ((c & 0x20) ? share1 : share2);
+      } else {  // collnet: dev -> NET, NET -> dev
+        src = x == 0 ? me : -2; dst = x == 0 ? -2 : me; bytes = s; sub = x;
+      }
+      if (fastdev) {  // every device of the block is < gcap
+        sk.add((uint32_t)((coll * g2 + (src < 0 ? kNet : src + 2)) * g2 + (dst < 0 ? kNet : dst + 2)), bytes);
+      } else {
+        sk.rec_key = base | ((unsigned long long)rs << 11);
+        sk.edge(coll, src, dst, (unsigned __int128)bytes, sub);
+      }
+    }
+    q = qn;
   }
 }
 
@@ -526,6 +521,26 @@ __device__ __forceinline__ void count_diag(uint32_t st) {
   else if (st == ST_DUPDEV) atomicAdd(&cta_mem().diag[CT_DIAG_DUPLICATE_DEVICE], 1u);
   else if (st == ST_MISMATCH) atomicAdd(&cta_mem().diag[CT_DIAG_MISMATCHED_P2P], 1u);
 }
+
+// copy statistics: one register accumulator per copy kind
+struct CopyStats {
+  unsigned long long sum[3];
+  uint32_t cnt[3];
+  __device__ __forceinline__ void add(int t, unsigned long long v) {
+#pragma unroll
+    for (int k = 0; k < 3; k++)
+      if (t == k) {
+        if (sum[k] + v < v) { flush_stat(CT_T_EXPLICIT + k, sum[k], cnt[k]); sum[k] = 0; cnt[k] = 0; }
+        sum[k] += v;
+        cnt[k]++;
+      }
+  }
+  __device__ __forceinline__ void drain() {
+#pragma unroll
+    for (int k = 0; k < 3; k++)
+      if (cnt[k]) flush_stat(CT_T_EXPLICIT + k, sum[k], cnt[k]);
+  }
+};
 
 }  // namespace
 
@@ -541,22 +556,37 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
   WarpMem* WM = reinterpret_cast<WarpMem*>(smem_raw);
   CtaMem& C = cta_mem();
   const int ncell = kTypes * P.g2 * P.g2;
-  unsigned long long* shb = hist_bytes<true>(P);
-  unsigned int* shf = static_cast<unsigned int*>(hist_freq<true>(P));
+  uint32_t* shl = hist_lo<true>(P);  // lo limbs, then hi limbs, then frequencies
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned lt = (1u << lane) - 1;
   WarpMem& W = WM[warp];
 
   // ---- init
   if (SH)
-    for (int c = tid; c < ncell; c += kThreads) { shb[c] = 0; shf[c] = 0; }
-  if (tid < kTypes) { C.calls[tid] = 0; C.pay_lo[tid] = 0; C.pay_hi[tid] = 0; }
+    for (int c = tid; c < 3 * ncell; c += kThreads) shl[c] = 0;
+  if (tid < kTypes) { C.calls[tid] = 0; C.pay_a[tid] = 0; C.pay_b[tid] = 0; }
   if (tid < 3) C.copy_first[tid] = kNone;
   if (tid < CT_NDIAG) C.diag[tid] = 0;
-  if (tid == 0) { C.flags = 0; C.max_dev = -1; C.oor_key = kNone; C.of_cell = kNone; }
-  W.tpl[lane].sig = 0;  // kTE == 32
-  W.tpl[lane].ndef = 0;
+  if (tid < (kTreeLut + 1) * kTreeLut) {
+    const int n = tid / kTreeLut, j = tid % kTreeLut;
+    uint2 e = make_uint2(0xFFFFFFu, 0xFFFFFFu);
+    if (j < n) {
+      int a0, a1, a2, q0, q1, q2;
+      tree_links(n, j, a0, a1, a2);
+      tree_links(n, j == 0 ? n - 1 : j - 1, q0, q1, q2);
+      const int b0 = q0 < 0 ? -1 : (q0 + 1 == n ? 0 : q0 + 1);
+      const int b1 = q1 < 0 ? -1 : (q1 + 1 == n ? 0 : q1 + 1);
+      const int b2 = q2 < 0 ? -1 : (q2 + 1 == n ? 0 : q2 + 1);
+      e.x = (uint32_t)(a0 & 0xFF) | ((uint32_t)(a1 & 0xFF) << 8) | ((uint32_t)(a2 & 0xFF) << 16);
+      e.y = (uint32_t)(b0 & 0xFF) | ((uint32_t)(b1 & 0xFF) << 8) | ((uint32_t)(b2 & 0xFF) << 16);
+    }
+    C.tree_lut[n][j] = e;
+  }
+  if (tid == 0) {
+    C.flags = 0; C.max_dev = -1; C.oor_key = kNone; C.of_cell = kNone;
+  }
   if (lane < kCS) {
-    W.tag[lane] = kEmptyTag; W.sn[lane] = 0; W.sver[lane] = 0;
+    W.tag[lane] = kEmptyTag; W.sn[lane] = 0;
     W.cfirst[lane] = kNone; W.clast[lane] = kNone;
     for (int t = 0; t < 5; t++) W.tfirst[lane][t] = kNone;
   }
@@ -566,376 +596,279 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
 
-  const long long t_start = clock64();
-  Acc<SH> acc(P);
+  Sink<SH> sk(P);
+  RingAcc racc;
+  racc.tag = 0;
+  racc.miss = 0;
+  CopyStats cps{{0, 0, 0}, {0, 0, 0}};
   int my_max_dev = -1;
   uint32_t copy_seen = 0;              // copy kinds this lane has seen (first index noted)
   uint32_t wflags = 0;
-  unsigned long long tf_pend = ~0ull;  // (slot, type) pairs whose first valid instance is not yet recorded
-  uint32_t sc_comm = kEmptyTag;        // last (comm, slot) pair looked up (warp-uniform)
+  unsigned long long tf_pend = (1ull << (kCS * 5)) - 1;  // (slot, type) first valid instance not yet noted
+  uint32_t sc_comm = kEmptyTag;        // this lane's last (comm, slot) look-up
   int sc_slot = -1;
 
   // ---- this warp's range, cut at element starts
   const uint64_t NC = P.n_chunks;
   const uint64_t c0 = NC * gw / P.total_warps, c1 = NC * (gw + 1) / P.total_warps;
-  bool bad = false;
-  const uint64_t start = c0 == 0 ? 0 : first_start(P.recs, P.n, c0 * 32, bad);
-  const uint64_t end = c1 >= NC ? P.n : first_start(P.recs, P.n, c1 * 32, bad);
-  if (bad) wflags |= F_NONCANON;
-  if (start < end && !bad) {
-    // The warp slides a 32-record window over its range.  A window always begins at an
-    // element start and consumes exactly the elements that lie whole inside it (n <= 32
-    // guarantees progress); the next window begins where the last one ended.  Positions
-    // are 32-bit, relative to the ring origin rb0 (chunk k0); relative chunk q lives in
-    // ring slot q % kRing, so record rb0 + x sits at ring index x & kRM.
+  bool bad0 = false;
+  const uint64_t start = c0 == 0 ? 0 : first_start(P.recs, P.n, c0 * 32, bad0);
+  const uint64_t end = c1 >= NC ? P.n : first_start(P.recs, P.n, c1 * 32, bad0);
+  if (bad0) wflags |= F_NONCANON;
+  if (start < end && !bad0) {
+    // Positions are 32-bit, relative to the ring origin rb0 (chunk k0); relative chunk q
+    // lives in ring slot q % kRing, so record rb0 + x sits at ring index x & kRM.
     const uint64_t k0 = start / 32;
     const uint64_t rb0 = k0 * 32;
-    const uint32_t lastc = (uint32_t)(min(NC, (end + 31) / 32 + 1) - k0);  // chunks below this may be read
+    const uint32_t s0 = (uint32_t)(start - rb0);
     const uint32_t eo = (uint32_t)(end - rb0);
-    const uint32_t no = (uint32_t)min((unsigned long long)(P.n - rb0), 0xFFFFFFFFull);
+    const uint32_t lastc = (eo + 31) / 32;  // chunks [0, lastc) hold the range
     const ct_record* R = &W.ring[0][0];
-    const WinDev wdv{R};
-    uint32_t issued = 0, ready = 0, freed = 0;
-    for (; issued < (uint32_t)kRing && issued < lastc; issued++)
+    for (uint32_t q = 0; q < (uint32_t)kRing && q < lastc; q++)
       if (lane == 0) {
-        const uint64_t first = (k0 + issued) * 32;
-        bulk_load(W.ring[issued], P.recs + first, (uint32_t)min((uint64_t)32, P.n - first) * (uint32_t)sizeof(ct_record),
-                  &W.bar[issued]);
+        const uint64_t first = (k0 + q) * 32;
+        bulk_load(W.ring[q], P.recs + first, (uint32_t)min((uint64_t)32, P.n - first) * (uint32_t)sizeof(ct_record),
+                  &W.bar[q]);
       }
-
-    int ts = -1;                     // steady comm slot (-1: none)
-    uint32_t tcomm = 0, tn = 0;      // its comm id and nranks
-    uint32_t pending = 0;            // deferred blocks not yet expanded
-    uint32_t skip = 0, backoff = 0;  // steady attempts back off after misses
-    uint32_t bo = (uint32_t)(start - rb0);
-    while (bo < eo) {
-      const uint32_t kB = min((bo + 31) / 32, lastc - 1);
-      while (ready <= kB) {
-        mbar_wait(&W.bar[ready % kRing], (ready / kRing) & 1);
-        ready++;
-      }
-      const uint32_t nval = min(32u, no - bo);  // records that exist
-      const uint32_t lim = min(32u, eo - bo);   // heads this range owns
-      const bool valid = (uint32_t)lane < nval;
-      Rec ra{};
-      int kind = 7;
-      if (valid) { ra = load_swz(R, (bo + lane) & kRM); kind = ra.kind(); }
-      uint32_t nbo;
-      if (P.dbg & 4) {  // diagnostic: stream only (roofline experiments)
-        my_max_dev = max(my_max_dev, (int)(ra.dev ^ ra.rank));
-        nbo = bo + 32;
+    uint32_t ready = 0, freed = 0;  // chunks waited for / released (slot re-issued)
+    uint32_t qh = 0, qt = 0;        // element queue head / tail
+    int cover = 0;                  // sum of element lengths minus records (tiling check)
+    uint32_t cross = 0;             // 1: the last queued element extends past the scanned chunks
+    uint32_t u = 0;                 // chunk of the oldest queued element (when the queue is not empty)
+    const bool stream_only = (P.dbg & 4) != 0, no_expand = (P.dbg & 1) != 0;
+    bool bail = false;
+    for (uint32_t q = 0; q < lastc && !bail; q++) {
+      mbar_wait(&W.bar[q % kRing], (q / kRing) & 1);
+      ready = q + 1;
+      if (stream_only) {  // diagnostic: stream only (roofline experiments)
+        const uint32_t rel = q * 32 + lane;
+        if (rel < eo) my_max_dev = max(my_max_dev, (int)(R[rel & kRM].dev ^ R[rel & kRM].rank));
       } else {
-        // ---------------- elements: starts, lengths, whole-in-window heads, coverage
-        const bool isS = valid && is_start(kind, ra.rank);
-        uint32_t len = 0;
-        bool badl = false;
-        if (isS) {
-          len = kind == CT_KIND_COLLECTIVE ? ra.nranks : (kind == CT_KIND_SEND ? 2u : 1u);
-          if (len == 0 || len > (uint32_t)kMaxN) { badl = true; len = 1; }
+        // ================= scan (lane = record)
+        {
+          const uint32_t rel = q * 32 + lane;
+          const bool act = rel >= s0 && rel < eo;
+          uint4 b = make_uint4(0, 0, 0, 0);
+          if (act) b = reinterpret_cast<const uint4*>(R + (rel & kRM))[1];
+          const int kind = act ? (int)((b.w >> 16) & 7) : 7;
+          const uint32_t nr = b.y & 0xFFFF, rk = b.y >> 16, dev = b.z & 0xFFFF;
+          if (act) my_max_dev = max(my_max_dev, (int)dev);
+          const bool isH = (kind == CT_KIND_COLLECTIVE && rk == 0) || kind == CT_KIND_SEND;
+          const bool isCp = kind >= CT_KIND_MEMCPY && kind <= CT_KIND_ZEROCOPY;
+          const uint32_t len = kind == CT_KIND_COLLECTIVE ? nr : 2u;
+          const bool badl = isH && (len == 0 || len > (uint32_t)kMaxN || rel + len > eo);
+          cover += (isH ? (int)len : (isCp ? 1 : 0)) - (act ? 1 : 0);
+          const unsigned hm = __ballot_sync(kFull, isH);
+          if (isH) W.q[(qt + __popc(hm & lt)) & kQM] = rel;
+          if (qt == qh && hm) u = q;  // the queue's oldest element now starts in this chunk
+          qt += __popc(hm);
+          // only the chunk's last element can extend past it (else the layout is not canonical
+          // and the tiling check fails): it waits for the next scan
+          cross = __any_sync(kFull, isH && rel + len > (q + 1) * 32) ? 1u : 0u;
+          if (isCp) {
+            const unsigned long long cnt = reinterpret_cast<const unsigned long long*>(R + (rel & kRM))[0];
+            const int ck = (int)(b.w >> 30);
+            const uint32_t aux = b.z >> 16, aux2 = b.w & 0xFFFF;
+            if (ck != CT_CKIND_H2D) my_max_dev = max(my_max_dev, (int)aux);
+            if (ck != CT_CKIND_D2H) my_max_dev = max(my_max_dev, (int)aux2);
+            const int t = kind - CT_KIND_MEMCPY;
+            cps.add(t, cnt);
+            if (!no_expand) {
+              const int src = ck == CT_CKIND_H2D ? -1 : (int)aux, dst = ck == CT_CKIND_D2H ? -1 : (int)aux2;
+              if (src < P.gcap && dst < P.gcap && (cnt >> 63) == 0) {
+                const int a = src < 0 ? kHost : src + 2, bb = dst < 0 ? kHost : dst + 2;
+                sk.add((uint32_t)(((CT_T_EXPLICIT + t) * P.g2 + a) * P.g2 + bb), cnt);
+              } else {
+                sk.rec_key = (2ull << 62) | (min((unsigned long long)(rb0 + rel), (1ull << 41) - 1) << 21);
+                sk.edge(CT_T_EXPLICIT + t, src, dst, (unsigned __int128)cnt);
+              }
+            }
+            // first record of each copy kind: positions only grow, so a lane's first is its min
+            const uint32_t bit = 1u << t;
+            if (!(copy_seen & bit)) {
+              copy_seen |= bit;
+              atomicMin(&C.copy_first[t], rb0 + rel);
+            }
+          }
+          if (__any_sync(kFull, badl)) { wflags |= F_NONCANON; bail = true; break; }
         }
-        const unsigned Sall = __ballot_sync(kFull, isS);
-        const unsigned Sown = lim >= 32 ? Sall : Sall & ((1u << lim) - 1);
-        const unsigned Inc = __ballot_sync(kFull, ((Sown >> lane) & 1) && (uint32_t)lane + len > 32);
-        const unsigned H = Inc ? Sown & ((1u << (__ffs(Inc) - 1)) - 1) : Sown;  // heads processed now
-        const bool head = (H >> lane) & 1;
-        if (!(H & 1)) badl = true;  // the window must begin with an element start
-        const int hL = H ? 31 - __clz(H) : 0;
-        const uint32_t Pw = hL + __shfl_sync(kFull, len, hL);      // records consumed
-        const bool mem = (uint32_t)lane < Pw;
-        const unsigned below = H & (0xFFFFFFFFu >> (31 - lane));
-        const int hA = below ? 31 - __clz(below) : 0;
-        const uint32_t lenA = __shfl_sync(kFull, len, hA);
-        if (mem && (uint32_t)lane >= (uint32_t)hA + lenA) badl = true;  // a record no element covers
-        if (head && ((uint32_t)lane + len > nval || !range_clear((unsigned long long)Sall, (uint32_t)lane + 1, len - 1)))
-          badl = true;  // runs past the trace, or another element starts inside this one
-        const uint32_t a2 = ra.kc | (ra.ad << 8) | (ra.aux << 16);
+        __syncwarp();
 
-        // ---------------- steady window: every element is a copy or a block of the steady
-        // communicator repeating a known-valid signature with the devices of its last block
-        // and increasing seqs.  Such blocks are valid instances with identical transfers:
-        // count them per template and expand once, multiplied, at the next flush.
-        bool steady = false;
-        if (ts >= 0 && skip == 0) {
-          bool okl = !badl;
-          uint32_t ti = 0;
-          const bool cl = mem && kind == CT_KIND_COLLECTIVE;
-          if (cl) {
-            const uint32_t sg = coll_sig(a2);
-            const uint32_t set = tpl_set(ra.count, sg);
-            const Tpl e0 = W.tpl[2 * set], e1 = W.tpl[2 * set + 1];
-            const bool h0 = e0.count == ra.count && e0.sig == sg;
-            const bool h1 = e1.count == ra.count && e1.sig == sg;
-            ti = 2 * set + (h0 ? 0u : 1u);
-            okl = okl && (h0 || h1) && ra.comm == tcomm && ra.nranks == tn && ra.rank == (uint32_t)(lane - hA) &&
-                  ra.dev == W.cdev[ts][ra.rank & 31] && ra.dev < (uint32_t)P.gcap;
-          } else if (mem) {
-            okl = okl && kind >= CT_KIND_MEMCPY && kind <= CT_KIND_ZEROCOPY;
-          }
-          const unsigned Hc = __ballot_sync(kFull, head && kind == CT_KIND_COLLECTIVE);
-          const uint32_t tiH = __shfl_sync(kFull, ti, hA);
-          const unsigned lower = Hc & ((1u << hA) - 1);
-          const int ph = lower ? 31 - __clz(lower) : -1;  // previous block of the comm in the window
-          const int src = ph >= 0 ? ((ph + (int)ra.rank) & 31) : lane;
-          const uint64_t pseq = ((uint64_t)__shfl_sync(kFull, (uint32_t)(ra.seq >> 32), src) << 32) |
-                                __shfl_sync(kFull, (uint32_t)ra.seq, src);
-          if (cl) {
-            const uint64_t prev = ph >= 0 ? pseq : W.cseq[ts][ra.rank & 31];
-            okl = okl && ti == tiH && prev < ra.seq;
-          }
-          if ((P.dbg & 8) && !okl) {  // diagnostic: why a steady attempt failed
-            uint32_t why = badl ? 1u : 0u;
-            if (cl) {
-              const uint32_t sg = coll_sig(a2);
-              const uint32_t set = tpl_set(ra.count, sg);
-              const bool hit = (W.tpl[2 * set].count == ra.count && W.tpl[2 * set].sig == sg) ||
-                               (W.tpl[2 * set + 1].count == ra.count && W.tpl[2 * set + 1].sig == sg);
-              if (!hit) why |= 2;
-              if (ra.comm != tcomm || ra.nranks != tn) why |= 4;
-              if (ra.rank != (uint32_t)(lane - hA)) why |= 8;
-              if (ra.dev != W.cdev[ts][ra.rank & 31]) why |= 16;
-              if (ti != tiH) why |= 128;
-              if (!((ph >= 0 ? pseq : W.cseq[ts][ra.rank & 31]) < ra.seq)) why |= 256;
-            } else if (mem) {
-              why |= 64;
-            }
-            atomicOr(&P.st->pad, why);
-          }
-          if (__all_sync(kFull, okl)) {
-            steady = true;
-            backoff = 0;
-            if ((P.dbg & 8) && lane == 0) atomicAdd(&P.st->n_chain, 1u);
-            if (Hc) {
-              const int hLc = 31 - __clz(Hc);
-              if (head && kind == CT_KIND_COLLECTIVE) atomicAdd(&W.tpl[ti].ndef, 1u);
-              pending += __popc(Hc);
-              if (cl && hA == hLc) W.cseq[ts][ra.rank] = ra.seq;
-              if (lane == 0) W.clast[ts] = rb0 + bo + hLc;
-              __syncwarp();
-            }
-            if (Hc != H && mem && kind != CT_KIND_COLLECTIVE && !(P.dbg & 1))
-              expand_record(P, acc, wdv, ra, rb0, bo + lane, ST_VALID, bo + lane, my_max_dev, copy_seen);
-          } else {
-            if (backoff == 63) {  // long miss streak: drop stale templates
-              W.tpl[lane].sig = 0;
-              __syncwarp();
-            }
-            backoff = min(2 * backoff + 1, 63u);
-            skip = backoff;
-          }
-        } else if (skip) {
-          skip--;
-        }
+        // ================= join + expand (lane = element), in batches of <= 32
+        // elements wholly inside chunks <= q are joinable; join when 32 are ready or when
+        // the ring is about to be full of unjoined records (the oldest one's chunk u)
+        const bool pressure = q + 1 + kDrainSlack >= u + kRing || q + 1 == lastc;
+        while (qt - qh - cross >= 32 || (pressure && qt - qh - cross > 0)) {
+          const uint32_t nb = min(32u, qt - qh - cross);
+          const bool act = (uint32_t)lane < nb;
+          const uint32_t p = act ? W.q[(qh + lane) & kQM] : 0u;
+          Rec h{};
+          int kind = 7;
+          if (act) { h = ring_rec(R, p); kind = h.kind(); }
+          const bool isC = kind == CT_KIND_COLLECTIVE, isS = kind == CT_KIND_SEND;
+          bool bad = false;
 
-        if (!steady) {
-          if (pending) {  // the general path may change the steady comm's devices: expand first
-            acc.flags |= flush_templates<SH>(P.ex, hist_bytes<SH>(P), hist_freq<SH>(P), P.g2, W, ts, tcomm, tn);
-            pending = 0;
+          // ---- comm slots of collective blocks
+          int slot = -1;
+          if (isC) {
+            if (h.comm >= P.n_comms) { wflags |= F_COMM_RANGE; bad = true; }
+            slot = h.comm == sc_comm ? sc_slot : find_slot(W, h.comm);
           }
-          // ---------------- member checks against the predecessor record (lane shuffles)
-          // words: comm | nranks, rank | kc, ad, aux | count lo | count hi
-          bool gfail = false, mis = false;
-          {
-            const uint32_t q0 = __shfl_up_sync(kFull, ra.comm, 1);
-            const uint32_t q1 = __shfl_up_sync(kFull, ra.nranks | (ra.rank << 16), 1);
-            const uint32_t q2 = __shfl_up_sync(kFull, a2, 1);
-            const uint32_t q3 = __shfl_up_sync(kFull, (uint32_t)ra.count, 1);
-            const uint32_t q4 = __shfl_up_sync(kFull, (uint32_t)(ra.count >> 32), 1);
-            if (mem && !head) member_check(ra, a2, q0, q1, q2, q3, q4, badl, gfail, mis);
+          while (true) {  // allocate slots for unseen comms (rare, warp-serial)
+            const unsigned miss = __ballot_sync(kFull, isC && slot < 0);
+            if (!miss) break;
+            const uint32_t cm = __shfl_sync(kFull, h.comm, __ffs(miss) - 1);
+            int free_s = -1;
+            for (int s = kCS - 1; s >= 0; s--)
+              if (W.tag[s] == kEmptyTag) free_s = s;
+            __syncwarp();
+            if (free_s < 0) { bad = true; break; }  // more comms than slots in one range
+            if (lane == 0) W.tag[free_s] = cm;
+            __syncwarp();
+            if (isC && slot < 0 && h.comm == cm) slot = free_s;
           }
-          if (__any_sync(kFull, badl)) { wflags |= F_NONCANON; break; }  // host re-runs the exact path
-          const bool collH = head && kind == CT_KIND_COLLECTIVE;
-          const bool sendH = head && kind == CT_KIND_SEND;
-          const unsigned Hc = __ballot_sync(kFull, collH);
-          const unsigned Hs = __ballot_sync(kFull, sendH);
-          const unsigned sigmask = __ballot_sync(kFull, gfail);
-          const unsigned mismask = Hs ? __ballot_sync(kFull, mis) : 0u;
+          if (isC) { sc_comm = h.comm; sc_slot = slot; }
+          const int hs = slot < 0 ? 0 : slot;
 
-          // ---------------- per-comm predecessor block, comm slot (uniform fast case)
-          uint32_t info = 0;  // slot | ph << 4 | has_ph << 10 | hist << 11 | ver << 12 | last << 13
-          int uslot = -1;     // the single comm slot of the window's blocks (uniform case)
-          if (Hc) {
-            const uint32_t c_first = __shfl_sync(kFull, ra.comm, __ffs(Hc) - 1);
-            if (__all_sync(kFull, !collH || ra.comm == c_first)) {
-              int su = c_first == sc_comm ? sc_slot : find_slot(W, c_first);
-              if (su < 0) {  // new comm in this range
-                for (int s = kCS - 1; s >= 0; s--)
-                  if (W.tag[s] == kEmptyTag) su = s;
-                __syncwarp();
-                if (su < 0) wflags |= F_NONCANON;  // more comms than slots in one range
-                else if (lane == 0) W.tag[su] = c_first;
-                __syncwarp();
-              }
-              if (c_first >= P.n_comms) wflags |= F_COMM_RANGE | F_NONCANON;
-              sc_comm = c_first;
-              sc_slot = su;
-              uslot = su;
-              const int slot = su < 0 ? 0 : su;
-              const uint32_t sn = W.sn[slot];
-              const uint32_t base = (uint32_t)slot | (sn ? 1u << 11 : 0u) | (sn && W.sver[slot] ? 1u << 12 : 0u);
-              const unsigned lower = Hc & ((1u << hA) - 1);
-              const int ph = lower ? 31 - __clz(lower) : -1;
-              info = base | ((uint32_t)(ph & 63) << 4) | (ph >= 0 ? 1u << 10 : 0u) | ((Hc >> hA) == 1u ? 1u << 13 : 0u);
-            } else {
-              // several comms start blocks in this window: per-head slots, MATCH for predecessors
-              int slot = -1;
-              if (collH) {
-                if (ra.comm >= P.n_comms) wflags |= F_COMM_RANGE | F_NONCANON;
-                slot = ra.comm == sc_comm ? sc_slot : find_slot(W, ra.comm);
-              }
-              while (true) {  // allocate slots for unseen comms (rare, warp-serial)
-                const unsigned miss = __ballot_sync(kFull, collH && slot < 0);
-                if (!miss) break;
-                const uint32_t cm = __shfl_sync(kFull, ra.comm, __ffs(miss) - 1);
-                int free_s = -1;
-                for (int s = kCS - 1; s >= 0; s--)
-                  if (W.tag[s] == kEmptyTag) free_s = s;
-                __syncwarp();
-                if (free_s < 0) { wflags |= F_NONCANON; break; }
-                if (lane == 0) W.tag[free_s] = cm;
-                __syncwarp();
-                if (collH && slot < 0 && ra.comm == cm) slot = free_s;
-              }
-              const unsigned lt = (1u << lane) - 1;
-              const unsigned same =
-                  __match_any_sync(kFull, collH ? (unsigned long long)ra.comm : (0xFFFFFFFF00000000ull | lane)) & Hc;
-              const unsigned lower = same & lt;
-              const int ph = lower ? 31 - __clz(lower) : -1;
-              const int hs = slot < 0 ? 0 : slot;
-              const bool hist = collH && W.sn[hs] != 0;
-              const uint32_t hinfo = (uint32_t)hs | ((uint32_t)(ph & 63) << 4) | (ph >= 0 ? 1u << 10 : 0u) |
-                                     (hist ? 1u << 11 : 0u) | (hist && W.sver[hs] ? 1u << 12 : 0u) |
-                                     ((same & ~lt & ~(1u << lane)) == 0 ? 1u << 13 : 0u);
-              info = __shfl_sync(kFull, hinfo, hA);
-            }
-          }
-          if (collH) {  // nranks constant per comm (grouping.py:104-108)
-            const uint32_t pn = (info & (1u << 10)) ? R[(bo + ((info >> 4) & 63)) & kRM].nranks
-                                                    : ((info & (1u << 11)) ? W.sn[info & 15] : ra.nranks);
-            if (pn != ra.nranks) wflags |= F_NONCANON;
-          }
+          // ---- the comm's previous block: earlier in this batch (ring) or the slot table
+          const unsigned same =
+              __match_any_sync(kFull, isC ? (unsigned long long)h.comm : (0xFFFFFFFF00000000ull | lane));
+          const unsigned lower = same & lt;
+          const int pl = lower ? 31 - __clz(lower) : -1;
+          const bool lastb = isC && (same >> lane) == 1u;  // no later block of this comm in the batch
+          const uint32_t ppos = __shfl_sync(kFull, p, pl < 0 ? lane : pl);
+          const uint32_t pn = __shfl_sync(kFull, h.nranks, pl < 0 ? lane : pl);
+          const uint32_t tsn = isC ? W.sn[hs] : 0u;
+          const bool hist = pl < 0 && tsn != 0;
+          const uint32_t n = h.nranks;
+          if (isC && (pl >= 0 ? pn != n : (tsn != 0 && tsn != n))) bad = true;  // grouping.py:104-108
 
-          // ---------------- per-member seq order and device inheritance from the last block
-          bool devf = false;
-          const bool cm = mem && kind == CT_KIND_COLLECTIVE;
-          {
-            const int src = (cm && (info & (1u << 10))) ? ((((info >> 4) & 63) + (int)ra.rank) & 31) : lane;
-            const uint64_t pseq = ((uint64_t)__shfl_sync(kFull, (uint32_t)(ra.seq >> 32), src) << 32) |
-                                  __shfl_sync(kFull, (uint32_t)ra.seq, src);
-            if (cm) order_check(W, ra, info, pseq, wflags, devf);
-          }
-          const unsigned devmask = __ballot_sync(kFull, devf);
-
-          // ---------------- element status (every member derives its element's status)
-          // collective: incompatible if any member's signature differs (grouping.py:144-155),
-          // duplicate device if devices are not pairwise distinct (grouping.py:156-167)
-          const unsigned needs_full = __ballot_sync(kFull, collH && !range_clear(devmask, (uint32_t)lane, ra.nranks));
-          bool dist = true;
-          if (needs_full) {  // devices changed since the comm's last block: full pairwise check
-            if ((needs_full >> lane) & 1) dist = devices_distinct(R, bo + lane, ra.nranks);
-          }
-          const unsigned dupmask = __ballot_sync(kFull, !dist);  // heads with duplicate devices
-          const uint32_t kindH = __shfl_sync(kFull, (uint32_t)kind, hA);
+          // ---- validation (lane walks its element)
           uint32_t st = ST_NONE;
-          if (mem) {
-            if (kindH == CT_KIND_COLLECTIVE)
-              st = !range_clear(sigmask, (uint32_t)hA + 1, lenA - 1) ? ST_INCOMPAT
-                                                                     : (((dupmask >> hA) & 1) ? ST_DUPDEV : ST_VALID);
-            else if (kindH == CT_KIND_SEND)
-              st = ((mismask >> (hA + 1)) & 1) ? ST_MISMATCH : ST_VALID;
-            else
-              st = ST_VALID;
+          bool fastdev = false, packed = false;  // all devices < gcap / held in ``devs``
+          unsigned long long devs = 0;          // device of rank j in byte j (n <= 8, devices < 64)
+          uint64_t rseq = 0;
+          uint32_t rdev = 0;
+          const uint32_t j0 = n == 0 ? 0u : ((uint32_t)lane < n ? (uint32_t)lane : (uint32_t)lane % n);
+          if (isC && !bad) {
+            // compare raw words against the head: w4 comm, w5 nranks | rank << 16, w6 dev |
+            // aux << 16 (aux = root when rooted), w7 aux2 | kc << 16 | ad << 24
+            const uint4* R4 = reinterpret_cast<const uint4*>(R);
+            const uint32_t hc0 = (uint32_t)h.count, hc1 = (uint32_t)(h.count >> 32);
+            const uint32_t hw7 = h.aux2 | (h.kc << 16) | (h.ad << 24);
+            const uint32_t rootm = h.has_root() ? 0xFFFF0000u : 0u, hw6 = h.aux << 16;
+            uint32_t badw = 0, incw = 0;
+            bool ord = false, big = false, dup = false;
+            unsigned long long dm = 0;
+            auto vrec = [&](uint32_t j) {  // one member record (independent across j)
+              const uint32_t ix = (p + j) & kRM;
+              const uint4 wa = R4[2 * ix], wb = R4[2 * ix + 1];
+              const uint32_t x7 = wb.w ^ hw7;
+              badw |= (wb.x ^ h.comm) | (wb.y ^ (n | (j << 16))) | (x7 & 0x00070000u);  // kind, comm, n, rank
+              incw |= (wa.x ^ hc0) | (wa.y ^ hc1) | (x7 & 0x3F780000u) | ((wb.z ^ hw6) & rootm);  // signature
+              const unsigned long long seq = ((unsigned long long)wa.w << 32) | wa.z;
+              if (pl >= 0 || hist) {
+                const uint64_t* ps = pl >= 0 ? &R[(ppos + j) & kRM].seq : reinterpret_cast<const uint64_t*>(&W.cseq[hs][j]);
+                if (!(*ps < seq)) ord = true;
+              }
+              const uint32_t dv = wb.z & 0xFFFF;
+              if (dv < 64) {
+                const unsigned long long bit = 1ull << dv;
+                dup = dup || (dm & bit) != 0;
+                dm |= bit;
+                devs |= (unsigned long long)dv << (8 * (j & 7));
+              } else {
+                big = true;
+              }
+            };
+            uint32_t j = j0;
+            uint32_t i = 0;
+            for (; i + 1 < n; i += 2) {
+              const uint32_t j1 = j + 1 == n ? 0 : j + 1;
+              vrec(j);
+              vrec(j1);
+              j = j1 + 1 == n ? 0 : j1 + 1;
+            }
+            if (i < n) vrec(j);
+            if (badw) bad = true;
+            if (ord) bad = true;  // per (comm, rank) seq must strictly increase
+            if (big && !dup) dup = !devices_distinct(R, p, n);
+            fastdev = !big && (P.gcap >= 64 || (dm >> P.gcap) == 0);
+            packed = !big && n <= 8;
+            st = incw ? ST_INCOMPAT : (dup ? ST_DUPDEV : ST_VALID);
+          } else if (isS) {
+            const Rec r = ring_rec(R, p + 1);
+            if (r.kind() != CT_KIND_RECV || r.comm != h.comm || r.aux != h.rank || r.rank != h.aux) bad = true;
+            st = (r.count != h.count || r.dtype() != h.dtype()) ? ST_MISMATCH : ST_VALID;  // decompose.py:362-372
+            rseq = r.seq;
+            rdev = r.dev;
           }
-          if (head && st != ST_VALID) count_diag(st);
+          if (__any_sync(kFull, bad)) { wflags |= F_NONCANON; bail = true; break; }
+          if (__any_sync(kFull, isS)) wflags |= p2p_order(P.chans + (size_t)gw * kPC, h, rseq, isS, lane);
+          if (st > ST_VALID) count_diag(st);
 
-          // ---------------- p2p order: per (comm, src, dst) channel non-decreasing send and
-          // recv seqs (decompose.py:359-361 sorts each side by seq; FIFO pairs by position)
-          if (Hs) {
-            const uint64_t nseq = ((uint64_t)__shfl_down_sync(kFull, (uint32_t)(ra.seq >> 32), 1) << 32) |
-                                  __shfl_down_sync(kFull, (uint32_t)ra.seq, 1);
-            p2p_order(P.chans + (size_t)gw * kPC, ra, nseq, sendH, lane, wflags);
+          // ---- tables: the last block of each comm in the batch; first occurrences
+          __syncwarp();  // every lane has read the tables
+          if (isC) {
+            const uint64_t gi = rb0 + p;
+            if (pl < 0 && tsn == 0) W.cfirst[hs] = gi;  // first block of this comm in the range
+            if (lastb) {
+              W.sn[hs] = n;
+              W.clast[hs] = gi;
+              for (uint32_t j = 0; j < n; j++) W.cseq[hs][j] = R[(p + j) & kRM].seq;
+            }
           }
-
-          // ---------------- table update with the last block of each comm in the window
-          __syncwarp();
-          if (cm && (info & (1u << 13))) { W.cseq[info & 15][ra.rank] = ra.seq; W.cdev[info & 15][ra.rank] = (uint16_t)ra.dev; }
-          if (collH) {
-            const int hs = info & 15;
-            const uint64_t gi = rb0 + bo + lane;
-            if (!(info & (3u << 10))) W.cfirst[hs] = gi;  // first block of this comm in the range
-            if (info & (1u << 13)) { W.sn[hs] = ra.nranks; W.sver[hs] = dist; W.clast[hs] = gi; }
-          }
-          if (Hc) {  // first valid instance per (comm slot, type): only until recorded once
-            const unsigned long long bit = (collH && st == ST_VALID) ? 1ull << ((info & 15) * 5 + ra.coll()) : 0ull;
+          if (tf_pend) {  // first valid instance per (comm slot, type): only until recorded once
+            const unsigned long long bit = (isC && st == ST_VALID) ? 1ull << (hs * 5 + h.coll()) : 0ull;
             const bool rec = (bit & tf_pend) != 0;
-            if (rec) note_min_smem(&W.tfirst[info & 15][ra.coll()], rb0 + bo + lane);
+            if (rec) note_min_smem(&W.tfirst[hs][h.coll()], rb0 + p);
             const unsigned lo = __reduce_or_sync(kFull, rec ? (unsigned)bit : 0u);
             const unsigned hi = __reduce_or_sync(kFull, rec ? (unsigned)(bit >> 32) : 0u);
             tf_pend &= ~(((unsigned long long)hi << 32) | lo);
           }
           __syncwarp();
 
-          // ---------------- expansion + accumulation
-          if (mem && !(P.dbg & 1))
-            expand_record(P, acc, wdv, ra, rb0, bo + lane, st, bo + (uint32_t)hA, my_max_dev, copy_seen);
-
-          // ---------------- steady comm and templates: the window's last block, when valid
-          if (ts >= 0 && !W.sver[ts]) ts = -1;  // duplicate devices: repeats are not valid
-          if (Hc && uslot >= 0) {
-            const int hLc = 31 - __clz(Hc);
-            if (__shfl_sync(kFull, st, hLc) == ST_VALID && W.sver[uslot] && uslot != ts) {
-              W.tpl[lane].sig = 0;
-              ts = uslot;
-              tcomm = __shfl_sync(kFull, ra.comm, hLc);
-              tn = __shfl_sync(kFull, ra.nranks, hLc);
-              skip = backoff = 0;
+          // ---- expansion + accumulation of valid elements
+          if (st == ST_VALID && !no_expand) {
+            if (isC) {
+              expand_block<SH>(P, sk, R, h, p, rb0 + p, j0, fastdev, packed, devs, racc);
+            } else {  // matched send/recv pair (decompose.py:319-339)
+              const unsigned __int128 nbytes = (unsigned __int128)h.count * (unsigned)dtype_width(h.dtype());
+              sk.stat(CT_T_SENDRECV, nbytes);
+              sk.rec_key = (1ull << 62) | (min((unsigned long long)(rb0 + p), (1ull << 41) - 1) << 21);
+              if (rdev != h.dev) sk.edge(CT_T_SENDRECV, (int)h.dev, (int)rdev, nbytes);
             }
-            __syncwarp();
-            if (ts == uslot && skip <= 3 && collH && st == ST_VALID) {  // valid signatures before an attempt
-              const uint32_t sg = coll_sig(a2);
-              const uint32_t set = tpl_set(ra.count, sg);
-              Tpl* e = &W.tpl[2 * set];
-              const bool in0 = e[0].count == ra.count && e[0].sig == sg;
-              const bool in1 = e[1].count == ra.count && e[1].sig == sg;
-              if (!in0 && !in1) {  // empty way first, else replace way (seq & 1); racing lanes only cost hits
-                const int way = e[0].sig == 0 ? 0 : (e[1].sig == 0 ? 1 : (int)(ra.seq & 1));
-                e[way].count = ra.count;
-                e[way].sig = sg;
-                e[way].ndef = 0;
-              }
-            }
-            __syncwarp();
           }
-        }  // general path
-        nbo = bo + Pw;
+          qh += nb;
+          if (qt != qh) u = W.q[qh & kQM] / 32;
+        }
+        if (bail) break;
       }
 
-      // ---------------- slide: chunks wholly behind the next window refill their slots
-      const uint32_t kf = nbo / 32;
-      if (kf > freed) {
+      // ---- release chunks no element still needs; their slots refill
+      const uint32_t keep = qt != qh ? u : q + 1;
+      if (keep > freed) {
         __syncwarp();
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         do {
-          const uint32_t q = freed + kRing;
-          if (q < lastc) {
-            if (lane == 0) {
-              const uint64_t first = (k0 + q) * 32;
-              bulk_load(W.ring[freed % kRing], P.recs + first,
-                        (uint32_t)min((uint64_t)32, P.n - first) * (uint32_t)sizeof(ct_record), &W.bar[freed % kRing]);
-            }
-            issued = q + 1;
+          const uint32_t nq = freed + kRing;
+          if (nq < lastc && lane == 0) {
+            const uint64_t first = (k0 + nq) * 32;
+            bulk_load(W.ring[freed % kRing], P.recs + first,
+                      (uint32_t)min((uint64_t)32, P.n - first) * (uint32_t)sizeof(ct_record), &W.bar[freed % kRing]);
           }
           freed++;
-        } while (freed < kf);
+        } while (freed < keep);
       }
-      bo = nbo;
     }
-    if (pending) acc.flags |= flush_templates<SH>(P.ex, hist_bytes<SH>(P), hist_freq<SH>(P), P.g2, W, ts, tcomm, tn);
+    if (!bail && !(P.dbg & 4)) {  // element lengths must tile the range exactly
+      const int tot = __reduce_add_sync(kFull, cover);
+      if (tot != 0) wflags |= F_NONCANON;
+    }
+    const uint32_t issued = min(freed + (uint32_t)kRing, lastc);
     for (uint32_t q = ready; q < issued; q++)  // drain outstanding bulk copies
       mbar_wait(&W.bar[q % kRing], (q / kRing) & 1);
   }
-
-  if ((P.dbg & 16) && lane == 0)  // diagnostic: slowest warp (cycles << 24 | warp)
-    atomicMax(&P.st->err_index, ((unsigned long long)(clock64() - t_start) << 24) | gw);
 
   // ---- per-warp summaries for the cross-range check and first-occurrence keys
   __syncwarp();
@@ -954,18 +887,20 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
   }
 
   // ---- CTA epilogue: drain caches, one global merge
-  acc.drain();
+  if (racc.tag) racc.flush(sk, P.g2);
+  sk.drain();
+  cps.drain();
   atomicMax(&C.max_dev, my_max_dev);
-  if (acc.flags | wflags) atomicOr(&C.flags, acc.flags | wflags);
+  if (sk.flags | wflags) atomicOr(&C.flags, sk.flags | wflags);
   __syncthreads();
 
   GlobalState* G = P.st;
   if (SH) {
     uint32_t of = 0;
     for (int c = tid; c < ncell; c += kThreads) {
-      const unsigned int f = shf[c];
+      const unsigned int f = shl[2 * ncell + c];
       if (!f) continue;
-      const unsigned long long bb = shb[c];
+      const unsigned long long bb = shl[c] | ((unsigned long long)shl[ncell + c] << 32);
       const unsigned long long old = atomicAdd(P.cells + c, bb);
       if (old + bb < old) { of |= F_OVERFLOW; atomicMin(&G->of_cell, (unsigned long long)c); }
       atomicAdd(P.freq + c, (unsigned long long)f);
@@ -973,8 +908,11 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
     if (of) atomicOr(&C.flags, of);
   }
   if (tid < kTypes) {
-    const unsigned long long lo = C.pay_lo[tid], hi = C.pay_hi[tid], c = C.calls[tid];
+    const unsigned long long a = C.pay_a[tid], b = C.pay_b[tid], c = C.calls[tid];
     if (c) {
+      // payload = a + b * 2^32 as 128 bits
+      const unsigned long long lo = a + (b << 32);
+      const unsigned long long hi = (b >> 32) + (lo < a ? 1ull : 0ull);
       const unsigned long long old = atomicAdd(&G->pay_lo[tid], lo);
       atomicAdd(&G->pay_hi[tid], hi + (old + lo < old ? 1ull : 0ull));
       atomicAdd(&G->calls[tid], c);

@@ -1,19 +1,19 @@
 // The fused layout-check + join + expand + accumulate kernel (fast path).
 //
-// Warp-autonomous streaming design (no block-wide barriers in the main loop):
+// Element-parallel streaming design (no block-wide barriers in the main loop):
 //   * every warp owns a contiguous range of the packed trace, cut at element starts
 //     (a collective rank-0 record, a send, or a copy), and streams it through its own
 //     ring of 1 KB TMA bulk copies (cp.async.bulk + mbarrier, kRing slots deep);
-//   * it walks the range in 64-record windows: elements starting in the first 32
-//     positions are processed whole (n <= 32 keeps every element inside the window),
-//     the window then slides by 32 and the carry skips the records already consumed;
-//   * element structure, instance validity (signature equality, distinct devices,
-//     grouping.py:132-167), pair matching and the seq-order preconditions are decided
-//     with ballots over the window and broadcast shared-memory reads of the heads;
-//   * per-(comm, rank) state of the last block (seq, device) lives in a small per-warp
-//     table, so a block is validated against its predecessor in O(1) per record;
-//   * transfers go into a per-thread register cache and spill to a per-CTA shared
-//     histogram; each CTA merges into global memory once at the end.
+//   * scan (lane = record, one 32-record chunk at a time): element starts and lengths,
+//     the tiling check (element lengths sum to the range), copies expanded in place,
+//     collective blocks and send/recv pairs appended to a per-warp element queue;
+//   * join (lane = element, up to 32 queued elements at a time): each lane walks its
+//     block's records -- membership, signature (grouping.py:78-79, 132-155), distinct
+//     devices (grouping.py:156-167), per-(comm, rank) seq order against the comm's
+//     previous block (same batch: the ring; else the per-warp table) -- then expands the
+//     valid instance edge by edge (rank-attributed rules, ct_common.cuh) into the CTA's
+//     shared-memory histogram;
+//   * each CTA merges its histogram and statistics into global memory once at the end.
 // Seq-order preconditions (exactly when the reference's seq-sorted grouping and FIFO
 // matching coincide with file order, grouping.py:118-131, decompose.py:357-361):
 //   collectives: per (comm, rank) strictly increasing seq, constant nranks per comm;
@@ -25,7 +25,10 @@
 
 namespace ct {
 
-constexpr int kThreads = 512;   // 16 warps, one CTA per SM
+#ifndef CT_WARPS
+#define CT_WARPS 16
+#endif
+constexpr int kThreads = 32 * CT_WARPS;  // one CTA per SM
 constexpr int kWarps = kThreads / 32;
 #ifndef CT_RING_SLOTS
 #define CT_RING_SLOTS 8
@@ -34,7 +37,7 @@ constexpr int kRing = CT_RING_SLOTS;  // per-warp TMA ring slots of 32 records (
 constexpr int kCS = 8;          // collective communicator slots per warp
 constexpr int kPC = 64;         // p2p channel table entries per warp
 constexpr int kMaxN = 32;       // largest communicator the fast path handles
-constexpr int kCacheE = 4;      // register cache entries per thread
+constexpr int kQ = 64;          // element queue entries per warp
 
 struct GlobalState {
   uint32_t flags;
