@@ -31,9 +31,8 @@ struct __align__(16) CtaMem {
   unsigned long long copy_first[3];
   unsigned long long oor_key;   // min out-of-range ordering key seen by the CTA
   unsigned long long of_cell;   // min cell index whose 64-bit sum wrapped
-  // double binary tree peers for n <= kTreeLut (trees.py:57-106): .x = T1 parent, left,
-  // right ranks (bytes, 0xFF none), .y = the same in T2 mapped to ranks
-  uint2 tree_lut[kTreeLut + 1][kTreeLut];
+  // double binary tree peers for n <= kTreeLut (trees.py:57-106): tree_pack() words
+  unsigned long long tree_lut[kTreeLut + 1][kTreeLut];
   unsigned int diag[CT_NDIAG];
   uint32_t flags;
   int max_dev;
@@ -368,30 +367,18 @@ __device__ __noinline__ uint32_t p2p_order(P2PEntry* chan, const Rec ra, uint64_
 }
 
 // Peers of position j in the double binary tree (trees.py:57-106, decompose.py:227-255)
-// as ``cnt`` packed 7-bit codes: rank in bits [0,5), bit 5 = T1 edge (ceil(S/2)), bit 6 =
-// T2 edge (floor(S/2), only when t2); an edge present in both trees is one transfer of S.
-__device__ __forceinline__ unsigned long long tree_peers(int n, int j, bool t2, int& cnt) {
-  int a0, a1, a2, b0 = -1, b1 = -1, b2 = -1;
-  if (n <= kTreeLut) {
-    const uint2 e = cta_mem().tree_lut[n][j];
-    a0 = (int)(e.x & 0xFF); a1 = (int)((e.x >> 8) & 0xFF); a2 = (int)((e.x >> 16) & 0xFF);
-    a0 = a0 == 0xFF ? -1 : a0; a1 = a1 == 0xFF ? -1 : a1; a2 = a2 == 0xFF ? -1 : a2;
-    if (t2) {
-      b0 = (int)(e.y & 0xFF); b1 = (int)((e.y >> 8) & 0xFF); b2 = (int)((e.y >> 16) & 0xFF);
-      b0 = b0 == 0xFF ? -1 : b0; b1 = b1 == 0xFF ? -1 : b1; b2 = b2 == 0xFF ? -1 : b2;
-    }
-  } else {
-    tree_links(n, j, a0, a1, a2);  // T1: rank == position
-    if (t2) {
-      int q0, q1, q2;
-      tree_links(n, j == 0 ? n - 1 : j - 1, q0, q1, q2);  // T2: rank at position q is (q + 1) % n
-      b0 = q0 < 0 ? -1 : (q0 + 1 == n ? 0 : q0 + 1);
-      b1 = q1 < 0 ? -1 : (q1 + 1 == n ? 0 : q1 + 1);
-      b2 = q2 < 0 ? -1 : (q2 + 1 == n ? 0 : q2 + 1);
-    }
-  }
+// packed as 7-bit codes (rank in bits [0,5), bit 5 = T1 edge carrying ceil(S/2), bit 6 =
+// T2 edge carrying floor(S/2); an edge in both trees is one transfer of S), the count in
+// bits [60,63).  T2 is always included; a T2-only edge is skipped when floor(S/2) == 0.
+__device__ __forceinline__ unsigned long long tree_pack(int n, int j) {
+  int a0, a1, a2, q0, q1, q2;
+  tree_links(n, j, a0, a1, a2);                       // T1: rank == position
+  tree_links(n, j == 0 ? n - 1 : j - 1, q0, q1, q2);  // T2: rank at position q is (q + 1) % n
+  const int b0 = q0 < 0 ? -1 : (q0 + 1 == n ? 0 : q0 + 1);
+  const int b1 = q1 < 0 ? -1 : (q1 + 1 == n ? 0 : q1 + 1);
+  const int b2 = q2 < 0 ? -1 : (q2 + 1 == n ? 0 : q2 + 1);
   unsigned long long w = 0;
-  cnt = 0;
+  int cnt = 0;
   auto put = [&](int r, uint32_t code) {
     w |= (unsigned long long)((uint32_t)r | (code << 5)) << (7 * cnt);
     cnt++;
@@ -402,7 +389,13 @@ __device__ __forceinline__ unsigned long long tree_peers(int n, int j, bool t2, 
   if (b0 >= 0 && b0 != a0 && b0 != a1 && b0 != a2) put(b0, 2u);
   if (b1 >= 0 && b1 != a0 && b1 != a1 && b1 != a2) put(b1, 2u);
   if (b2 >= 0 && b2 != a0 && b2 != a1 && b2 != a2) put(b2, 2u);
-  return w;
+  return w | ((unsigned long long)cnt << 60);
+}
+
+__device__ __noinline__ unsigned long long tree_pack_big(int n, int j) { return tree_pack(n, j); }
+
+__device__ __forceinline__ unsigned long long tree_peers(int n, int j) {
+  return n <= kTreeLut ? cta_mem().tree_lut[n][j] : tree_pack_big(n, j);
 }
 
 // Expansion + statistics of one VALID collective instance whose head (rank 0) sits at
@@ -466,8 +459,9 @@ __device__ __forceinline__ void expand_block(const FastParams& P, Sink<SH>& sk, 
   }
   // tree shares
   const uint64_t share1 = s - s / 2, share2 = s / 2;
+  const uint32_t dlo = (uint32_t)devs, dhi = (uint32_t)(devs >> 32);
   auto devof = [&](int r) -> int {
-    return packed ? (int)((devs >> (8 * r)) & 0xFF) : (int)R[(p + r) & kRM].dev;
+    return packed ? (int)(__byte_perm(dlo, dhi, (uint32_t)r) & 0xFF) : (int)R[(p + r) & kRM].dev;
   };
   int q = ring ? (int)j0 : 0;
   for (int i = 0; i < n; i++) {
@@ -487,7 +481,8 @@ __device__ __forceinline__ void expand_block(const FastParams& P, Sink<SH>& sk, 
       }
       cnt = rbytes != 0 ? 1 : 0;
     } else if (tree) {
-      w = tree_peers(n, q, share2 != 0, cnt);
+      w = tree_peers(n, q);
+      cnt = (int)(w >> 60);
     } else {
       cnt = 2;
     }
@@ -499,6 +494,7 @@ __device__ __forceinline__ void expand_block(const FastParams& P, Sink<SH>& sk, 
         dst = devof(rd); bytes = rbytes; sub = rd;
       } else if (tree) {
         const uint32_t c = (uint32_t)(w >> (7 * x));
+        if ((c & 0x60) == 0x40 && share2 == 0) continue;  // T2-only edge of a 1-byte payload
         sub = (int)(c & 31);
         dst = devof(sub);
         bytes = (c & 0x60) == 0x60 ? s : ((c & 0x20) ? share1 : share2);
@@ -522,23 +518,21 @@ __device__ __forceinline__ void count_diag(uint32_t st) {
   else if (st == ST_MISMATCH) atomicAdd(&cta_mem().diag[CT_DIAG_MISMATCHED_P2P], 1u);
 }
 
-// copy statistics: one register accumulator per copy kind
+// copy statistics: a one-entry register cache (copy kind, payload, calls)
 struct CopyStats {
-  unsigned long long sum[3];
-  uint32_t cnt[3];
-  __device__ __forceinline__ void add(int t, unsigned long long v) {
-#pragma unroll
-    for (int k = 0; k < 3; k++)
-      if (t == k) {
-        if (sum[k] + v < v) { flush_stat(CT_T_EXPLICIT + k, sum[k], cnt[k]); sum[k] = 0; cnt[k] = 0; }
-        sum[k] += v;
-        cnt[k]++;
-      }
+  uint32_t t;  // 3: empty
+  uint32_t cnt;
+  unsigned long long sum;
+  __device__ __forceinline__ void add(uint32_t k, unsigned long long v) {
+    if (k != t || sum + v < v) {
+      if (t < 3) flush_stat(CT_T_EXPLICIT + t, sum, cnt);
+      t = k; sum = 0; cnt = 0;
+    }
+    sum += v;
+    cnt++;
   }
   __device__ __forceinline__ void drain() {
-#pragma unroll
-    for (int k = 0; k < 3; k++)
-      if (cnt[k]) flush_stat(CT_T_EXPLICIT + k, sum[k], cnt[k]);
+    if (t < 3) flush_stat(CT_T_EXPLICIT + t, sum, cnt);
   }
 };
 
@@ -569,18 +563,7 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
   if (tid < CT_NDIAG) C.diag[tid] = 0;
   if (tid < (kTreeLut + 1) * kTreeLut) {
     const int n = tid / kTreeLut, j = tid % kTreeLut;
-    uint2 e = make_uint2(0xFFFFFFu, 0xFFFFFFu);
-    if (j < n) {
-      int a0, a1, a2, q0, q1, q2;
-      tree_links(n, j, a0, a1, a2);
-      tree_links(n, j == 0 ? n - 1 : j - 1, q0, q1, q2);
-      const int b0 = q0 < 0 ? -1 : (q0 + 1 == n ? 0 : q0 + 1);
-      const int b1 = q1 < 0 ? -1 : (q1 + 1 == n ? 0 : q1 + 1);
-      const int b2 = q2 < 0 ? -1 : (q2 + 1 == n ? 0 : q2 + 1);
-      e.x = (uint32_t)(a0 & 0xFF) | ((uint32_t)(a1 & 0xFF) << 8) | ((uint32_t)(a2 & 0xFF) << 16);
-      e.y = (uint32_t)(b0 & 0xFF) | ((uint32_t)(b1 & 0xFF) << 8) | ((uint32_t)(b2 & 0xFF) << 16);
-    }
-    C.tree_lut[n][j] = e;
+    C.tree_lut[n][j] = j < n ? tree_pack(n, j) : 0ull;
   }
   if (tid == 0) {
     C.flags = 0; C.max_dev = -1; C.oor_key = kNone; C.of_cell = kNone;
@@ -600,7 +583,7 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
   RingAcc racc;
   racc.tag = 0;
   racc.miss = 0;
-  CopyStats cps{{0, 0, 0}, {0, 0, 0}};
+  CopyStats cps{3u, 0u, 0ull};
   int my_max_dev = -1;
   uint32_t copy_seen = 0;              // copy kinds this lane has seen (first index noted)
   uint32_t wflags = 0;
@@ -672,7 +655,7 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
             if (ck != CT_CKIND_H2D) my_max_dev = max(my_max_dev, (int)aux);
             if (ck != CT_CKIND_D2H) my_max_dev = max(my_max_dev, (int)aux2);
             const int t = kind - CT_KIND_MEMCPY;
-            cps.add(t, cnt);
+            cps.add((uint32_t)t, cnt);
             if (!no_expand) {
               const int src = ck == CT_CKIND_H2D ? -1 : (int)aux, dst = ck == CT_CKIND_D2H ? -1 : (int)aux2;
               if (src < P.gcap && dst < P.gcap && (cnt >> 63) == 0) {
