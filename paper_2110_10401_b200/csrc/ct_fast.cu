@@ -615,7 +615,7 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
       }
     uint32_t ready = 0, freed = 0;  // chunks waited for / released (slot re-issued)
     uint32_t qh = 0, qt = 0;        // element queue head / tail
-    int cover = 0;                  // sum of element lengths minus records (tiling check)
+    int cover = 0;                  // element lengths + copies (must equal the range's records)
     uint32_t cross = 0;             // 1: the last queued element extends past the scanned chunks
     uint32_t u = 0;                 // chunk of the oldest queued element (when the queue is not empty)
     const bool stream_only = (P.dbg & 4) != 0, no_expand = (P.dbg & 1) != 0;
@@ -631,16 +631,14 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
         {
           const uint32_t rel = q * 32 + lane;
           const bool act = rel >= s0 && rel < eo;
-          uint4 b = make_uint4(0, 0, 0, 0);
-          if (act) b = reinterpret_cast<const uint4*>(R + (rel & kRM))[1];
+          const uint4 b = reinterpret_cast<const uint4*>(R + (rel & kRM))[1];  // any ring slot is readable
           const int kind = act ? (int)((b.w >> 16) & 7) : 7;
           const uint32_t nr = b.y & 0xFFFF, rk = b.y >> 16, dev = b.z & 0xFFFF;
-          if (act) my_max_dev = max(my_max_dev, (int)dev);
+          my_max_dev = max(my_max_dev, act ? (int)dev : -1);
           const bool isH = (kind == CT_KIND_COLLECTIVE && rk == 0) || kind == CT_KIND_SEND;
           const bool isCp = kind >= CT_KIND_MEMCPY && kind <= CT_KIND_ZEROCOPY;
-          const uint32_t len = kind == CT_KIND_COLLECTIVE ? nr : 2u;
-          const bool badl = isH && (len == 0 || len > (uint32_t)kMaxN || rel + len > eo);
-          cover += (isH ? (int)len : (isCp ? 1 : 0)) - (act ? 1 : 0);
+          const uint32_t len = kind == CT_KIND_COLLECTIVE ? nr : 2u;  // of a head (checked by the join)
+          cover += isCp ? 1 : 0;
           const unsigned hm = __ballot_sync(kFull, isH);
           if (isH) W.q[(qt + __popc(hm & lt)) & kQM] = rel;
           if (qt == qh && hm) u = q;  // the queue's oldest element now starts in this chunk
@@ -673,7 +671,6 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
               atomicMin(&C.copy_first[t], rb0 + rel);
             }
           }
-          if (__any_sync(kFull, badl)) { wflags |= F_NONCANON; bail = true; break; }
         }
         __syncwarp();
 
@@ -685,9 +682,8 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
           const uint32_t nb = min(32u, qt - qh - cross);
           const bool act = (uint32_t)lane < nb;
           const uint32_t p = act ? W.q[(qh + lane) & kQM] : 0u;
-          Rec h{};
-          int kind = 7;
-          if (act) { h = ring_rec(R, p); kind = h.kind(); }
+          const Rec h = ring_rec(R, p);  // inactive lanes read slot 0 and are ignored
+          const int kind = act ? h.kind() : 7;
           const bool isC = kind == CT_KIND_COLLECTIVE, isS = kind == CT_KIND_SEND;
           bool bad = false;
 
@@ -725,6 +721,12 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
           const bool hist = pl < 0 && tsn != 0;
           const uint32_t n = h.nranks;
           if (isC && (pl >= 0 ? pn != n : (tsn != 0 && tsn != n))) bad = true;  // grouping.py:104-108
+          {  // the element lies inside the range; lengths tile it (with the copies)
+            const uint32_t len = isC ? n : (isS ? 2u : 0u);
+            if (isC && (n == 0 || n > (uint32_t)kMaxN)) bad = true;
+            if (p + len > eo) bad = true;
+            cover += (int)len;
+          }
 
           // ---- validation (lane walks its element)
           uint32_t st = ST_NONE;
@@ -742,6 +744,7 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
             const uint32_t rootm = h.has_root() ? 0xFFFF0000u : 0u, hw6 = h.aux << 16;
             uint32_t badw = 0, incw = 0;
             bool ord = false, big = false, dup = false;
+            const bool have = pl >= 0 || hist;
             unsigned long long dm = 0;
             auto vrec = [&](uint32_t j) {  // one member record (independent across j)
               const uint32_t ix = (p + j) & kRM;
@@ -750,19 +753,17 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
               badw |= (wb.x ^ h.comm) | (wb.y ^ (n | (j << 16))) | (x7 & 0x00070000u);  // kind, comm, n, rank
               incw |= (wa.x ^ hc0) | (wa.y ^ hc1) | (x7 & 0x3F780000u) | ((wb.z ^ hw6) & rootm);  // signature
               const unsigned long long seq = ((unsigned long long)wa.w << 32) | wa.z;
-              if (pl >= 0 || hist) {
-                const uint64_t* ps = pl >= 0 ? &R[(ppos + j) & kRM].seq : reinterpret_cast<const uint64_t*>(&W.cseq[hs][j]);
-                if (!(*ps < seq)) ord = true;
-              }
+              // previous block of the comm: this batch (ring) or the slot table (always a valid
+              // address; ignored without history)
+              const uint64_t* ps = pl >= 0 ? &R[(ppos + j) & kRM].seq : reinterpret_cast<const uint64_t*>(&W.cseq[hs][j]);
+              const unsigned long long pv = *ps;
+              ord |= have & (pv >= seq);
               const uint32_t dv = wb.z & 0xFFFF;
-              if (dv < 64) {
-                const unsigned long long bit = 1ull << dv;
-                dup = dup || (dm & bit) != 0;
-                dm |= bit;
-                devs |= (unsigned long long)dv << (8 * (j & 7));
-              } else {
-                big = true;
-              }
+              const unsigned long long bit = dv < 64 ? 1ull << dv : 0ull;
+              big |= dv >= 64;
+              dup |= (dm & bit) != 0;
+              dm |= bit;
+              devs |= (unsigned long long)(dv & 0xFF) << (8 * (j & 7));
             };
             uint32_t j = j0;
             uint32_t i = 0;
@@ -846,7 +847,7 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
     }
     if (!bail && !(P.dbg & 4)) {  // element lengths must tile the range exactly
       const int tot = __reduce_add_sync(kFull, cover);
-      if (tot != 0) wflags |= F_NONCANON;
+      if (tot != (int)(eo - s0)) wflags |= F_NONCANON;
     }
     const uint32_t issued = min(freed + (uint32_t)kRing, lastc);
     for (uint32_t q = ready; q < issued; q++)  // drain outstanding bulk copies
