@@ -26,8 +26,9 @@ struct __align__(16) WarpMem {
 constexpr int kTreeLut = 16;
 
 struct __align__(16) CtaMem {
-  // per-type statistics: payload = pay_a + pay_b * 2^32 (exact, no return-value atomics)
-  unsigned long long calls[kTypes], pay_a[kTypes], pay_b[kTypes];
+  // per-type statistics as 32-bit limbs (native shared atomics): [0,4) payload (128-bit),
+  // [4,6) calls (64-bit)
+  uint32_t st[kTypes][8];
   unsigned long long copy_first[3];
   unsigned long long oor_key;   // min out-of-range ordering key seen by the CTA
   unsigned long long of_cell;   // min cell index whose 64-bit sum wrapped
@@ -135,11 +136,38 @@ __device__ __noinline__ uint32_t note_overflow(unsigned long long key) {
   return F_OVERFLOW;
 }
 
-__device__ __noinline__ void flush_stat(uint32_t t, unsigned long long v, uint32_t c) {
-  CtaMem& C = cta_mem();
-  atomicAdd(&C.pay_a[t], v & 0xFFFFFFFFull);
-  atomicAdd(&C.pay_b[t], v >> 32);
-  atomicAdd(&C.calls[t], (unsigned long long)c);
+// statistics of type t: payload += (hi:lo), calls += c, carried limb by limb
+__device__ __noinline__ void stat_limbs(uint32_t t, unsigned long long lo, unsigned long long hi, uint32_t c) {
+  uint32_t* L = cta_mem().st[t];
+  unsigned long long carry = 0;
+#pragma unroll
+  for (int k = 0; k < 4; k++) {
+    const unsigned long long add = ((k < 2 ? lo >> (32 * k) : hi >> (32 * (k - 2))) & 0xFFFFFFFFull) + carry;
+    carry = add >> 32;
+    const uint32_t a32 = (uint32_t)add;
+    if (a32) {
+      const uint32_t old = atomicAdd(&L[k], a32);
+      carry += old + a32 < old ? 1u : 0u;
+    }
+  }
+  const uint32_t old = atomicAdd(&L[4], c);
+  if (old + c < old) atomicAdd(&L[5], 1u);
+}
+
+// calls += 1, payload += v: the common case inline (two limbs), carries out of line
+__device__ __forceinline__ void stat1(uint32_t t, unsigned long long v) {
+  uint32_t* L = cta_mem().st[t];
+  const uint32_t a = (uint32_t)v, b = (uint32_t)(v >> 32);
+  const uint32_t o0 = atomicAdd(&L[0], a);
+  const uint32_t c0 = o0 + a < o0 ? 1u : 0u;
+  if (b == 0xFFFFFFFFu && c0) {
+    stat_limbs(t, 0, 1, 0);  // 2^64
+  } else if (b + c0) {
+    const uint32_t o1 = atomicAdd(&L[1], b + c0);
+    if (o1 + (b + c0) < o1) stat_limbs(t, 0, 1, 0);  // carry into limb 2
+  }
+  const uint32_t oc = atomicAdd(&L[4], 1u);
+  if (oc == 0xFFFFFFFFu) atomicAdd(&L[5], 1u);
 }
 
 // Transfers are added straight into the CTA histogram; statistics of the collective
@@ -149,16 +177,12 @@ struct Sink {
   const FastParams& P;
   uint32_t flags;
   unsigned long long rec_key;  // (class << 62) | (element << 21) | (src rank << 11) for oor ordering
-  unsigned long long ssum[6];
-  uint32_t scnt[6];
   uint32_t nc;  // cells per array
 
   __device__ __forceinline__ explicit Sink(const FastParams& p) : P(p) {
     nc = (uint32_t)(kTypes * p.g2 * p.g2);
     flags = 0;
     rec_key = 0;
-#pragma unroll
-    for (int k = 0; k < 6; k++) { ssum[k] = 0; scnt[k] = 0; }
   }
 
   __device__ __forceinline__ void add(uint32_t key, unsigned long long v, uint32_t c = 1) {
@@ -193,29 +217,10 @@ struct Sink {
     add((uint32_t)((type * P.g2 + a) * P.g2 + b), (unsigned long long)bytes);
   }
 
-  // stats: calls += 1, payload += s (128-bit capable; s < 2^72)
+  // stats: calls += 1, payload += s (128-bit capable)
   __device__ __forceinline__ void stat(int type, unsigned __int128 s) {
-    if ((s >> 63) == 0 && type < 6) {
-      const unsigned long long v = (unsigned long long)s;
-#pragma unroll
-      for (int k = 0; k < 6; k++)
-        if (type == k) {
-          if (ssum[k] + v < v) { flush_stat(k, ssum[k], scnt[k]); ssum[k] = 0; scnt[k] = 0; }
-          ssum[k] += v;
-          scnt[k]++;
-        }
-      return;
-    }
-    CtaMem& C = cta_mem();
-    atomicAdd(&C.pay_a[type], (unsigned long long)s & 0xFFFFFFFFull);
-    atomicAdd(&C.pay_b[type], (unsigned long long)(s >> 32));
-    atomicAdd(&C.calls[type], 1ull);
-  }
-
-  __device__ __forceinline__ void drain() {
-#pragma unroll
-    for (int k = 0; k < 6; k++)
-      if (scnt[k]) flush_stat(k, ssum[k], scnt[k]);
+    if ((s >> 64) == 0) stat1((uint32_t)type, (unsigned long long)s);
+    else stat_limbs((uint32_t)type, (unsigned long long)s, (unsigned long long)(s >> 64), 1u);
   }
 };
 
@@ -228,9 +233,11 @@ struct Sink {
 template <bool SH>
 __device__ __noinline__ uint32_t flush_ring(const FastParams& P, int g2, uint32_t nc, uint32_t tag,
                                             unsigned long long devs, unsigned long long g_lo, uint32_t g_hi,
-                                            unsigned long long d_lo, uint32_t d_hi, uint32_t cnt) {
+                                            unsigned long long d_lo, uint32_t d_hi, uint32_t cnt,
+                                            unsigned long long s_lo, uint32_t s_hi) {
   Sink<SH> sk(P);
   const int coll = tag & 0xFF, n = (int)(tag >> 8);
+  stat_limbs((uint32_t)coll, s_lo, s_hi, cnt);
   const int a = n - 2, b = n >= 3 ? n - 3 : n - 1;
   for (int q = 0; q < n; q++) {
     const int qn = q + 1 == n ? 0 : q + 1;
@@ -254,31 +261,32 @@ __device__ __noinline__ uint32_t flush_ring(const FastParams& P, int g2, uint32_
 struct RingAcc {
   uint32_t tag;                 // coll | n << 8 (0: empty)
   unsigned long long devs;
-  unsigned long long g_lo, d_lo;
-  uint32_t g_hi, d_hi, cnt;
+  unsigned long long g_lo, d_lo, s_lo;  // edge sums, payload sum
+  uint32_t g_hi, d_hi, s_hi, cnt;
   uint32_t miss;                // consecutive instances that did not match the key
 
   template <bool SH>
   __device__ __forceinline__ void flush(Sink<SH>& sk, int g2) {
-    sk.flags |= flush_ring<SH>(sk.P, g2, sk.nc, tag, devs, g_lo, g_hi, d_lo, d_hi, cnt);
+    sk.flags |= flush_ring<SH>(sk.P, g2, sk.nc, tag, devs, g_lo, g_hi, d_lo, d_hi, cnt, s_lo, s_hi);
   }
 
   // false: the key differs and is kept (the caller expands the instance itself); after a
   // streak of misses the accumulator is flushed and re-keyed
   template <bool SH>
   __device__ __forceinline__ bool add(Sink<SH>& sk, int g2, uint32_t t, unsigned long long dv, unsigned long long g,
-                                      unsigned long long d) {
+                                      unsigned long long d, unsigned long long sz) {
     if (t != tag || dv != devs) {
       if (tag && ++miss < 8) return false;
       if (tag) flush(sk, g2);
       tag = t; devs = dv;
-      g_lo = d_lo = 0; g_hi = d_hi = cnt = 0;
+      g_lo = d_lo = s_lo = 0; g_hi = d_hi = s_hi = cnt = 0;
     }
     miss = 0;
-    const unsigned long long x = g_lo + g, y = d_lo + d;
+    const unsigned long long x = g_lo + g, y = d_lo + d, z = s_lo + sz;
     g_hi += x < g ? 1u : 0u;
     d_hi += y < d ? 1u : 0u;
-    g_lo = x; d_lo = y;
+    s_hi += z < sz ? 1u : 0u;
+    g_lo = x; d_lo = y; s_lo = z;
     cnt++;
     if (cnt == 0xFFFFFFFFu) { flush(sk, g2); tag = 0; }
     return true;
@@ -299,7 +307,6 @@ __device__ __noinline__ uint32_t expand_wide(const FastParams& P, const ct_recor
   Sink<SH> sk(P);
   sk.rec_key = rec_key;
   expand_collective<unsigned __int128>(P.ex, wdv, sk, rc, head);
-  sk.drain();
   return sk.flags;
 }
 
@@ -430,6 +437,23 @@ __device__ __forceinline__ void expand_block(const FastParams& P, Sink<SH>& sk, 
     if (algo == CT_ALGO_TREE || algo == CT_ALGO_COLLNET) { sk.flags |= F_WRONG_ALGO; return; }
     algo = CT_ALGO_RING;
   }
+  const int g2 = P.g2;
+  const bool ring = algo == CT_ALGO_RING, tree = algo == CT_ALGO_TREE;
+  // ring family
+  const bool rmap = ring && n == P.ex.ring_len;
+  const int root_pos = rmap ? (h.has_root() ? (int)P.ex.ring_inv[h.aux] : 0) : (int)h.aux;
+  const int skip_pos = coll == CT_COLL_BROADCAST ? (root_pos == 0 ? n - 1 : root_pos - 1)
+                                                 : (coll == CT_COLL_REDUCE ? root_pos : -1);
+  const uint64_t chunk = ring && coll == CT_COLL_ALLREDUCE ? ceil_div(s, (uint32_t)n) : 0;
+  // allreduce blocks b[i] (decompose.py:104-107): chunk for i < n-1 and the remainder
+  // s - (n-1)*chunk for i = n-1 unless s is tiny (then trailing blocks are empty)
+  const bool simple = ring && coll == CT_COLL_ALLREDUCE && (uint64_t)(n - 1) * chunk < s;
+  const uint64_t gen = 2 * s - 2 * chunk, dlt = chunk - (s - (uint64_t)(n - 1) * chunk);
+  const uint64_t fixed = scatter ? s - blk : s;
+  if (ring && fastdev && packed && !rmap && n >= 2 && s != 0 && (simple || scatter)) {  // register accumulator
+    if (ra.add(sk, g2, (uint32_t)coll | ((uint32_t)n << 8), devs, simple ? gen : fixed, simple ? dlt : 0ull, s))
+      return;
+  }
   sk.stat(coll, (unsigned __int128)s);
   if (algo == CT_ALGO_COLLNET) {
     if (s == 0) return;
@@ -440,23 +464,7 @@ __device__ __forceinline__ void expand_block(const FastParams& P, Sink<SH>& sk, 
     }
     if (n == 1 || s == 0) return;
   }
-  const int g2 = P.g2;
-  const bool ring = algo == CT_ALGO_RING, tree = algo == CT_ALGO_TREE;
-  // ring family
-  const bool rmap = ring && n == P.ex.ring_len;
   if (rmap && !P.ex.ring_valid) { sk.flags |= F_BAD_RING; return; }
-  const int root_pos = rmap ? (h.has_root() ? (int)P.ex.ring_inv[h.aux] : 0) : (int)h.aux;
-  const int skip_pos = coll == CT_COLL_BROADCAST ? (root_pos == 0 ? n - 1 : root_pos - 1)
-                                                 : (coll == CT_COLL_REDUCE ? root_pos : -1);
-  const uint64_t chunk = ring && coll == CT_COLL_ALLREDUCE ? ceil_div(s, (uint32_t)n) : 0;
-  // allreduce blocks b[i] (decompose.py:104-107): chunk for i < n-1 and the remainder
-  // s - (n-1)*chunk for i = n-1 unless s is tiny (then trailing blocks are empty)
-  const bool simple = ring && coll == CT_COLL_ALLREDUCE && (uint64_t)(n - 1) * chunk < s;
-  const uint64_t gen = 2 * s - 2 * chunk, dlt = chunk - (s - (uint64_t)(n - 1) * chunk);
-  const uint64_t fixed = scatter ? s - blk : s;
-  if (ring && fastdev && packed && !rmap && (simple || scatter)) {  // uniform: register accumulator
-    if (ra.add(sk, g2, (uint32_t)coll | ((uint32_t)n << 8), devs, simple ? gen : fixed, simple ? dlt : 0ull)) return;
-  }
   // tree shares
   const uint64_t share1 = s - s / 2, share2 = s / 2;
   const uint32_t dlo = (uint32_t)devs, dhi = (uint32_t)(devs >> 32);
@@ -525,14 +533,14 @@ struct CopyStats {
   unsigned long long sum;
   __device__ __forceinline__ void add(uint32_t k, unsigned long long v) {
     if (k != t || sum + v < v) {
-      if (t < 3) flush_stat(CT_T_EXPLICIT + t, sum, cnt);
+      if (t < 3) stat_limbs(CT_T_EXPLICIT + t, sum, 0, cnt);
       t = k; sum = 0; cnt = 0;
     }
     sum += v;
     cnt++;
   }
   __device__ __forceinline__ void drain() {
-    if (t < 3) flush_stat(CT_T_EXPLICIT + t, sum, cnt);
+    if (t < 3) stat_limbs(CT_T_EXPLICIT + t, sum, 0, cnt);
   }
 };
 
@@ -558,7 +566,7 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
   // ---- init
   if (SH)
     for (int c = tid; c < 3 * ncell; c += kThreads) shl[c] = 0;
-  if (tid < kTypes) { C.calls[tid] = 0; C.pay_a[tid] = 0; C.pay_b[tid] = 0; }
+  if (tid < kTypes * 8) (&C.st[0][0])[tid] = 0;
   if (tid < 3) C.copy_first[tid] = kNone;
   if (tid < CT_NDIAG) C.diag[tid] = 0;
   if (tid < (kTreeLut + 1) * kTreeLut) {
@@ -872,7 +880,6 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
 
   // ---- CTA epilogue: drain caches, one global merge
   if (racc.tag) racc.flush(sk, P.g2);
-  sk.drain();
   cps.drain();
   atomicMax(&C.max_dev, my_max_dev);
   if (sk.flags | wflags) atomicOr(&C.flags, sk.flags | wflags);
@@ -892,11 +899,11 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
     if (of) atomicOr(&C.flags, of);
   }
   if (tid < kTypes) {
-    const unsigned long long a = C.pay_a[tid], b = C.pay_b[tid], c = C.calls[tid];
+    const uint32_t* L = C.st[tid];
+    const unsigned long long c = L[4] | ((unsigned long long)L[5] << 32);
     if (c) {
-      // payload = a + b * 2^32 as 128 bits
-      const unsigned long long lo = a + (b << 32);
-      const unsigned long long hi = (b >> 32) + (lo < a ? 1ull : 0ull);
+      const unsigned long long lo = L[0] | ((unsigned long long)L[1] << 32);
+      const unsigned long long hi = L[2] | ((unsigned long long)L[3] << 32);
       const unsigned long long old = atomicAdd(&G->pay_lo[tid], lo);
       atomicAdd(&G->pay_hi[tid], hi + (old + lo < old ? 1ull : 0ull));
       atomicAdd(&G->calls[tid], c);
