@@ -644,10 +644,11 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
           const uint32_t nr = b.y & 0xFFFF, rk = b.y >> 16, dev = b.z & 0xFFFF;
           my_max_dev = max(my_max_dev, act ? (int)dev : -1);
           const bool isH = (kind == CT_KIND_COLLECTIVE && rk == 0) || kind == CT_KIND_SEND;
-          const bool isCp = kind >= CT_KIND_MEMCPY && kind <= CT_KIND_ZEROCOPY;
+          const bool isCp = (uint32_t)(kind - CT_KIND_MEMCPY) < 3u;
           const uint32_t len = kind == CT_KIND_COLLECTIVE ? nr : 2u;  // of a head (checked by the join)
-          cover += isCp ? 1 : 0;
           const unsigned hm = __ballot_sync(kFull, isH);
+          const unsigned cpm = __ballot_sync(kFull, isCp);
+          cover += lane == 0 ? __popc(cpm) : 0;
           if (isH) W.q[(qt + __popc(hm & lt)) & kQM] = rel;
           if (qt == qh && hm) u = q;  // the queue's oldest element now starts in this chunk
           qt += __popc(hm);
@@ -807,8 +808,15 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
             if (lastb) {
               W.sn[hs] = n;
               W.clast[hs] = gi;
-              for (uint32_t j = 0; j < n; j++) W.cseq[hs][j] = R[(p + j) & kRM].seq;
             }
+          }
+          // the last block of each comm becomes the slot's seq table: one block per step,
+          // lane = rank
+          for (unsigned lb = __ballot_sync(kFull, lastb); lb; lb &= lb - 1) {
+            const int L = __ffs(lb) - 1;
+            const uint32_t pL = __shfl_sync(kFull, p, L), nL = __shfl_sync(kFull, n, L);
+            const int sL = __shfl_sync(kFull, hs, L);
+            if ((uint32_t)lane < nL) W.cseq[sL][lane] = R[(pL + lane) & kRM].seq;
           }
           if (tf_pend) {  // first valid instance per (comm slot, type): only until recorded once
             const unsigned long long bit = (isC && st == ST_VALID) ? 1ull << (hs * 5 + h.coll()) : 0ull;
