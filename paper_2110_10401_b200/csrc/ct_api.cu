@@ -151,6 +151,8 @@ int run_fast(ct_context* c, const ct_record* recs, uint64_t n, int gcap, bool ex
   P.total_warps = total_warps;
   P.n_chunks = n_chunks;
   P.dbg = getenv("CT_DEBUG_MODE") ? atoi(getenv("CT_DEBUG_MODE")) : 0;
+  P.sa_flush = 1u << 14;  // CT_SA_FLUSH (tests): write slot accumulators out more often
+  if (getenv("CT_SA_FLUSH")) P.sa_flush = (uint32_t)std::min(std::max(atoi(getenv("CT_SA_FLUSH")), 1), 1 << 14);
   uint32_t launches = 0;  // kernels launched (cudaMemset/Memcpy are copy-engine work)
   out->ms_kernel = 0;
   if (n) {

@@ -12,8 +12,24 @@ constexpr unsigned kFull = 0xFFFFFFFFu;
 constexpr uint32_t kQM = kQ - 1;
 static_assert((kQ & (kQ - 1)) == 0 && kQ >= 64, "queue holds < 32 carried + 32 new heads");
 
+// Shared-memory accumulator of repeated instances of one (comm slot, class): class 0 ring
+// allreduce (every block but the last full), 1 allgather, 2 reduce-scatter, 3 tree
+// allreduce.  Sums are 64-bit as two 32-bit limbs (native atomics) and are written to the
+// histogram before they can wrap (kSAFlush instances).
+struct __align__(16) SAE {
+  uint32_t key;               // 1 << 31 | slot | cls << 3 | coll << 5 | n << 8; 0: empty
+  uint32_t cnt;               // instances
+  unsigned long long devs;    // device of rank j in byte j
+  uint32_t g[2], d[2], s[2];  // edge sums (ring: gen / dlt; tree: ceil(S/2) / floor(S/2)), payload
+  uint32_t cnt2;              // tree: instances with floor(S/2) != 0
+  uint32_t pad;
+};
+constexpr int kSE = 16;             // slot accumulators per warp
+constexpr uint32_t kSAFlush = 1u << 14;  // default write-out threshold (FastParams::sa_flush)
+
 struct __align__(16) WarpMem {
   ct_record ring[kRing][32];                 // TMA ring: chunk k lives in slot k % kRing
+  SAE sa[kSE];
   unsigned long long cseq[kCS][kMaxN];       // last collective block of the comm: seq per rank
   unsigned long long bar[kRing];
   unsigned long long cfirst[kCS], clast[kCS];
@@ -230,32 +246,59 @@ struct Sink {
 // but the last full (gen = 2S - 2 chunk, dlt = chunk - last block), allgather /
 // reduce-scatter (gen = (n-1) * block, dlt = 0).  Instances with the same (type, n,
 // devices) add into 128-bit sums; the n cells are written when the key changes.
+__device__ __forceinline__ unsigned long long tree_peers(int n, int j);
+
+// Write accumulated instances of one (type, n, devices) key into the histogram:
+// ring classes -- the edge leaving position q carries g + d * ([q == n-2] + [q == n-3]);
+// tree -- T1-only peers g, peers in both trees g + d, T2-only peers d (cnt2 transfers).
 template <bool SH>
-__device__ __noinline__ uint32_t flush_ring(const FastParams& P, int g2, uint32_t nc, uint32_t tag,
-                                            unsigned long long devs, unsigned long long g_lo, uint32_t g_hi,
-                                            unsigned long long d_lo, uint32_t d_hi, uint32_t cnt,
-                                            unsigned long long s_lo, uint32_t s_hi) {
+__device__ __noinline__ uint32_t flush_acc(const FastParams& P, int g2, int coll, int n, bool tree,
+                                           unsigned long long devs, unsigned long long g_lo, uint32_t g_hi,
+                                           unsigned long long d_lo, uint32_t d_hi, unsigned long long s_lo,
+                                           uint32_t s_hi, uint32_t cnt, uint32_t cnt2) {
   Sink<SH> sk(P);
-  const int coll = tag & 0xFF, n = (int)(tag >> 8);
   stat_limbs((uint32_t)coll, s_lo, s_hi, cnt);
-  const int a = n - 2, b = n >= 3 ? n - 3 : n - 1;
-  for (int q = 0; q < n; q++) {
-    const int qn = q + 1 == n ? 0 : q + 1;
-    const uint32_t k = (uint32_t)(q == a) + (uint32_t)(q == b);
-    // v = g + k * d as 128 bits
-    unsigned long long lo = g_lo;
-    unsigned __int128 hi = g_hi;
-    for (uint32_t t = 0; t < k; t++) {
-      const unsigned long long x = lo + d_lo;
-      hi += (unsigned __int128)d_hi + (x < lo ? 1u : 0u);
-      lo = x;
+  const uint32_t dlo = (uint32_t)devs, dhi = (uint32_t)(devs >> 32);
+  auto emit = [&](int q, int r, uint32_t k_g, uint32_t k_d, uint32_t c) {
+    // v = k_g * g + k_d * d as 128 bits (k_* in {0, 1, 2})
+    unsigned __int128 v = (unsigned __int128)k_g * (((unsigned __int128)g_hi << 64) | g_lo) +
+                          (unsigned __int128)k_d * (((unsigned __int128)d_hi << 64) | d_lo);
+    const uint32_t key = (uint32_t)((coll * g2 + (int)(__byte_perm(dlo, dhi, (uint32_t)q) & 0xFF) + 2) * g2 +
+                                    (int)(__byte_perm(dlo, dhi, (uint32_t)r) & 0xFF) + 2);
+    if ((v >> 63) != 0) sk.flags |= note_overflow(key);  // the cell exceeds 2^63 - 1
+    else sk.add(key, (unsigned long long)v, c);
+  };
+  if (!tree) {
+    const int a = n - 2, b = n >= 3 ? n - 3 : n - 1;
+    for (int q = 0; q < n; q++) emit(q, q + 1 == n ? 0 : q + 1, 1u, (uint32_t)(q == a) + (uint32_t)(q == b), cnt);
+  } else {
+    for (int j = 0; j < n; j++) {
+      const unsigned long long w = tree_peers(n, j);
+      const int c = (int)(w >> 60);
+      for (int x = 0; x < c; x++) {
+        const uint32_t code = (uint32_t)(w >> (7 * x));
+        const int r = (int)(code & 31);
+        if ((code & 0x60) == 0x60) emit(j, r, 1u, 1u, cnt);
+        else if (code & 0x20) emit(j, r, 1u, 0u, cnt);
+        else if (cnt2) emit(j, r, 0u, 1u, cnt2);
+      }
     }
-    const uint32_t key = (uint32_t)((coll * g2 + (int)((devs >> (8 * q)) & 0xFF) + 2) * g2 +
-                                    (int)((devs >> (8 * qn)) & 0xFF) + 2);
-    if (hi != 0 || (lo >> 63) != 0) sk.flags |= note_overflow(key);  // the cell exceeds 2^63 - 1
-    else sk.add(key, lo, cnt);
   }
   return sk.flags;
+}
+
+// Write out slot accumulator E, then re-key it to ``key`` (with ``devs``) unless key is 0.
+template <bool SH>
+__device__ __noinline__ uint32_t sa_flush(const FastParams& P, SAE* E, uint32_t key, unsigned long long devs) {
+  uint32_t f = 0;
+  if (E->key && E->cnt)
+    f = flush_acc<SH>(P, P.g2, (int)(E->key >> 5 & 7u), (int)(E->key >> 8 & 0xFFu), (E->key >> 3 & 3u) == 3u, E->devs,
+                      E->g[0] | ((unsigned long long)E->g[1] << 32), 0u, E->d[0] | ((unsigned long long)E->d[1] << 32),
+                      0u, E->s[0] | ((unsigned long long)E->s[1] << 32), 0u, E->cnt, E->cnt2);
+  if (key) { E->key = key; E->devs = devs; }
+  E->g[0] = E->g[1] = E->d[0] = E->d[1] = E->s[0] = E->s[1] = 0;
+  E->cnt = E->cnt2 = 0;
+  return f;
 }
 
 struct RingAcc {
@@ -267,7 +310,8 @@ struct RingAcc {
 
   template <bool SH>
   __device__ __forceinline__ void flush(Sink<SH>& sk, int g2) {
-    sk.flags |= flush_ring<SH>(sk.P, g2, sk.nc, tag, devs, g_lo, g_hi, d_lo, d_hi, cnt, s_lo, s_hi);
+    sk.flags |= flush_acc<SH>(sk.P, g2, (int)(tag & 0xFF), (int)(tag >> 8), false, devs, g_lo, g_hi, d_lo, d_hi,
+                              s_lo, s_hi, cnt, 0u);
   }
 
   // false: the key differs and is kept (the caller expands the instance itself); after a
@@ -405,6 +449,20 @@ __device__ __forceinline__ unsigned long long tree_peers(int n, int j) {
   return n <= kTreeLut ? cta_mem().tree_lut[n][j] : tree_pack_big(n, j);
 }
 
+// a lane's follow-up on the warp's slot accumulator after a batch: entry e is full
+// (key 0) or held another key (re-key to ``key``)
+struct SAReq {
+  uint32_t e, key;
+  bool act;
+};
+
+__device__ __forceinline__ void limb_add(uint32_t* L, unsigned long long v) {  // v < 2^63, no wrap
+  const uint32_t a = (uint32_t)v;
+  const uint32_t o = atomicAdd(L, a);
+  const uint32_t h = (uint32_t)(v >> 32) + (o + a < o ? 1u : 0u);
+  if (h) atomicAdd(L + 1, h);
+}
+
 // Expansion + statistics of one VALID collective instance whose head (rank 0) sits at
 // ring position p; gidx is its global record index.  Rank-attributed rules (ct_common.cuh,
 // SURVEY App. A): ring family -- the record at ring position q (rank order[q]) sends to
@@ -415,7 +473,7 @@ __device__ __forceinline__ unsigned long long tree_peers(int n, int j) {
 template <bool SH>
 __device__ __forceinline__ void expand_block(const FastParams& P, Sink<SH>& sk, const ct_record* R, const Rec& h,
                                              uint32_t p, uint64_t gidx, uint32_t j0, bool fastdev, bool packed,
-                                             unsigned long long devs, RingAcc& ra) {
+                                             unsigned long long devs, RingAcc& ra, int slot, SAE* sa, SAReq& sq) {
   const int n = (int)h.nranks, coll = h.coll();
   const unsigned long long base = min((unsigned long long)gidx, (1ull << 41) - 1) << 21;
   if ((h.count >> 40) != 0) {
@@ -450,9 +508,26 @@ __device__ __forceinline__ void expand_block(const FastParams& P, Sink<SH>& sk, 
   const bool simple = ring && coll == CT_COLL_ALLREDUCE && (uint64_t)(n - 1) * chunk < s;
   const uint64_t gen = 2 * s - 2 * chunk, dlt = chunk - (s - (uint64_t)(n - 1) * chunk);
   const uint64_t fixed = scatter ? s - blk : s;
-  if (ring && fastdev && packed && !rmap && n >= 2 && s != 0 && (simple || scatter)) {  // register accumulator
-    if (ra.add(sk, g2, (uint32_t)coll | ((uint32_t)n << 8), devs, simple ? gen : fixed, simple ? dlt : 0ull, s))
-      return;
+  if (fastdev && packed && !rmap && n >= 2 && s != 0) {
+    if (ring && (simple || scatter)) {  // per-lane register accumulator
+      if (ra.add(sk, g2, (uint32_t)coll | ((uint32_t)n << 8), devs, simple ? gen : fixed, simple ? dlt : 0ull, s))
+        return;
+    }
+    if (slot >= 0 && ((ring && (simple || scatter)) || tree)) {  // the warp's slot accumulator
+      const uint32_t cls = tree ? 3u : (coll == CT_COLL_ALLREDUCE ? 0u : (coll == CT_COLL_ALLGATHER ? 1u : 2u));
+      const uint32_t e = ((((uint32_t)slot & 3u) << 2) | cls) ^ (((uint32_t)slot >> 2) << 1);
+      const uint32_t key = 0x80000000u | (uint32_t)slot | (cls << 3) | ((uint32_t)coll << 5) | ((uint32_t)n << 8);
+      SAE& E = sa[e];
+      if (E.key == key && E.devs == devs) {
+        limb_add(E.g, tree ? s - s / 2 : (simple ? gen : fixed));
+        limb_add(E.d, tree ? s / 2 : (simple ? dlt : 0ull));
+        limb_add(E.s, s);
+        if (tree && s / 2 != 0) atomicAdd(&E.cnt2, 1u);
+        if (atomicAdd(&E.cnt, 1u) + 1 == P.sa_flush) { sq.e = e; sq.key = 0; sq.act = true; }  // write out after the batch
+        return;
+      }
+      sq.e = e; sq.key = key; sq.act = true;  // re-key after the batch; this instance is expanded now
+    }
   }
   sk.stat(coll, (unsigned __int128)s);
   if (algo == CT_ALGO_COLLNET) {
@@ -576,6 +651,7 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
   if (tid == 0) {
     C.flags = 0; C.max_dev = -1; C.oor_key = kNone; C.of_cell = kNone;
   }
+  if (lane < kSE) { W.sa[lane].key = 0; W.sa[lane].cnt = 0; }
   if (lane < kCS) {
     W.tag[lane] = kEmptyTag; W.sn[lane] = 0;
     W.cfirst[lane] = kNone; W.clast[lane] = kNone;
@@ -829,15 +905,22 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
           __syncwarp();
 
           // ---- expansion + accumulation of valid elements
+          SAReq sq{0u, 0u, false};
           if (st == ST_VALID && !no_expand) {
             if (isC) {
-              expand_block<SH>(P, sk, R, h, p, rb0 + p, j0, fastdev, packed, devs, racc);
+              expand_block<SH>(P, sk, R, h, p, rb0 + p, j0, fastdev, packed, devs, racc, slot, W.sa, sq);
             } else {  // matched send/recv pair (decompose.py:319-339)
               const unsigned __int128 nbytes = (unsigned __int128)h.count * (unsigned)dtype_width(h.dtype());
               sk.stat(CT_T_SENDRECV, nbytes);
               sk.rec_key = (1ull << 62) | (min((unsigned long long)(rb0 + p), (1ull << 41) - 1) << 21);
               if (rdev != h.dev) sk.edge(CT_T_SENDRECV, (int)h.dev, (int)rdev, nbytes);
             }
+          }
+          if (__any_sync(kFull, sq.act)) {  // slot accumulators: one lane per entry writes out / re-keys
+            __syncwarp();
+            const unsigned grp = __match_any_sync(kFull, sq.act ? sq.e : (0x100u | (uint32_t)lane));
+            if (sq.act && (grp >> lane) == 1u) sk.flags |= sa_flush<SH>(P, &W.sa[sq.e], sq.key, devs);
+            __syncwarp();
           }
           qh += nb;
           if (qt != qh) u = W.q[qh & kQM] / 32;
@@ -888,6 +971,7 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
 
   // ---- CTA epilogue: drain caches, one global merge
   if (racc.tag) racc.flush(sk, P.g2);
+  if (lane < kSE && W.sa[lane].key && W.sa[lane].cnt) sk.flags |= sa_flush<SH>(P, &W.sa[lane], 0u, 0ull);
   cps.drain();
   atomicMax(&C.max_dev, my_max_dev);
   if (sk.flags | wflags) atomicOr(&C.flags, sk.flags | wflags);

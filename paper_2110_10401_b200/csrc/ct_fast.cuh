@@ -86,6 +86,7 @@ struct FastParams {
   P2PEntry* chans;            // [total warps][kPC]
   uint32_t total_warps;
   uint64_t n_chunks;          // ceil(n / 32)
+  uint32_t sa_flush;          // slot accumulator write-out threshold (instances, <= 2^14)
   int dbg;                    // diagnostic knobs (CT_DEBUG_MODE): 1 skip expansion, 4 stream only
 };
 

@@ -145,6 +145,19 @@ def test_mixed_canonical_with_diagnostics(seed):
     assert sum(s.diag) > 0
 
 
+def test_slot_accumulator_write_outs(monkeypatch):
+    """Many communicators of different sizes (the per-lane accumulator cannot hold them;
+    the warp's slot accumulators do) with the write-out threshold forced down to 3
+    instances, so full entries are written out and re-keyed all the time."""
+    monkeypatch.setenv("CT_SA_FLUSH", "3")
+    rng = np.random.default_rng(9)
+    g = Gen(rng, n_comms=7, dev_change=0.005)
+    g.n = [2, 3, 4, 5, 6, 7, 8]
+    g.devs = [g._perm(n) for n in g.n]
+    g.mixed(400_000, p_pair=0.02, p_copy=0.02)
+    _check(g.array(), n_comms=7)
+
+
 def test_repeated_ring_blocks_with_device_changes():
     """Long runs of identical ring allreduce / allgather / reduce-scatter instances (the
     register accumulator's case), with the devices and types changing between runs."""
