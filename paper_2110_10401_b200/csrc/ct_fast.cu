@@ -14,10 +14,10 @@ static_assert((kQ & (kQ - 1)) == 0 && kQ >= 64, "queue holds < 32 carried + 32 n
 
 // Shared-memory accumulator of repeated instances of one (comm slot, class): class 0 ring
 // allreduce (every block but the last full), 1 allgather, 2 reduce-scatter, 3 tree
-// allreduce.  Sums are 64-bit as two 32-bit limbs (native atomics) and are written to the
+// allreduce, 4 collnet allreduce.  Sums are 64-bit as two 32-bit limbs (native atomics) and are written to the
 // histogram before they can wrap (kSAFlush instances).
 struct __align__(16) SAE {
-  uint32_t key;               // 1 << 31 | slot | cls << 3 | coll << 5 | n << 8; 0: empty
+  uint32_t key;               // 1 << 31 | slot | cls << 3 | coll << 6 | n << 9; 0: empty
   uint32_t cnt;               // instances
   unsigned long long devs;    // device of rank j in byte j
   uint32_t g[2], d[2], s[2];  // edge sums (ring: gen / dlt; tree: ceil(S/2) / floor(S/2)), payload
@@ -252,7 +252,7 @@ __device__ __forceinline__ unsigned long long tree_peers(int n, int j);
 // ring classes -- the edge leaving position q carries g + d * ([q == n-2] + [q == n-3]);
 // tree -- T1-only peers g, peers in both trees g + d, T2-only peers d (cnt2 transfers).
 template <bool SH>
-__device__ __noinline__ uint32_t flush_acc(const FastParams& P, int g2, int coll, int n, bool tree,
+__device__ __noinline__ uint32_t flush_acc(const FastParams& P, int g2, int coll, int n, int mode,
                                            unsigned long long devs, unsigned long long g_lo, uint32_t g_hi,
                                            unsigned long long d_lo, uint32_t d_hi, unsigned long long s_lo,
                                            uint32_t s_hi, uint32_t cnt, uint32_t cnt2) {
@@ -268,9 +268,22 @@ __device__ __noinline__ uint32_t flush_acc(const FastParams& P, int g2, int coll
     if ((v >> 63) != 0) sk.flags |= note_overflow(key);  // the cell exceeds 2^63 - 1
     else sk.add(key, (unsigned long long)v, c);
   };
-  if (!tree) {
+  if (mode == 0) {
     const int a = n - 2, b = n >= 3 ? n - 3 : n - 1;
     for (int q = 0; q < n; q++) emit(q, q + 1 == n ? 0 : q + 1, 1u, (uint32_t)(q == a) + (uint32_t)(q == b), cnt);
+  } else if (mode == 2) {  // collnet: every rank sends S to NET and receives S from it
+    const unsigned long long v = g_lo;
+    for (int j = 0; j < n; j++) {
+      const int dv = (int)(__byte_perm(dlo, dhi, (uint32_t)j) & 0xFF) + 2;
+      const uint32_t k_up = (uint32_t)((coll * g2 + dv) * g2 + kNet), k_dn = (uint32_t)((coll * g2 + kNet) * g2 + dv);
+      if (g_hi != 0 || (v >> 63) != 0) {
+        sk.flags |= note_overflow(k_up);
+        sk.flags |= note_overflow(k_dn);
+      } else {
+        sk.add(k_up, v, cnt);
+        sk.add(k_dn, v, cnt);
+      }
+    }
   } else {
     for (int j = 0; j < n; j++) {
       const unsigned long long w = tree_peers(n, j);
@@ -292,7 +305,8 @@ template <bool SH>
 __device__ __noinline__ uint32_t sa_flush(const FastParams& P, SAE* E, uint32_t key, unsigned long long devs) {
   uint32_t f = 0;
   if (E->key && E->cnt)
-    f = flush_acc<SH>(P, P.g2, (int)(E->key >> 5 & 7u), (int)(E->key >> 8 & 0xFFu), (E->key >> 3 & 3u) == 3u, E->devs,
+    f = flush_acc<SH>(P, P.g2, (int)(E->key >> 6 & 7u), (int)(E->key >> 9 & 0xFFu),
+                      (E->key >> 3 & 7u) == 3u ? 1 : ((E->key >> 3 & 7u) == 4u ? 2 : 0), E->devs,
                       E->g[0] | ((unsigned long long)E->g[1] << 32), 0u, E->d[0] | ((unsigned long long)E->d[1] << 32),
                       0u, E->s[0] | ((unsigned long long)E->s[1] << 32), 0u, E->cnt, E->cnt2);
   if (key) { E->key = key; E->devs = devs; }
@@ -310,7 +324,7 @@ struct RingAcc {
 
   template <bool SH>
   __device__ __forceinline__ void flush(Sink<SH>& sk, int g2) {
-    sk.flags |= flush_acc<SH>(sk.P, g2, (int)(tag & 0xFF), (int)(tag >> 8), false, devs, g_lo, g_hi, d_lo, d_hi,
+    sk.flags |= flush_acc<SH>(sk.P, g2, (int)(tag & 0xFF), (int)(tag >> 8), 0, devs, g_lo, g_hi, d_lo, d_hi,
                               s_lo, s_hi, cnt, 0u);
   }
 
@@ -513,14 +527,14 @@ __device__ __forceinline__ void expand_block(const FastParams& P, Sink<SH>& sk, 
       if (ra.add(sk, g2, (uint32_t)coll | ((uint32_t)n << 8), devs, simple ? gen : fixed, simple ? dlt : 0ull, s))
         return;
     }
-    if (slot >= 0 && ((ring && (simple || scatter)) || tree)) {  // the warp's slot accumulator
-      const uint32_t cls = tree ? 3u : (coll == CT_COLL_ALLREDUCE ? 0u : (coll == CT_COLL_ALLGATHER ? 1u : 2u));
-      const uint32_t e = ((((uint32_t)slot & 3u) << 2) | cls) ^ (((uint32_t)slot >> 2) << 1);
-      const uint32_t key = 0x80000000u | (uint32_t)slot | (cls << 3) | ((uint32_t)coll << 5) | ((uint32_t)n << 8);
+    if (slot >= 0 && ((ring && (simple || scatter)) || !ring)) {  // the warp's slot accumulator
+      const uint32_t cls = tree ? 3u : (!ring ? 4u : (coll == CT_COLL_ALLREDUCE ? 0u : (coll == CT_COLL_ALLGATHER ? 1u : 2u)));
+      const uint32_t e = ((uint32_t)slot * 5u + cls) & (uint32_t)(kSE - 1);
+      const uint32_t key = 0x80000000u | (uint32_t)slot | (cls << 3) | ((uint32_t)coll << 6) | ((uint32_t)n << 9);
       SAE& E = sa[e];
       if (E.key == key && E.devs == devs) {
-        limb_add(E.g, tree ? s - s / 2 : (simple ? gen : fixed));
-        limb_add(E.d, tree ? s / 2 : (simple ? dlt : 0ull));
+        limb_add(E.g, tree ? s - s / 2 : (ring ? (simple ? gen : fixed) : s));
+        if (tree || simple) limb_add(E.d, tree ? s / 2 : dlt);
         limb_add(E.s, s);
         if (tree && s / 2 != 0) atomicAdd(&E.cnt2, 1u);
         if (atomicAdd(&E.cnt, 1u) + 1 == P.sa_flush) { sq.e = e; sq.key = 0; sq.act = true; }  // write out after the batch
@@ -601,21 +615,23 @@ __device__ __forceinline__ void count_diag(uint32_t st) {
   else if (st == ST_MISMATCH) atomicAdd(&cta_mem().diag[CT_DIAG_MISMATCHED_P2P], 1u);
 }
 
-// copy statistics: a one-entry register cache (copy kind, payload, calls)
+// copy statistics: one register accumulator per copy kind
 struct CopyStats {
-  uint32_t t;  // 3: empty
-  uint32_t cnt;
-  unsigned long long sum;
+  unsigned long long sum[3];
+  uint32_t cnt[3];
   __device__ __forceinline__ void add(uint32_t k, unsigned long long v) {
-    if (k != t || sum + v < v) {
-      if (t < 3) stat_limbs(CT_T_EXPLICIT + t, sum, 0, cnt);
-      t = k; sum = 0; cnt = 0;
-    }
-    sum += v;
-    cnt++;
+#pragma unroll
+    for (uint32_t t = 0; t < 3; t++)
+      if (k == t) {
+        if (sum[t] + v < v) { stat_limbs(CT_T_EXPLICIT + t, sum[t], 0, cnt[t]); sum[t] = 0; cnt[t] = 0; }
+        sum[t] += v;
+        cnt[t]++;
+      }
   }
   __device__ __forceinline__ void drain() {
-    if (t < 3) stat_limbs(CT_T_EXPLICIT + t, sum, 0, cnt);
+#pragma unroll
+    for (uint32_t t = 0; t < 3; t++)
+      if (cnt[t]) stat_limbs(CT_T_EXPLICIT + t, sum[t], 0, cnt[t]);
   }
 };
 
@@ -667,7 +683,7 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
   RingAcc racc;
   racc.tag = 0;
   racc.miss = 0;
-  CopyStats cps{3u, 0u, 0ull};
+  CopyStats cps{{0ull, 0ull, 0ull}, {0u, 0u, 0u}};
   int my_max_dev = -1;
   uint32_t copy_seen = 0;              // copy kinds this lane has seen (first index noted)
   uint32_t wflags = 0;
