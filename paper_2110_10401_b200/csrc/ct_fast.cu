@@ -61,7 +61,7 @@ static_assert(sizeof(WarpMem) * kWarps + sizeof(CtaMem) + kTypes * 18 * 18 * 12 
               "shared memory budget: CTA histogram no longer fits for d <= 16");
 
 #ifndef CT_SLACK
-#define CT_SLACK 1
+#define CT_SLACK 0
 #endif
 constexpr uint32_t kDrainSlack = CT_SLACK;  // chunks of read-ahead kept free for the TMA ring
 constexpr uint32_t kRM = kRing * 32 - 1;  // ring index mask (kRing is a power of two)
@@ -188,6 +188,7 @@ __device__ __forceinline__ void stat1(uint32_t t, unsigned long long v) {
 
 // Transfers are added straight into the CTA histogram; statistics of the collective
 // types and sendrecv (types 0..5) accumulate in registers until the end (or a wrap).
+// REGION sink
 template <bool SH>
 struct Sink {
   const FastParams& P;
@@ -246,6 +247,7 @@ struct Sink {
 // but the last full (gen = 2S - 2 chunk, dlt = chunk - last block), allgather /
 // reduce-scatter (gen = (n-1) * block, dlt = 0).  Instances with the same (type, n,
 // devices) add into 128-bit sums; the n cells are written when the key changes.
+// REGION accumulators
 __device__ __forceinline__ unsigned long long tree_peers(int n, int j);
 
 // Write accumulated instances of one (type, n, devices) key into the histogram:
@@ -389,6 +391,7 @@ __device__ __noinline__ bool devices_distinct(const ct_record* R, uint32_t p, ui
 // p2p order: per (comm, src, dst) channel, send seqs and recv seqs non-decreasing in file
 // order (then FIFO-by-position pairing equals the reference's seq-sorted pairing).  Lanes
 // hold send/recv pairs in file order (lane = element).
+// REGION p2p
 __device__ __noinline__ uint32_t p2p_order(P2PEntry* chan, const Rec ra, uint64_t next_seq, bool sendA, int lane) {
   uint32_t wflags = 0;
   const unsigned lt = (1u << lane) - 1;
@@ -431,6 +434,7 @@ __device__ __noinline__ uint32_t p2p_order(P2PEntry* chan, const Rec ra, uint64_
   return wflags;
 }
 
+// REGION tree
 // Peers of position j in the double binary tree (trees.py:57-106, decompose.py:227-255)
 // packed as 7-bit codes (rank in bits [0,5), bit 5 = T1 edge carrying ceil(S/2), bit 6 =
 // T2 edge carrying floor(S/2); an edge in both trees is one transfer of S), the count in
@@ -463,6 +467,7 @@ __device__ __forceinline__ unsigned long long tree_peers(int n, int j) {
   return n <= kTreeLut ? cta_mem().tree_lut[n][j] : tree_pack_big(n, j);
 }
 
+// REGION expand_block
 // a lane's follow-up on the warp's slot accumulator after a batch: entry e is full
 // (key 0) or held another key (re-key to ``key``)
 struct SAReq {
@@ -615,6 +620,7 @@ __device__ __forceinline__ void count_diag(uint32_t st) {
   else if (st == ST_MISMATCH) atomicAdd(&cta_mem().diag[CT_DIAG_MISMATCHED_P2P], 1u);
 }
 
+// REGION copystats
 // copy statistics: one register accumulator per copy kind
 struct CopyStats {
   unsigned long long sum[3];
@@ -644,6 +650,7 @@ size_t fast_smem_bytes(int g2, int smem_hist) {
 }
 
 template <bool SH>
+// REGION kernel_init
 __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   WarpMem* WM = reinterpret_cast<WarpMem*>(smem_raw);
@@ -727,6 +734,7 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
         const uint32_t rel = q * 32 + lane;
         if (rel < eo) my_max_dev = max(my_max_dev, (int)(R[rel & kRM].dev ^ R[rel & kRM].rank));
       } else {
+        // REGION scan
         // ================= scan (lane = record)
         {
           const uint32_t rel = q * 32 + lane;
@@ -775,6 +783,7 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
         }
         __syncwarp();
 
+        // REGION join_setup
         // ================= join + expand (lane = element), in batches of <= 32
         // elements wholly inside chunks <= q are joinable; join when 32 are ready or when
         // the ring is about to be full of unjoined records (the oldest one's chunk u)
@@ -829,6 +838,7 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
             cover += (int)len;
           }
 
+          // REGION validate
           // ---- validation (lane walks its element)
           uint32_t st = ST_NONE;
           bool fastdev = false, packed = false;  // all devices < gcap / held in ``devs``
@@ -892,6 +902,7 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
           if (__any_sync(kFull, isS)) wflags |= p2p_order(P.chans + (size_t)gw * kPC, h, rseq, isS, lane);
           if (st > ST_VALID) count_diag(st);
 
+          // REGION tables
           // ---- tables: the last block of each comm in the batch; first occurrences
           __syncwarp();  // every lane has read the tables
           if (isC) {
@@ -920,6 +931,7 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
           }
           __syncwarp();
 
+          // REGION expand_call
           // ---- expansion + accumulation of valid elements
           SAReq sq{0u, 0u, false};
           if (st == ST_VALID && !no_expand) {
@@ -944,6 +956,7 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
         if (bail) break;
       }
 
+      // REGION release
       // ---- release chunks no element still needs; their slots refill
       const uint32_t keep = qt != qh ? u : q + 1;
       if (keep > freed) {
@@ -969,6 +982,7 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
       mbar_wait(&W.bar[q % kRing], (q / kRing) & 1);
   }
 
+  // REGION epilogue
   // ---- per-warp summaries for the cross-range check and first-occurrence keys
   __syncwarp();
   if (lane < kCS) {
@@ -1028,6 +1042,7 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
   }
 }
 
+// REGION range_check
 template __global__ void fast_kernel<true>(FastParams);
 template __global__ void fast_kernel<false>(FastParams);
 
