@@ -14,23 +14,25 @@ static_assert((kQ & (kQ - 1)) == 0 && kQ >= 64, "queue holds < 32 carried + 32 n
 
 // Shared-memory accumulator of repeated instances of one (comm slot, class): class 0 ring
 // allreduce (every block but the last full), 1 allgather, 2 reduce-scatter, 3 tree
-// allreduce, 4 collnet allreduce.  Sums are 64-bit as two 32-bit limbs (native atomics) and are written to the
+// allreduce, 4 collnet allreduce, 5 broadcast, 6 reduce (keyed with the root).  Sums are 64-bit as two 32-bit limbs (native atomics) and are written to the
 // histogram before they can wrap (kSAFlush instances).
 struct __align__(16) SAE {
-  uint32_t key;               // 1 << 31 | slot | cls << 3 | coll << 6 | n << 9; 0: empty
+  uint32_t key;               // 1 << 31 | slot | cls << 3 | coll << 6 | n << 9 | root << 13; 0: empty
   uint32_t cnt;               // instances
   unsigned long long devs;    // device of rank j in byte j
   uint32_t g[2], d[2], s[2];  // edge sums (ring: gen / dlt; tree: ceil(S/2) / floor(S/2)), payload
   uint32_t cnt2;              // tree: instances with floor(S/2) != 0
   uint32_t pad;
 };
-constexpr int kSE = 16;             // slot accumulators per warp
+constexpr int kSE = 32;             // slot accumulators per warp
+constexpr int kCP = 64;             // pooled per-rank seq entries per warp (all comm slots)
 constexpr uint32_t kSAFlush = 1u << 14;  // default write-out threshold (FastParams::sa_flush)
 
 struct __align__(16) WarpMem {
   ct_record ring[kRing][32];                 // TMA ring: chunk k lives in slot k % kRing
   SAE sa[kSE];
-  unsigned long long cseq[kCS][kMaxN];       // last collective block of the comm: seq per rank
+  unsigned long long cpool[kCP];             // last collective block of each comm: seq per rank,
+  uint32_t cbase[kCS];                       //   slot s at cpool[cbase[s] ...] (n entries)
   unsigned long long bar[kRing];
   unsigned long long cfirst[kCS], clast[kCS];
   unsigned long long tfirst[kCS][5];
@@ -254,7 +256,7 @@ __device__ __forceinline__ unsigned long long tree_peers(int n, int j);
 // ring classes -- the edge leaving position q carries g + d * ([q == n-2] + [q == n-3]);
 // tree -- T1-only peers g, peers in both trees g + d, T2-only peers d (cnt2 transfers).
 template <bool SH>
-__device__ __noinline__ uint32_t flush_acc(const FastParams& P, int g2, int coll, int n, int mode,
+__device__ __noinline__ uint32_t flush_acc(const FastParams& P, int g2, int coll, int n, int mode, int root,
                                            unsigned long long devs, unsigned long long g_lo, uint32_t g_hi,
                                            unsigned long long d_lo, uint32_t d_hi, unsigned long long s_lo,
                                            uint32_t s_hi, uint32_t cnt, uint32_t cnt2) {
@@ -270,7 +272,11 @@ __device__ __noinline__ uint32_t flush_acc(const FastParams& P, int g2, int coll
     if ((v >> 63) != 0) sk.flags |= note_overflow(key);  // the cell exceeds 2^63 - 1
     else sk.add(key, (unsigned long long)v, c);
   };
-  if (mode == 0) {
+  if (mode == 3) {  // broadcast / reduce pipeline: every position but one sends S (decompose.py:192-224)
+    const int skip = coll == CT_COLL_BROADCAST ? (root == 0 ? n - 1 : root - 1) : root;
+    for (int q = 0; q < n; q++)
+      if (q != skip) emit(q, q + 1 == n ? 0 : q + 1, 1u, 0u, cnt);
+  } else if (mode == 0) {
     const int a = n - 2, b = n >= 3 ? n - 3 : n - 1;
     for (int q = 0; q < n; q++) emit(q, q + 1 == n ? 0 : q + 1, 1u, (uint32_t)(q == a) + (uint32_t)(q == b), cnt);
   } else if (mode == 2) {  // collnet: every rank sends S to NET and receives S from it
@@ -307,10 +313,13 @@ template <bool SH>
 __device__ __noinline__ uint32_t sa_flush(const FastParams& P, SAE* E, uint32_t key, unsigned long long devs) {
   uint32_t f = 0;
   if (E->key && E->cnt)
-    f = flush_acc<SH>(P, P.g2, (int)(E->key >> 6 & 7u), (int)(E->key >> 9 & 0xFFu),
-                      (E->key >> 3 & 7u) == 3u ? 1 : ((E->key >> 3 & 7u) == 4u ? 2 : 0), E->devs,
+  {
+    const uint32_t cls = E->key >> 3 & 7u;
+    f = flush_acc<SH>(P, P.g2, (int)(E->key >> 6 & 7u), (int)(E->key >> 9 & 15u),
+                      cls == 3u ? 1 : (cls == 4u ? 2 : (cls >= 5u ? 3 : 0)), (int)(E->key >> 13 & 7u), E->devs,
                       E->g[0] | ((unsigned long long)E->g[1] << 32), 0u, E->d[0] | ((unsigned long long)E->d[1] << 32),
                       0u, E->s[0] | ((unsigned long long)E->s[1] << 32), 0u, E->cnt, E->cnt2);
+  }
   if (key) { E->key = key; E->devs = devs; }
   E->g[0] = E->g[1] = E->d[0] = E->d[1] = E->s[0] = E->s[1] = 0;
   E->cnt = E->cnt2 = 0;
@@ -326,7 +335,7 @@ struct RingAcc {
 
   template <bool SH>
   __device__ __forceinline__ void flush(Sink<SH>& sk, int g2) {
-    sk.flags |= flush_acc<SH>(sk.P, g2, (int)(tag & 0xFF), (int)(tag >> 8), 0, devs, g_lo, g_hi, d_lo, d_hi,
+    sk.flags |= flush_acc<SH>(sk.P, g2, (int)(tag & 0xFF), (int)(tag >> 8), 0, 0, devs, g_lo, g_hi, d_lo, d_hi,
                               s_lo, s_hi, cnt, 0u);
   }
 
@@ -532,13 +541,17 @@ __device__ __forceinline__ void expand_block(const FastParams& P, Sink<SH>& sk, 
       if (ra.add(sk, g2, (uint32_t)coll | ((uint32_t)n << 8), devs, simple ? gen : fixed, simple ? dlt : 0ull, s))
         return;
     }
-    if (slot >= 0 && ((ring && (simple || scatter)) || !ring)) {  // the warp's slot accumulator
-      const uint32_t cls = tree ? 3u : (!ring ? 4u : (coll == CT_COLL_ALLREDUCE ? 0u : (coll == CT_COLL_ALLGATHER ? 1u : 2u)));
-      const uint32_t e = ((uint32_t)slot * 5u + cls) & (uint32_t)(kSE - 1);
-      const uint32_t key = 0x80000000u | (uint32_t)slot | (cls << 3) | ((uint32_t)coll << 6) | ((uint32_t)n << 9);
+    const bool rooted = coll == CT_COLL_BROADCAST || coll == CT_COLL_REDUCE;
+    if (slot >= 0 && (!ring || simple || scatter || (rooted && h.has_root()))) {  // the warp's slot accumulator
+      const uint32_t cls = tree ? 3u : (!ring ? 4u : (coll == CT_COLL_ALLREDUCE ? 0u : (coll == CT_COLL_ALLGATHER ? 1u
+                           : (coll == CT_COLL_REDUCESCATTER ? 2u : (coll == CT_COLL_BROADCAST ? 5u : 6u)))));
+      const uint32_t root = rooted ? h.aux & 7u : 0u;
+      const uint32_t e = ((cls < 5u ? cls : (cls == 5u ? 8u : 16u) + root) + (uint32_t)slot * 5u) & (uint32_t)(kSE - 1);
+      const uint32_t key =
+          0x80000000u | (uint32_t)slot | (cls << 3) | ((uint32_t)coll << 6) | ((uint32_t)n << 9) | (root << 13);
       SAE& E = sa[e];
       if (E.key == key && E.devs == devs) {
-        limb_add(E.g, tree ? s - s / 2 : (ring ? (simple ? gen : fixed) : s));
+        limb_add(E.g, tree ? s - s / 2 : (ring && !rooted ? (simple ? gen : fixed) : s));
         if (tree || simple) limb_add(E.d, tree ? s / 2 : dlt);
         limb_add(E.s, s);
         if (tree && s / 2 != 0) atomicAdd(&E.cnt2, 1u);
@@ -725,6 +738,7 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
     int cover = 0;                  // element lengths + copies (must equal the range's records)
     uint32_t cross = 0;             // 1: the last queued element extends past the scanned chunks
     uint32_t u = 0;                 // chunk of the oldest queued element (when the queue is not empty)
+    uint32_t cnext = 0;             // next free entry of the seq-table pool
     const bool stream_only = (P.dbg & 4) != 0, no_expand = (P.dbg & 1) != 0;
     bool bail = false;
     for (uint32_t q = 0; q < lastc && !bail; q++) {
@@ -831,6 +845,18 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
           const bool hist = pl < 0 && tsn != 0;
           const uint32_t n = h.nranks;
           if (isC && (pl >= 0 ? pn != n : (tsn != 0 && tsn != n))) bad = true;  // grouping.py:104-108
+          // a comm's first block in this range: its seq table gets n pooled entries
+          for (unsigned need = __ballot_sync(kFull, isC && pl < 0 && tsn == 0 && n >= 1 && n <= (uint32_t)kMaxN);
+               need; need &= need - 1) {
+            const int L = __ffs(need) - 1;
+            const uint32_t nL = __shfl_sync(kFull, n, L);
+            const int sL = __shfl_sync(kFull, hs, L);
+            if (lane == 0) W.cbase[sL] = cnext;
+            cnext += nL;
+          }
+          if (cnext > (uint32_t)kCP) bad = true;  // more ranks in one range than the pool holds
+          __syncwarp();
+          const uint32_t cb = W.cbase[hs];
           {  // the element lies inside the range; lengths tile it (with the copies)
             const uint32_t len = isC ? n : (isS ? 2u : 0u);
             if (isC && (n == 0 || n > (uint32_t)kMaxN)) bad = true;
@@ -866,7 +892,8 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
               const unsigned long long seq = ((unsigned long long)wa.w << 32) | wa.z;
               // previous block of the comm: this batch (ring) or the slot table (always a valid
               // address; ignored without history)
-              const uint64_t* ps = pl >= 0 ? &R[(ppos + j) & kRM].seq : reinterpret_cast<const uint64_t*>(&W.cseq[hs][j]);
+              const uint64_t* ps =
+                  pl >= 0 ? &R[(ppos + j) & kRM].seq : reinterpret_cast<const uint64_t*>(&W.cpool[(cb + j) & (kCP - 1)]);
               const unsigned long long pv = *ps;
               ord |= have & (pv >= seq);
               const uint32_t dv = wb.z & 0xFFFF;
@@ -919,7 +946,7 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
             const int L = __ffs(lb) - 1;
             const uint32_t pL = __shfl_sync(kFull, p, L), nL = __shfl_sync(kFull, n, L);
             const int sL = __shfl_sync(kFull, hs, L);
-            if ((uint32_t)lane < nL) W.cseq[sL][lane] = R[(pL + lane) & kRM].seq;
+            if ((uint32_t)lane < nL) W.cpool[(W.cbase[sL] + lane) & (kCP - 1)] = R[(pL + lane) & kRM].seq;
           }
           if (tf_pend) {  // first valid instance per (comm slot, type): only until recorded once
             const unsigned long long bit = (isC && st == ST_VALID) ? 1ull << (hs * 5 + h.coll()) : 0ull;
