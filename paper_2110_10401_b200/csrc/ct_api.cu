@@ -252,6 +252,20 @@ int summarize_state(ct_context* c, const GlobalState& gs, int gcap, int64_t d, i
   std::vector<unsigned long long> h(2 * ncell);
   CTX_TRY(c, cudaMemcpyAsync(h.data(), c->cells, 2 * ncell * 8, cudaMemcpyDeviceToHost, st));
   CTX_TRY(c, cudaStreamSynchronize(st));
+  // copy statistics: every copy adds exactly one transfer of its byte count to its type
+  // (decompose.py:397-406), so calls / payload are the plane's frequency / byte sums
+  // (the fast kernel does not count them separately)
+  for (int t = CT_T_EXPLICIT; t < kTypes; t++) {
+    unsigned __int128 pay = 0;
+    uint64_t calls = 0;
+    for (size_t k = (size_t)t * g2 * g2; k < (size_t)(t + 1) * g2 * g2; k++) {
+      pay += h[k];
+      calls += h[ncell + k];
+    }
+    out->calls[t] = calls;
+    out->payload_lo[t] = (uint64_t)pay;
+    out->payload_hi[t] = (uint64_t)(pay >> 64);
+  }
   bool overflow = (gs.flags & F_OVERFLOW) != 0;
   uint64_t of_cell = ~0ull;
   int net_used = 0;

@@ -15,7 +15,7 @@ static_assert((kQ & (kQ - 1)) == 0 && kQ >= 64, "queue holds < 32 carried + 32 n
 // Shared-memory accumulator of repeated instances of one (comm slot, class): class 0 ring
 // allreduce (every block but the last full), 1 allgather, 2 reduce-scatter, 3 tree
 // allreduce, 4 collnet allreduce, 5 broadcast, 6 reduce (keyed with the root).  Sums are 64-bit as two 32-bit limbs (native atomics) and are written to the
-// histogram before they can wrap (kSAFlush instances).
+// histogram before they can wrap (FastParams::sa_flush instances, <= 2^14).
 struct __align__(16) SAE {
   uint32_t key;               // 1 << 31 | slot | cls << 3 | coll << 6 | n << 9 | root << 13; 0: empty
   uint32_t cnt;               // instances
@@ -26,7 +26,6 @@ struct __align__(16) SAE {
 };
 constexpr int kSE = 32;             // slot accumulators per warp
 constexpr int kCP = 64;             // pooled per-rank seq entries per warp (all comm slots)
-constexpr uint32_t kSAFlush = 1u << 14;  // default write-out threshold (FastParams::sa_flush)
 
 struct __align__(16) WarpMem {
   ct_record ring[kRing][32];                 // TMA ring: chunk k lives in slot k % kRing
@@ -491,87 +490,40 @@ __device__ __forceinline__ void limb_add(uint32_t* L, unsigned long long v) {  /
   if (h) atomicAdd(L + 1, h);
 }
 
-// Expansion + statistics of one VALID collective instance whose head (rank 0) sits at
-// ring position p; gidx is its global record index.  Rank-attributed rules (ct_common.cuh,
-// SURVEY App. A): ring family -- the record at ring position q (rank order[q]) sends to
-// order[q+1]; tree -- every rank sends to its peers in both trees; collnet -- every rank
-// sends S to NET and receives S from it.  All edges leave through one emission site.
-// Ring lanes start at different positions (j0) so their shared-memory reads spread over
-// the banks.
+// Edge-by-edge expansion of one VALID instance (the accumulators did not take it):
+// statistics, then every transfer through one emission site.  Out of line to keep the
+// accumulator fast path compact in the instruction cache.
 template <bool SH>
-__device__ __forceinline__ void expand_block(const FastParams& P, Sink<SH>& sk, const ct_record* R, const Rec& h,
-                                             uint32_t p, uint64_t gidx, uint32_t j0, bool fastdev, bool packed,
-                                             unsigned long long devs, RingAcc& ra, int slot, SAE* sa, SAReq& sq) {
+__device__ __noinline__ uint32_t expand_direct(const FastParams& P, const ct_record* R, const Rec h, uint32_t p,
+                                               uint64_t gidx, uint32_t j0, bool fastdev, bool packed,
+                                               unsigned long long devs, int algo) {
+  Sink<SH> sk(P);
   const int n = (int)h.nranks, coll = h.coll();
   const unsigned long long base = min((unsigned long long)gidx, (1ull << 41) - 1) << 21;
-  if ((h.count >> 40) != 0) {
-    for (int j = 0; j < n; j++) {
-      Rec rc = h;
-      rc.rank = (uint32_t)j;
-      rc.dev = R[(p + j) & kRM].dev;
-      sk.flags |= expand_wide<SH>(P, R, rc, p, base | ((unsigned long long)j << 11));
-    }
-    return;
-  }
   const uint64_t blk = h.count * (uint64_t)dtype_width(h.dtype());
   const bool scatter = coll == CT_COLL_ALLGATHER || coll == CT_COLL_REDUCESCATTER;
   const uint64_t s = scatter ? blk * (uint64_t)n : blk;
-  int algo = h.algo();
-  if (coll == CT_COLL_ALLREDUCE) {
-    if (algo == CT_ALGO_AUTO) algo = s < P.ex.tree_threshold ? CT_ALGO_TREE : CT_ALGO_RING;
-  } else {
-    if (algo == CT_ALGO_TREE || algo == CT_ALGO_COLLNET) { sk.flags |= F_WRONG_ALGO; return; }
-    algo = CT_ALGO_RING;
-  }
   const int g2 = P.g2;
   const bool ring = algo == CT_ALGO_RING, tree = algo == CT_ALGO_TREE;
-  // ring family
   const bool rmap = ring && n == P.ex.ring_len;
   const int root_pos = rmap ? (h.has_root() ? (int)P.ex.ring_inv[h.aux] : 0) : (int)h.aux;
   const int skip_pos = coll == CT_COLL_BROADCAST ? (root_pos == 0 ? n - 1 : root_pos - 1)
                                                  : (coll == CT_COLL_REDUCE ? root_pos : -1);
   const uint64_t chunk = ring && coll == CT_COLL_ALLREDUCE ? ceil_div(s, (uint32_t)n) : 0;
-  // allreduce blocks b[i] (decompose.py:104-107): chunk for i < n-1 and the remainder
-  // s - (n-1)*chunk for i = n-1 unless s is tiny (then trailing blocks are empty)
   const bool simple = ring && coll == CT_COLL_ALLREDUCE && (uint64_t)(n - 1) * chunk < s;
   const uint64_t gen = 2 * s - 2 * chunk, dlt = chunk - (s - (uint64_t)(n - 1) * chunk);
   const uint64_t fixed = scatter ? s - blk : s;
-  if (fastdev && packed && !rmap && n >= 2 && s != 0) {
-    if (ring && (simple || scatter)) {  // per-lane register accumulator
-      if (ra.add(sk, g2, (uint32_t)coll | ((uint32_t)n << 8), devs, simple ? gen : fixed, simple ? dlt : 0ull, s))
-        return;
-    }
-    const bool rooted = coll == CT_COLL_BROADCAST || coll == CT_COLL_REDUCE;
-    if (slot >= 0 && (!ring || simple || scatter || (rooted && h.has_root()))) {  // the warp's slot accumulator
-      const uint32_t cls = tree ? 3u : (!ring ? 4u : (coll == CT_COLL_ALLREDUCE ? 0u : (coll == CT_COLL_ALLGATHER ? 1u
-                           : (coll == CT_COLL_REDUCESCATTER ? 2u : (coll == CT_COLL_BROADCAST ? 5u : 6u)))));
-      const uint32_t root = rooted ? h.aux & 7u : 0u;
-      const uint32_t e = ((cls < 5u ? cls : (cls == 5u ? 8u : 16u) + root) + (uint32_t)slot * 5u) & (uint32_t)(kSE - 1);
-      const uint32_t key =
-          0x80000000u | (uint32_t)slot | (cls << 3) | ((uint32_t)coll << 6) | ((uint32_t)n << 9) | (root << 13);
-      SAE& E = sa[e];
-      if (E.key == key && E.devs == devs) {
-        limb_add(E.g, tree ? s - s / 2 : (ring && !rooted ? (simple ? gen : fixed) : s));
-        if (tree || simple) limb_add(E.d, tree ? s / 2 : dlt);
-        limb_add(E.s, s);
-        if (tree && s / 2 != 0) atomicAdd(&E.cnt2, 1u);
-        if (atomicAdd(&E.cnt, 1u) + 1 == P.sa_flush) { sq.e = e; sq.key = 0; sq.act = true; }  // write out after the batch
-        return;
-      }
-      sq.e = e; sq.key = key; sq.act = true;  // re-key after the batch; this instance is expanded now
-    }
-  }
   sk.stat(coll, (unsigned __int128)s);
   if (algo == CT_ALGO_COLLNET) {
-    if (s == 0) return;
+    if (s == 0) return sk.flags;
   } else {
     if ((coll == CT_COLL_BROADCAST || coll == CT_COLL_REDUCE) && !h.has_root()) {
       sk.flags |= F_MISSING_ROOT;
-      return;
+      return sk.flags;
     }
-    if (n == 1 || s == 0) return;
+    if (n == 1 || s == 0) return sk.flags;
   }
-  if (rmap && !P.ex.ring_valid) { sk.flags |= F_BAD_RING; return; }
+  if (rmap && !P.ex.ring_valid) { sk.flags |= F_BAD_RING; return sk.flags; }
   // tree shares
   const uint64_t share1 = s - s / 2, share2 = s / 2;
   const uint32_t dlo = (uint32_t)devs, dhi = (uint32_t)(devs >> 32);
@@ -625,6 +577,77 @@ __device__ __forceinline__ void expand_block(const FastParams& P, Sink<SH>& sk, 
     }
     q = qn;
   }
+  return sk.flags;
+}
+
+// Expansion + statistics of one VALID collective instance whose head (rank 0) sits at
+// ring position p; gidx is its global record index.  Rank-attributed rules (ct_common.cuh,
+// SURVEY App. A): ring family -- the record at ring position q (rank order[q]) sends to
+// order[q+1]; tree -- every rank sends to its peers in both trees; collnet -- every rank
+// sends S to NET and receives S from it.  All edges leave through one emission site.
+// Ring lanes start at different positions (j0) so their shared-memory reads spread over
+// the banks.
+template <bool SH>
+__device__ __forceinline__ void expand_block(const FastParams& P, Sink<SH>& sk, const ct_record* R, const Rec& h,
+                                             uint32_t p, uint64_t gidx, uint32_t j0, bool fastdev, bool packed,
+                                             unsigned long long devs, RingAcc& ra, int slot, SAE* sa, SAReq& sq) {
+  const int n = (int)h.nranks, coll = h.coll();
+  const unsigned long long base = min((unsigned long long)gidx, (1ull << 41) - 1) << 21;
+  if ((h.count >> 40) != 0) {
+    for (int j = 0; j < n; j++) {
+      Rec rc = h;
+      rc.rank = (uint32_t)j;
+      rc.dev = R[(p + j) & kRM].dev;
+      sk.flags |= expand_wide<SH>(P, R, rc, p, base | ((unsigned long long)j << 11));
+    }
+    return;
+  }
+  const uint64_t blk = h.count * (uint64_t)dtype_width(h.dtype());
+  const bool scatter = coll == CT_COLL_ALLGATHER || coll == CT_COLL_REDUCESCATTER;
+  const uint64_t s = scatter ? blk * (uint64_t)n : blk;
+  int algo = h.algo();
+  if (coll == CT_COLL_ALLREDUCE) {
+    if (algo == CT_ALGO_AUTO) algo = s < P.ex.tree_threshold ? CT_ALGO_TREE : CT_ALGO_RING;
+  } else {
+    if (algo == CT_ALGO_TREE || algo == CT_ALGO_COLLNET) { sk.flags |= F_WRONG_ALGO; return; }
+    algo = CT_ALGO_RING;
+  }
+  const int g2 = P.g2;
+  const bool ring = algo == CT_ALGO_RING, tree = algo == CT_ALGO_TREE;
+  // ring family
+  const bool rmap = ring && n == P.ex.ring_len;
+  const uint64_t chunk = ring && coll == CT_COLL_ALLREDUCE ? ceil_div(s, (uint32_t)n) : 0;
+  // allreduce blocks b[i] (decompose.py:104-107): chunk for i < n-1 and the remainder
+  // s - (n-1)*chunk for i = n-1 unless s is tiny (then trailing blocks are empty)
+  const bool simple = ring && coll == CT_COLL_ALLREDUCE && (uint64_t)(n - 1) * chunk < s;
+  const uint64_t gen = 2 * s - 2 * chunk, dlt = chunk - (s - (uint64_t)(n - 1) * chunk);
+  const uint64_t fixed = scatter ? s - blk : s;
+  if (fastdev && packed && !rmap && n >= 2 && s != 0) {
+    if (ring && (simple || scatter)) {  // per-lane register accumulator
+      if (ra.add(sk, g2, (uint32_t)coll | ((uint32_t)n << 8), devs, simple ? gen : fixed, simple ? dlt : 0ull, s))
+        return;
+    }
+    const bool rooted = coll == CT_COLL_BROADCAST || coll == CT_COLL_REDUCE;
+    if (slot >= 0 && (!ring || simple || scatter || (rooted && h.has_root()))) {  // the warp's slot accumulator
+      const uint32_t cls = tree ? 3u : (!ring ? 4u : (coll == CT_COLL_ALLREDUCE ? 0u : (coll == CT_COLL_ALLGATHER ? 1u
+                           : (coll == CT_COLL_REDUCESCATTER ? 2u : (coll == CT_COLL_BROADCAST ? 5u : 6u)))));
+      const uint32_t root = rooted ? h.aux & 7u : 0u;
+      const uint32_t e = ((cls < 5u ? cls : (cls == 5u ? 8u : 16u) + root) + (uint32_t)slot * 5u) & (uint32_t)(kSE - 1);
+      const uint32_t key =
+          0x80000000u | (uint32_t)slot | (cls << 3) | ((uint32_t)coll << 6) | ((uint32_t)n << 9) | (root << 13);
+      SAE& E = sa[e];
+      if (E.key == key && E.devs == devs) {
+        limb_add(E.g, tree ? s - s / 2 : (ring && !rooted ? (simple ? gen : fixed) : s));
+        if (tree || simple) limb_add(E.d, tree ? s / 2 : dlt);
+        limb_add(E.s, s);
+        if (tree && s / 2 != 0) atomicAdd(&E.cnt2, 1u);
+        if (atomicAdd(&E.cnt, 1u) + 1 == P.sa_flush) { sq.e = e; sq.key = 0; sq.act = true; }  // write out after the batch
+        return;
+      }
+      sq.e = e; sq.key = key; sq.act = true;  // re-key after the batch; this instance is expanded now
+    }
+  }
+  sk.flags |= expand_direct<SH>(P, R, h, p, gidx, j0, fastdev, packed, devs, algo);
 }
 
 __device__ __forceinline__ void count_diag(uint32_t st) {
@@ -632,27 +655,6 @@ __device__ __forceinline__ void count_diag(uint32_t st) {
   else if (st == ST_DUPDEV) atomicAdd(&cta_mem().diag[CT_DIAG_DUPLICATE_DEVICE], 1u);
   else if (st == ST_MISMATCH) atomicAdd(&cta_mem().diag[CT_DIAG_MISMATCHED_P2P], 1u);
 }
-
-// REGION copystats
-// copy statistics: one register accumulator per copy kind
-struct CopyStats {
-  unsigned long long sum[3];
-  uint32_t cnt[3];
-  __device__ __forceinline__ void add(uint32_t k, unsigned long long v) {
-#pragma unroll
-    for (uint32_t t = 0; t < 3; t++)
-      if (k == t) {
-        if (sum[t] + v < v) { stat_limbs(CT_T_EXPLICIT + t, sum[t], 0, cnt[t]); sum[t] = 0; cnt[t] = 0; }
-        sum[t] += v;
-        cnt[t]++;
-      }
-  }
-  __device__ __forceinline__ void drain() {
-#pragma unroll
-    for (uint32_t t = 0; t < 3; t++)
-      if (cnt[t]) stat_limbs(CT_T_EXPLICIT + t, sum[t], 0, cnt[t]);
-  }
-};
 
 }  // namespace
 
@@ -703,7 +705,6 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
   RingAcc racc;
   racc.tag = 0;
   racc.miss = 0;
-  CopyStats cps{{0ull, 0ull, 0ull}, {0u, 0u, 0u}};
   int my_max_dev = -1;
   uint32_t copy_seen = 0;              // copy kinds this lane has seen (first index noted)
   uint32_t wflags = 0;
@@ -775,8 +776,7 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
             const uint32_t aux = b.z >> 16, aux2 = b.w & 0xFFFF;
             if (ck != CT_CKIND_H2D) my_max_dev = max(my_max_dev, (int)aux);
             if (ck != CT_CKIND_D2H) my_max_dev = max(my_max_dev, (int)aux2);
-            const int t = kind - CT_KIND_MEMCPY;
-            cps.add((uint32_t)t, cnt);
+            const int t = kind - CT_KIND_MEMCPY;  // statistics: the host sums the type's cells
             if (!no_expand) {
               const int src = ck == CT_CKIND_H2D ? -1 : (int)aux, dst = ck == CT_CKIND_D2H ? -1 : (int)aux2;
               if (src < P.gcap && dst < P.gcap && (cnt >> 63) == 0) {
@@ -1029,7 +1029,6 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
   // ---- CTA epilogue: drain caches, one global merge
   if (racc.tag) racc.flush(sk, P.g2);
   if (lane < kSE && W.sa[lane].key && W.sa[lane].cnt) sk.flags |= sa_flush<SH>(P, &W.sa[lane], 0u, 0ull);
-  cps.drain();
   atomicMax(&C.max_dev, my_max_dev);
   if (sk.flags | wflags) atomicOr(&C.flags, sk.flags | wflags);
   __syncthreads();
