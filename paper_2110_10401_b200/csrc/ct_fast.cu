@@ -2,6 +2,9 @@
 // (design notes in ct_fast.cuh).
 #include "ct_fast.cuh"
 
+#define CT_LIKELY(x) __builtin_expect(!!(x), 1)
+#define CT_UNLIKELY(x) __builtin_expect(!!(x), 0)
+
 namespace ct {
 
 namespace {
@@ -38,6 +41,8 @@ struct __align__(16) WarpMem {
   uint32_t q[kQ];                            // element queue: ring-relative head positions
   uint32_t tag[kCS];                         // comm id of the slot
   uint32_t sn[kCS];                          // collective nranks of the slot (0: none yet)
+  uint32_t uni[kCS];                         // 1: the slot's last block had one seq on every rank,
+  unsigned long long useq[kCS];              //    useq (then cpool is not kept up to date)
 };
 
 constexpr int kTreeLut = 16;
@@ -209,7 +214,7 @@ struct Sink {
       const uint32_t vlo = (uint32_t)v, vhi = (uint32_t)(v >> 32);  // v < 2^63
       const uint32_t old = atomicAdd(lo + key, vlo);
       const uint32_t inc = vhi + (old + vlo < old ? 1u : 0u);
-      if (inc) {
+      if (CT_UNLIKELY(inc)) {
         const uint32_t oh = atomicAdd(lo + nc + key, inc);
         if (oh + inc < oh) flags |= note_overflow(key);  // the 64-bit cell wrapped
       }
@@ -225,7 +230,7 @@ struct Sink {
   // decomposition (destination rank of a collective edge, transfers are sorted by rank
   // pair, decompose.py:92; 0/1 for collnet) for the EndpointOutOfRange message.
   __device__ __forceinline__ void edge(int type, int src, int dst, unsigned __int128 bytes, int sub = 0) {
-    if (src >= P.gcap || dst >= P.gcap) {
+    if (CT_UNLIKELY(src >= P.gcap || dst >= P.gcap)) {
       flags |= oor(rec_key, sub, src >= P.gcap, P.explicit_d);
       return;
     }
@@ -344,7 +349,7 @@ struct RingAcc {
   __device__ __forceinline__ bool add(Sink<SH>& sk, int g2, uint32_t t, unsigned long long dv, unsigned long long g,
                                       unsigned long long d, unsigned long long sz) {
     if (t != tag || dv != devs) {
-      if (tag && ++miss < 8) return false;
+      if (CT_LIKELY(tag && ++miss < 8)) return false;
       if (tag) flush(sk, g2);
       tag = t; devs = dv;
       g_lo = d_lo = s_lo = 0; g_hi = d_hi = s_hi = cnt = 0;
@@ -384,6 +389,19 @@ __device__ __forceinline__ int find_slot(const WarpMem& W, uint32_t comm) {
   for (int k = 0; k < kCS; k++)
     if (W.tag[k] == comm) s = k;
   return s;
+}
+
+// per-rank seq order of the block at ring position p against the comm's previous block:
+// the same batch (ring position pp) or the slot table (uniform seq useq, or the pool)
+__device__ __noinline__ bool seq_order_ranks(const ct_record* R, uint32_t p, uint32_t n, uint32_t pp, bool in_batch,
+                                             bool uni, unsigned long long useq, const unsigned long long* pool,
+                                             uint32_t cb) {
+  bool ok = true;
+  for (uint32_t r = 0; r < n; r++) {
+    const unsigned long long ps = in_batch ? R[(pp + r) & kRM].seq : (uni ? useq : pool[(cb + r) & (kCP - 1)]);
+    ok = ok && ps < R[(p + r) & kRM].seq;
+  }
+  return ok;
 }
 
 // pairwise-distinct devices of the block of n records starting at ring position p
@@ -593,7 +611,7 @@ __device__ __forceinline__ void expand_block(const FastParams& P, Sink<SH>& sk, 
                                              unsigned long long devs, RingAcc& ra, int slot, SAE* sa, SAReq& sq) {
   const int n = (int)h.nranks, coll = h.coll();
   const unsigned long long base = min((unsigned long long)gidx, (1ull << 41) - 1) << 21;
-  if ((h.count >> 40) != 0) {
+  if (CT_UNLIKELY((h.count >> 40) != 0)) {
     for (int j = 0; j < n; j++) {
       Rec rc = h;
       rc.rank = (uint32_t)j;
@@ -819,7 +837,7 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
           }
           while (true) {  // allocate slots for unseen comms (rare, warp-serial)
             const unsigned miss = __ballot_sync(kFull, isC && slot < 0);
-            if (!miss) break;
+            if (CT_LIKELY(!miss)) break;
             const uint32_t cm = __shfl_sync(kFull, h.comm, __ffs(miss) - 1);
             int free_s = -1;
             for (int s = kCS - 1; s >= 0; s--)
@@ -854,7 +872,7 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
             if (lane == 0) W.cbase[sL] = cnext;
             cnext += nL;
           }
-          if (cnext > (uint32_t)kCP) bad = true;  // more ranks in one range than the pool holds
+          if (CT_UNLIKELY(cnext > (uint32_t)kCP)) bad = true;  // more ranks in one range than the pool holds
           __syncwarp();
           const uint32_t cb = W.cbase[hs];
           {  // the element lies inside the range; lengths tile it (with the copies)
@@ -868,6 +886,7 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
           // ---- validation (lane walks its element)
           uint32_t st = ST_NONE;
           bool fastdev = false, packed = false;  // all devices < gcap / held in ``devs``
+          bool uniform = true;                    // every rank of the block carries the head's seq
           unsigned long long devs = 0;          // device of rank j in byte j (n <= 8, devices < 64)
           uint64_t rseq = 0;
           uint32_t rdev = 0;
@@ -879,9 +898,9 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
             const uint32_t hc0 = (uint32_t)h.count, hc1 = (uint32_t)(h.count >> 32);
             const uint32_t hw7 = h.aux2 | (h.kc << 16) | (h.ad << 24);
             const uint32_t rootm = h.has_root() ? 0xFFFF0000u : 0u, hw6 = h.aux << 16;
-            uint32_t badw = 0, incw = 0;
-            bool ord = false, big = false, dup = false;
-            const bool have = pl >= 0 || hist;
+            uint32_t badw = 0, incw = 0, useqw = 0;
+            bool big = false, dup;
+            const uint32_t hq0 = (uint32_t)h.seq, hq1 = (uint32_t)(h.seq >> 32);
             unsigned long long dm = 0;
             auto vrec = [&](uint32_t j) {  // one member record (independent across j)
               const uint32_t ix = (p + j) & kRM;
@@ -889,18 +908,10 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
               const uint32_t x7 = wb.w ^ hw7;
               badw |= (wb.x ^ h.comm) | (wb.y ^ (n | (j << 16))) | (x7 & 0x00070000u);  // kind, comm, n, rank
               incw |= (wa.x ^ hc0) | (wa.y ^ hc1) | (x7 & 0x3F780000u) | ((wb.z ^ hw6) & rootm);  // signature
-              const unsigned long long seq = ((unsigned long long)wa.w << 32) | wa.z;
-              // previous block of the comm: this batch (ring) or the slot table (always a valid
-              // address; ignored without history)
-              const uint64_t* ps =
-                  pl >= 0 ? &R[(ppos + j) & kRM].seq : reinterpret_cast<const uint64_t*>(&W.cpool[(cb + j) & (kCP - 1)]);
-              const unsigned long long pv = *ps;
-              ord |= have & (pv >= seq);
+              useqw |= (wa.z ^ hq0) | (wa.w ^ hq1);  // every rank carries the head's seq
               const uint32_t dv = wb.z & 0xFFFF;
-              const unsigned long long bit = dv < 64 ? 1ull << dv : 0ull;
               big |= dv >= 64;
-              dup |= (dm & bit) != 0;
-              dm |= bit;
+              dm |= dv < 64 ? 1ull << dv : 0ull;
               devs |= (unsigned long long)(dv & 0xFF) << (8 * (j & 7));
             };
             uint32_t j = j0;
@@ -913,8 +924,8 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
             }
             if (i < n) vrec(j);
             if (badw) bad = true;
-            if (ord) bad = true;  // per (comm, rank) seq must strictly increase
-            if (big && !dup) dup = !devices_distinct(R, p, n);
+            uniform = useqw == 0;
+            dup = big ? !devices_distinct(R, p, n) : __popcll(dm) != (int)n;  // pairwise distinct devices
             fastdev = !big && (P.gcap >= 64 || (dm >> P.gcap) == 0);
             packed = !big && n <= 8;
             st = incw ? ST_INCOMPAT : (dup ? ST_DUPDEV : ST_VALID);
@@ -925,9 +936,21 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
             rseq = r.seq;
             rdev = r.dev;
           }
-          if (__any_sync(kFull, bad)) { wflags |= F_NONCANON; bail = true; break; }
+          {  // per (comm, rank) seq strictly increasing from the comm's previous block
+            const bool pu = __shfl_sync(kFull, uniform, pl < 0 ? lane : pl);
+            const unsigned long long pq = __shfl_sync(kFull, h.seq, pl < 0 ? lane : pl);
+            if (isC && !bad && (pl >= 0 || hist)) {
+              const bool tu = pl < 0 && W.uni[hs];
+              if (CT_LIKELY(uniform && (pl >= 0 ? pu : tu))) {  // one comparison per block
+                if (!((pl >= 0 ? pq : W.useq[hs]) < h.seq)) bad = true;
+              } else {  // rank by rank
+                if (!seq_order_ranks(R, p, n, pl >= 0 ? ppos : 0u, pl >= 0, tu, W.useq[hs], W.cpool, cb)) bad = true;
+              }
+            }
+          }
+          if (CT_UNLIKELY(__any_sync(kFull, bad))) { wflags |= F_NONCANON; bail = true; break; }
           if (__any_sync(kFull, isS)) wflags |= p2p_order(P.chans + (size_t)gw * kPC, h, rseq, isS, lane);
-          if (st > ST_VALID) count_diag(st);
+          if (CT_UNLIKELY(st > ST_VALID)) count_diag(st);
 
           // REGION tables
           // ---- tables: the last block of each comm in the batch; first occurrences
@@ -938,11 +961,13 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
             if (lastb) {
               W.sn[hs] = n;
               W.clast[hs] = gi;
+              W.uni[hs] = uniform ? 1u : 0u;
+              W.useq[hs] = h.seq;
             }
           }
           // the last block of each comm becomes the slot's seq table: one block per step,
           // lane = rank
-          for (unsigned lb = __ballot_sync(kFull, lastb); lb; lb &= lb - 1) {
+          for (unsigned lb = __ballot_sync(kFull, lastb && !uniform); lb; lb &= lb - 1) {
             const int L = __ffs(lb) - 1;
             const uint32_t pL = __shfl_sync(kFull, p, L), nL = __shfl_sync(kFull, n, L);
             const int sL = __shfl_sync(kFull, hs, L);
@@ -971,7 +996,7 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
               if (rdev != h.dev) sk.edge(CT_T_SENDRECV, (int)h.dev, (int)rdev, nbytes);
             }
           }
-          if (__any_sync(kFull, sq.act)) {  // slot accumulators: one lane per entry writes out / re-keys
+          if (CT_UNLIKELY(__any_sync(kFull, sq.act))) {  // slot accumulators: one lane per entry writes out / re-keys
             __syncwarp();
             const unsigned grp = __match_any_sync(kFull, sq.act ? sq.e : (0x100u | (uint32_t)lane));
             if (sq.act && (grp >> lane) == 1u) sk.flags |= sa_flush<SH>(P, &W.sa[sq.e], sq.key, devs);

@@ -35,12 +35,14 @@ class Gen:
     """Canonical-layout trace builder (blocks contiguous in rank order, per-(comm, rank)
     seq increasing, p2p channels FIFO)."""
 
-    def __init__(self, rng, n_comms, max_n=8, dev_pool=8, wide=0.0, diag=0.0, dev_change=0.01):
+    def __init__(self, rng, n_comms, max_n=8, dev_pool=8, wide=0.0, diag=0.0, dev_change=0.01, ragged=0.0):
         self.rng, self.recs = rng, []
+        self.ragged = ragged  # probability that a block's ranks carry different seqs
         self.wide, self.diag, self.dev_change, self.dev_pool = wide, diag, dev_change, dev_pool
         self.n = [int(rng.integers(1, max_n + 1)) for _ in range(n_comms)]
         self.devs = [self._perm(n) for n in self.n]
         self.seq = [0] * n_comms
+        self.rseq = [[0] * 32 for _ in range(n_comms)]  # per-(comm, rank) counters
         self.p2p_comm, self.copy_comm = n_comms, n_comms + 1
         self.chan = {}
 
@@ -58,7 +60,13 @@ class Gen:
         count = int(rng.integers(1 << 40, 1 << 42)) if rng.random() < self.wide else int(2 ** rng.uniform(0, 24))
         rooted = coll in (BC, RD)
         root = int(rng.integers(0, n))
-        seq = self.seq[c] = self.seq[c] + int(rng.integers(1, 3))
+        seq = self.seq[c] = max(self.seq[c], max(self.rseq[c][:n])) + int(rng.integers(1, 3))
+        if rng.random() < self.ragged:  # per-rank seqs, each still strictly increasing
+            seqs = [max(self.rseq[c][r], seq) + int(rng.integers(0, 3)) for r in range(n)]
+        else:
+            seqs = [seq] * n
+        for r in range(n):
+            self.rseq[c][r] = seqs[r]
         bad = rng.random() < self.diag
         devs = list(self.devs[c])
         if bad and n > 1 and rng.random() < 0.5:
@@ -66,7 +74,7 @@ class Gen:
             bad = False
         for r in range(n):
             cnt = count + (1 if bad and r == n - 1 else 0)  # incompatible signature
-            _rec(self.recs, cnt, seq, c, n, r, devs[r], aux=root if rooted else 0, coll=coll, root=rooted,
+            _rec(self.recs, cnt, seqs[r], c, n, r, devs[r], aux=root if rooted else 0, coll=coll, root=rooted,
                  algo=algo, dtype=dtype)
 
     def pair(self):
@@ -140,7 +148,7 @@ def _check(recs, n_comms, d=None, ring_order=None):
 @pytest.mark.parametrize("seed", [0, 1, 2])
 def test_mixed_canonical_with_diagnostics(seed):
     rng = np.random.default_rng(seed)
-    g = Gen(rng, n_comms=6, diag=0.02, dev_change=0.02).mixed(600_000)
+    g = Gen(rng, n_comms=6, diag=0.02, dev_change=0.02, ragged=0.3 if seed else 0.0).mixed(600_000)
     s, _ = _check(g.array(), n_comms=6)
     assert sum(s.diag) > 0
 
