@@ -712,76 +712,81 @@ uint64_t partial_words(int g2, uint32_t n_comms) {
 }
 
 // comm / channel lists of a shard in first-seen order (single thread, once per export)
-__global__ void k_shard_lists(const WarpSlot* slots, const P2PEntry* chans, uint32_t total_warps, uint64_t* exp,
-                              uint64_t* chx, uint64_t* overflow) {
-  int cnt = 0, cc = 0;
-  for (uint32_t w = 0; w < total_warps; w++) {
-    for (int s = 0; s < kCS; s++) {
-      const WarpSlot& x = slots[(size_t)w * kCS + s];
-      if (x.comm == 0xFFFFFFFFu || x.n == 0) continue;
-      bool seen = false;
-      for (int e = 0; e < cnt; e++) seen |= exp[e * kExpWords] == x.comm;
-      if (seen) continue;
-      if (cnt == kExport) { *overflow = 1; return; }
-      exp[(cnt++) * kExpWords] = x.comm;
+// One CTA: the unique communicators (<= kExport) and p2p channels (<= kExportCh) of this
+// shard's warp ranges, each with its first and last occurrence (lowest / highest warp
+// range), found with shared-memory hash sets; then the boundary summaries the merge
+// checks across shards (first / last block records, first / last channel seqs).
+__global__ void __launch_bounds__(1024) k_shard_export(const WarpSlot* slots, const P2PEntry* chans,
+                                                       uint32_t total_warps, const ct_record* recs, uint64_t* exp,
+                                                       uint64_t* chx, uint64_t* overflow) {
+  constexpr int TC = 2 * kExport, TH = 2 * kExportCh;
+  __shared__ unsigned long long ckey[TC], hkey[TH];
+  __shared__ uint32_t cmin[TC], cmax[TC], hmin[TH], hmax[TH];
+  __shared__ int nc, nh, ovf;
+  const int tid = threadIdx.x;
+  for (int i = tid; i < TC; i += blockDim.x) { ckey[i] = ~0ull; cmin[i] = ~0u; cmax[i] = 0; }
+  for (int i = tid; i < TH; i += blockDim.x) { hkey[i] = ~0ull; hmin[i] = ~0u; hmax[i] = 0; }
+  if (tid == 0) { nc = 0; nh = 0; ovf = 0; }
+  __syncthreads();
+  auto insert = [&](unsigned long long* tab, int cap, unsigned long long key) -> int {
+    uint32_t h = (uint32_t)((key * 0x9E3779B97F4A7C15ull) >> 40) % (uint32_t)cap;
+    for (int probe = 0; probe < cap; probe++, h = (h + 1) % (uint32_t)cap) {
+      const unsigned long long old = atomicCAS(&tab[h], ~0ull, key);
+      if (old == ~0ull || old == key) return (int)h;
     }
-    for (int q = 0; q < kPC; q++) {
-      const uint64_t key = chans[(size_t)w * kPC + q].key;
-      if (key == ~0ull) continue;
-      bool seen = false;
-      for (int e = 0; e < cc; e++) seen |= chx[e * kChWords] == key;
-      if (seen) continue;
-      if (cc == kExportCh) { *overflow = 1; return; }
-      chx[(cc++) * kChWords] = key;
-    }
+    return -1;
+  };
+  const uint32_t ns = total_warps * kCS, nq = total_warps * kPC;
+  for (uint32_t i = tid; i < ns; i += blockDim.x) {
+    const WarpSlot& x = slots[i];
+    if (x.comm == 0xFFFFFFFFu || x.n == 0) continue;
+    const int h = insert(ckey, TC, x.comm);
+    if (h < 0) { ovf = 1; continue; }
+    atomicMin(&cmin[h], i);
+    atomicMax(&cmax[h], i);
   }
-}
-
-// block e < kExport: collective summary of comm e; block kExport: channel summaries
-__global__ void k_shard_summary(const WarpSlot* slots, const P2PEntry* chans, uint32_t total_warps,
-                                const ct_record* recs, uint64_t* exp, uint64_t* chx) {
-  if (blockIdx.x == kExport) {
-    const int e = threadIdx.x;
-    if (e >= kExportCh) return;
-    uint64_t* o = chx + e * kChWords;
-    if (o[0] == ~0ull) return;
-    bool got = false;
-    for (uint32_t w = 0; w < total_warps && !got; w++)
-      for (int q = 0; q < kPC; q++) {
-        const P2PEntry& x = chans[(size_t)w * kPC + q];
-        if (x.key == o[0]) { o[1] = x.first_s; o[2] = x.first_r; got = true; break; }
+  for (uint32_t i = tid; i < nq; i += blockDim.x) {
+    const unsigned long long key = chans[i].key;
+    if (key == ~0ull) continue;
+    const int h = insert(hkey, TH, key);
+    if (h < 0) { ovf = 1; continue; }
+    atomicMin(&hmin[h], i);
+    atomicMax(&hmax[h], i);
+  }
+  __syncthreads();
+  // compact into the export lists (any order: the merge matches entries by key)
+  for (int i = tid; i < TC; i += blockDim.x)
+    if (ckey[i] != ~0ull) {
+      const int e = atomicAdd(&nc, 1);
+      if (e >= kExport) { ovf = 1; continue; }
+      const WarpSlot& f = slots[cmin[i]];
+      const WarpSlot& l = slots[cmax[i]];
+      uint64_t* o = exp + e * kExpWords;
+      o[0] = ckey[i];
+      o[1] = f.n;
+      o[2] = f.coll_first;
+      o[3] = l.coll_last;
+      if (f.n <= 32) {
+        ct_record* fr = reinterpret_cast<ct_record*>(o + 4);
+        ct_record* lr = reinterpret_cast<ct_record*>(o + 4 + 32 * 4);
+        for (uint32_t r = 0; r < f.n; r++) { fr[r] = recs[f.coll_first + r]; lr[r] = recs[l.coll_last + r]; }
       }
-    got = false;
-    for (int64_t w = (int64_t)total_warps - 1; w >= 0 && !got; w--)
-      for (int q = 0; q < kPC; q++) {
-        const P2PEntry& x = chans[(size_t)w * kPC + q];
-        if (x.key == o[0]) { o[3] = x.last_s; o[4] = x.last_r; got = true; break; }
-      }
-    return;
-  }
-  if (threadIdx.x) return;
-  uint64_t* o = exp + blockIdx.x * kExpWords;
-  const uint64_t cm = o[0];
-  if (cm == ~0ull) return;
-  uint64_t first = ~0ull, last = ~0ull, n = 0;
-  for (uint32_t w = 0; w < total_warps && first == ~0ull; w++)
-    for (int s = 0; s < kCS; s++) {
-      const WarpSlot& x = slots[(size_t)w * kCS + s];
-      if (x.comm == cm && x.n) { first = x.coll_first; n = x.n; break; }
     }
-  for (int64_t w = (int64_t)total_warps - 1; w >= 0 && last == ~0ull; w--)
-    for (int s = 0; s < kCS; s++) {
-      const WarpSlot& x = slots[(size_t)w * kCS + s];
-      if (x.comm == cm && x.n) { last = x.coll_last; break; }
+  for (int i = tid; i < TH; i += blockDim.x)
+    if (hkey[i] != ~0ull) {
+      const int e = atomicAdd(&nh, 1);
+      if (e >= kExportCh) { ovf = 1; continue; }
+      const P2PEntry& f = chans[hmin[i]];
+      const P2PEntry& l = chans[hmax[i]];
+      uint64_t* o = chx + e * kChWords;
+      o[0] = hkey[i];
+      o[1] = f.first_s;
+      o[2] = f.first_r;
+      o[3] = l.last_s;
+      o[4] = l.last_r;
     }
-  o[1] = n;
-  o[2] = first;
-  o[3] = last;
-  if (n && n <= 32) {
-    ct_record* fr = reinterpret_cast<ct_record*>(o + 4);
-    ct_record* lr = reinterpret_cast<ct_record*>(o + 4 + 32 * 4);
-    for (uint64_t r = 0; r < n; r++) { fr[r] = recs[first + r]; lr[r] = recs[last + r]; }
-  }
+  __syncthreads();
+  if (tid == 0 && ovf) *overflow = 1;
 }
 
 __global__ void k_merge_partials(const uint64_t* parts, int world, uint64_t words, int g2, uint32_t n_comms,
@@ -922,9 +927,8 @@ int ct_partial_export(ct_context* c, uint64_t* dev_out, uint64_t words, void* st
   CTX_TRY(c, cudaMemsetAsync(dev_out + words - 1, 0, 8, st));
   if (c->last.path == 1 && c->last_total_warps) {
     uint64_t* chx = dev_out + o_exp + kExport * kExpWords;
-    k_shard_lists<<<1, 1, 0, st>>>(c->slots, c->chans, c->last_total_warps, dev_out + o_exp, chx, dev_out + words - 1);
-    k_shard_summary<<<kExport + 1, 64, 0, st>>>(c->slots, c->chans, c->last_total_warps, c->last_input,
-                                                dev_out + o_exp, chx);
+    k_shard_export<<<1, 1024, 0, st>>>(c->slots, c->chans, c->last_total_warps, c->last_input, dev_out + o_exp, chx,
+                                       dev_out + words - 1);
     CTX_TRY(c, cudaGetLastError());
   }
   return CT_OK;
