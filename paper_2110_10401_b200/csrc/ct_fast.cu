@@ -336,6 +336,7 @@ struct RingAcc {
   unsigned long long g_lo, d_lo, s_lo;  // edge sums, payload sum
   uint32_t g_hi, d_hi, s_hi, cnt;
   uint32_t miss;                // consecutive instances that did not match the key
+  uint32_t thr;                 // misses before re-keying: doubles when a key collected few instances
 
   template <bool SH>
   __device__ __forceinline__ void flush(Sink<SH>& sk, int g2) {
@@ -349,8 +350,11 @@ struct RingAcc {
   __device__ __forceinline__ bool add(Sink<SH>& sk, int g2, uint32_t t, unsigned long long dv, unsigned long long g,
                                       unsigned long long d, unsigned long long sz) {
     if (t != tag || dv != devs) {
-      if (CT_LIKELY(tag && ++miss < 8)) return false;
-      if (tag) flush(sk, g2);
+      if (CT_LIKELY(tag && ++miss < thr)) return false;
+      if (tag) {
+        thr = cnt < thr ? min(2 * thr, 4096u) : 8u;  // back off when keys do not repeat per lane
+        flush(sk, g2);
+      }
       tag = t; devs = dv;
       g_lo = d_lo = s_lo = 0; g_hi = d_hi = s_hi = cnt = 0;
     }
@@ -723,6 +727,7 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
   RingAcc racc;
   racc.tag = 0;
   racc.miss = 0;
+  racc.thr = 8;
   int my_max_dev = -1;
   uint32_t copy_seen = 0;              // copy kinds this lane has seen (first index noted)
   uint32_t wflags = 0;
