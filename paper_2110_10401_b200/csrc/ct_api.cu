@@ -209,9 +209,6 @@ int summarize_state(ct_context* c, const GlobalState& gs, int gcap, int64_t d, i
   out->path = path;
   out->d = d;
   out->g_cap = gcap;
-  out->reserved = gs.n_chain;  // diagnostic counter (CT_DEBUG_MODE & 8: steady windows)
-  out->err_aux[2] = gs.err_index;  // diagnostic (CT_DEBUG_MODE & 16), overwritten by error detail
-  out->err_aux[3] = gs.pad;  // diagnostic bits (CT_DEBUG_MODE & 8), overwritten by error detail
   for (int t = 0; t < kTypes; t++) {
     out->calls[t] = gs.calls[t];
     out->payload_lo[t] = gs.pay_lo[t];

@@ -42,8 +42,8 @@ constexpr int kQ = 64;          // element queue entries per warp
 struct GlobalState {
   uint32_t flags;
   int32_t max_dev;
-  uint32_t n_chain;
-  uint32_t pad;
+  uint32_t unused0;
+  uint32_t unused1;
   unsigned long long diag[CT_NDIAG];
   unsigned long long calls[kTypes];
   unsigned long long pay_lo[kTypes];
