@@ -437,24 +437,38 @@ __device__ __noinline__ uint32_t p2p_order(P2PEntry* chan, const Rec ra, uint64_
   const int pl = lower ? 31 - __clz(lower) : -1;  // previous pair of the channel in this batch
   const uint64_t ps = __shfl_sync(kFull, sseq, pl < 0 ? lane : pl);
   const uint64_t pr = __shfl_sync(kFull, rseq, pl < 0 ? lane : pl);
+  // first pair of the channel in this batch: the warp's (private) channel table, looked up
+  // with plain loads; channels new to this range are inserted one lane at a time
+  const bool first = sendA && !lower;
   int e = -1;
-  if (sendA && !lower) {  // first pair of the channel in this batch: channel table
+  bool ins = false;
+  if (first) {
     uint32_t h = (uint32_t)((key * 0x9E3779B97F4A7C15ull) >> 58) % kPC;
     for (int probe = 0; probe < kPC; probe++, h = (h + 1) % kPC) {
-      const unsigned long long old = atomicCAS(reinterpret_cast<unsigned long long*>(&chan[h].key), kNone, key);
-      if (old == kNone) {  // first pair of the channel in this range
-        chan[h].first_s = sseq; chan[h].first_r = rseq;
-        chan[h].last_s = sseq; chan[h].last_r = rseq;
-        e = (int)h;
-        break;
-      }
-      if (old == key) {
+      const uint64_t k = chan[h].key;
+      if (k == key) {
         if (sseq < chan[h].last_s || rseq < chan[h].last_r) wflags |= F_NONCANON;
         e = (int)h;
         break;
       }
+      if (k == kNone) { ins = true; break; }
     }
-    if (e < 0) wflags |= F_NONCANON;  // more channels than the table holds
+    if (e < 0 && !ins) wflags |= F_NONCANON;  // more channels than the table holds
+  }
+  for (unsigned todo = __ballot_sync(kFull, ins); todo; todo &= todo - 1) {
+    __syncwarp();
+    if (lane == __ffs(todo) - 1) {
+      uint32_t h = (uint32_t)((key * 0x9E3779B97F4A7C15ull) >> 58) % kPC;
+      for (int probe = 0; probe < kPC; probe++, h = (h + 1) % kPC)
+        if (chan[h].key == kNone) {
+          chan[h].key = key;
+          chan[h].first_s = sseq; chan[h].first_r = rseq;
+          chan[h].last_s = sseq; chan[h].last_r = rseq;
+          e = (int)h;
+          break;
+        }
+      if (e < 0) wflags |= F_NONCANON;
+    }
   }
   if (sendA && pl >= 0 && (sseq < ps || rseq < pr)) wflags |= F_NONCANON;
   const int e_grp = __shfl_sync(kFull, e, sendA ? __ffs(m) - 1 : lane);
