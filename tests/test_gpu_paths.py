@@ -230,3 +230,32 @@ def test_overflow_through_accumulated_repeats():
     # one instance fewer than the bound stays exact
     m = (1 << 21) - 1
     _check(recs[:2 * m], n_comms=1)
+
+
+def _check_any_path(recs, n_comms, d=None):
+    """Like _check, but the trace may exceed the fast path's per-warp capacities: the host
+    then re-runs through the exact (sort-based) path; results must still match."""
+    from oracle import c_oracle as CO
+    s, cells, freq = _gpu(recs, n_comms, d=d, force=0)
+    want = CO.analyze_records(recs, d=d, gcap=s.g_cap)
+    want_status = want["status"] or (4 if want["overflow"] else 0)
+    assert s.status == want_status
+    assert np.array_equal(cells, want["cells"]) and np.array_equal(freq, want["freq"])
+    for t in range(9):
+        assert s.calls[t] == int(want["calls"][t]), t
+    return s
+
+
+def test_capacity_fallbacks_match():
+    """> 8 communicators interleaved within one warp range (comm slots) and communicators
+    totalling > 64 ranks (pooled seq tables) leave the fast path; the answer is the same."""
+    rng = np.random.default_rng(11)
+    g = Gen(rng, n_comms=12, max_n=4).mixed(20_000, p_pair=0.0, p_copy=0.0)
+    s = _check_any_path(g.array(), n_comms=12)
+    assert s.path == 2
+    g = Gen(rng, n_comms=3, max_n=32, dev_pool=32)
+    g.n = [32, 32, 32]
+    g.devs = [g._perm(32) for _ in range(3)]
+    g.mixed(20_000, p_pair=0.0, p_copy=0.0)
+    s = _check_any_path(g.array(), n_comms=3)
+    assert s.path == 2
