@@ -765,13 +765,14 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
     const uint32_t eo = (uint32_t)(end - rb0);
     const uint32_t lastc = (eo + 31) / 32;  // chunks [0, lastc) hold the range
     const ct_record* R = &W.ring[0][0];
+    // chunk c of the range is gsrc[32c, 32c + 32): full below nfull, else the trace's tail
+    const ct_record* gsrc = P.recs + rb0;
+    const uint32_t nfull = (uint32_t)min((unsigned long long)((P.n - rb0) >> 5), 0xFFFFFFFFull);
+    const uint32_t tail = (uint32_t)((P.n - rb0) & 31) * (uint32_t)sizeof(ct_record);
+    auto chunk_bytes = [&](uint32_t c) -> uint32_t { return c < nfull ? 32u * (uint32_t)sizeof(ct_record) : tail; };
     for (uint32_t q = 0; q < (uint32_t)kRing && q < lastc; q++)
-      if (lane == 0) {
-        const uint64_t first = (k0 + q) * 32;
-        bulk_load(W.ring[q], P.recs + first, (uint32_t)min((uint64_t)32, P.n - first) * (uint32_t)sizeof(ct_record),
-                  &W.bar[q]);
-      }
-    uint32_t ready = 0, freed = 0;  // chunks waited for / released (slot re-issued)
+      if (lane == 0) bulk_load(W.ring[q], gsrc + (size_t)q * 32, chunk_bytes(q), &W.bar[q]);
+    uint32_t freed = 0;             // chunks released (slot re-issued)
     uint32_t qh = 0, qt = 0;        // element queue head / tail
     int cover = 0;                  // element lengths + copies (must equal the range's records)
     uint32_t cross = 0;             // 1: the last queued element extends past the scanned chunks
@@ -779,9 +780,9 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
     uint32_t cnext = 0;             // next free entry of the seq-table pool
     const bool stream_only = (P.dbg & 4) != 0, no_expand = (P.dbg & 1) != 0;
     bool bail = false;
-    for (uint32_t q = 0; q < lastc && !bail; q++) {
+    uint32_t q = 0;
+    for (; q < lastc && !bail; q++) {
       mbar_wait(&W.bar[q % kRing], (q / kRing) & 1);
-      ready = q + 1;
       if (stream_only) {  // diagnostic: stream only (roofline experiments)
         const uint32_t rel = q * 32 + lane;
         if (rel < eo) my_max_dev = max(my_max_dev, (int)(R[rel & kRM].dev ^ R[rel & kRM].rank));
@@ -1035,11 +1036,8 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         do {
           const uint32_t nq = freed + kRing;
-          if (nq < lastc && lane == 0) {
-            const uint64_t first = (k0 + nq) * 32;
-            bulk_load(W.ring[freed % kRing], P.recs + first,
-                      (uint32_t)min((uint64_t)32, P.n - first) * (uint32_t)sizeof(ct_record), &W.bar[freed % kRing]);
-          }
+          if (nq < lastc && lane == 0)
+            bulk_load(W.ring[freed % kRing], gsrc + (size_t)nq * 32, chunk_bytes(nq), &W.bar[freed % kRing]);
           freed++;
         } while (freed < keep);
       }
@@ -1049,8 +1047,8 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
       if (tot != (int)(eo - s0)) wflags |= F_NONCANON;
     }
     const uint32_t issued = min(freed + (uint32_t)kRing, lastc);
-    for (uint32_t q = ready; q < issued; q++)  // drain outstanding bulk copies
-      mbar_wait(&W.bar[q % kRing], (q / kRing) & 1);
+    for (uint32_t c = bail ? q + 1 : q; c < issued; c++)  // drain outstanding bulk copies
+      mbar_wait(&W.bar[c % kRing], (c / kRing) & 1);
   }
 
   // REGION epilogue
