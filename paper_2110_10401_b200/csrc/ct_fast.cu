@@ -910,7 +910,7 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
           unsigned long long devs = 0;          // device of rank j in byte j (n <= 8, devices < 64)
           uint64_t rseq = 0;
           uint32_t rdev = 0;
-          const uint32_t j0 = n == 0 ? 0u : ((uint32_t)lane < n ? (uint32_t)lane : (uint32_t)lane % n);
+          const uint32_t j0 = n == 0 ? 0u : ((n & (n - 1)) == 0 ? (uint32_t)lane & (n - 1) : (uint32_t)lane % n);
           if (isC && !bad) {
             // compare raw words against the head: w4 comm, w5 nranks | rank << 16, w6 dev |
             // aux << 16 (aux = root when rooted), w7 aux2 | kc << 16 | ad << 24
