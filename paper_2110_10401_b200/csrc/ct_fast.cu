@@ -22,7 +22,8 @@ static_assert((kQ & (kQ - 1)) == 0 && kQ >= 64, "queue holds < 32 carried + 32 n
 struct __align__(16) SAE {
   uint32_t key;               // 1 << 31 | slot | cls << 3 | coll << 6 | n << 9 | root << 13; 0: empty
   uint32_t cnt;               // instances
-  unsigned long long devs;    // device of rank j in byte j
+  uint32_t devs;              // device of rank j in bits [4j, 4j + 4)
+  uint32_t pad0;
   uint32_t g[2], d[2], s[2];  // edge sums (ring: gen / dlt; tree: ceil(S/2) / floor(S/2)), payload
   uint32_t cnt2;              // tree: instances with floor(S/2) != 0
   uint32_t pad;
@@ -261,18 +262,17 @@ __device__ __forceinline__ unsigned long long tree_peers(int n, int j);
 // tree -- T1-only peers g, peers in both trees g + d, T2-only peers d (cnt2 transfers).
 template <bool SH>
 __device__ __noinline__ uint32_t flush_acc(const FastParams& P, int g2, int coll, int n, int mode, int root,
-                                           unsigned long long devs, unsigned long long g_lo, uint32_t g_hi,
+                                           uint32_t devs, unsigned long long g_lo, uint32_t g_hi,
                                            unsigned long long d_lo, uint32_t d_hi, unsigned long long s_lo,
                                            uint32_t s_hi, uint32_t cnt, uint32_t cnt2) {
   Sink<SH> sk(P);
   stat_limbs((uint32_t)coll, s_lo, s_hi, cnt);
-  const uint32_t dlo = (uint32_t)devs, dhi = (uint32_t)(devs >> 32);
   auto emit = [&](int q, int r, uint32_t k_g, uint32_t k_d, uint32_t c) {
     // v = k_g * g + k_d * d as 128 bits (k_* in {0, 1, 2})
     unsigned __int128 v = (unsigned __int128)k_g * (((unsigned __int128)g_hi << 64) | g_lo) +
                           (unsigned __int128)k_d * (((unsigned __int128)d_hi << 64) | d_lo);
-    const uint32_t key = (uint32_t)((coll * g2 + (int)(__byte_perm(dlo, dhi, (uint32_t)q) & 0xFF) + 2) * g2 +
-                                    (int)(__byte_perm(dlo, dhi, (uint32_t)r) & 0xFF) + 2);
+    const uint32_t key = (uint32_t)((coll * g2 + (int)((devs >> (4 * q)) & 15u) + 2) * g2 +
+                                    (int)((devs >> (4 * r)) & 15u) + 2);
     if ((v >> 63) != 0) sk.flags |= note_overflow(key);  // the cell exceeds 2^63 - 1
     else sk.add(key, (unsigned long long)v, c);
   };
@@ -286,7 +286,7 @@ __device__ __noinline__ uint32_t flush_acc(const FastParams& P, int g2, int coll
   } else if (mode == 2) {  // collnet: every rank sends S to NET and receives S from it
     const unsigned long long v = g_lo;
     for (int j = 0; j < n; j++) {
-      const int dv = (int)(__byte_perm(dlo, dhi, (uint32_t)j) & 0xFF) + 2;
+      const int dv = (int)((devs >> (4 * j)) & 15u) + 2;
       const uint32_t k_up = (uint32_t)((coll * g2 + dv) * g2 + kNet), k_dn = (uint32_t)((coll * g2 + kNet) * g2 + dv);
       if (g_hi != 0 || (v >> 63) != 0) {
         sk.flags |= note_overflow(k_up);
@@ -314,7 +314,7 @@ __device__ __noinline__ uint32_t flush_acc(const FastParams& P, int g2, int coll
 
 // Write out slot accumulator E, then re-key it to ``key`` (with ``devs``) unless key is 0.
 template <bool SH>
-__device__ __noinline__ uint32_t sa_flush(const FastParams& P, SAE* E, uint32_t key, unsigned long long devs) {
+__device__ __noinline__ uint32_t sa_flush(const FastParams& P, SAE* E, uint32_t key, uint32_t devs) {
   uint32_t f = 0;
   if (E->key && E->cnt)
   {
@@ -332,7 +332,7 @@ __device__ __noinline__ uint32_t sa_flush(const FastParams& P, SAE* E, uint32_t 
 
 struct RingAcc {
   uint32_t tag;                 // coll | n << 8 (0: empty)
-  unsigned long long devs;
+  uint32_t devs;
   unsigned long long g_lo, d_lo, s_lo;  // edge sums, payload sum
   uint32_t g_hi, d_hi, s_hi, cnt;
   uint32_t miss;                // consecutive instances that did not match the key
@@ -347,7 +347,7 @@ struct RingAcc {
   // false: the key differs and is kept (the caller expands the instance itself); after a
   // streak of misses the accumulator is flushed and re-keyed
   template <bool SH>
-  __device__ __forceinline__ bool add(Sink<SH>& sk, int g2, uint32_t t, unsigned long long dv, unsigned long long g,
+  __device__ __forceinline__ bool add(Sink<SH>& sk, int g2, uint32_t t, uint32_t dv, unsigned long long g,
                                       unsigned long long d, unsigned long long sz) {
     if (t != tag || dv != devs) {
       if (CT_LIKELY(tag && ++miss < thr)) return false;
@@ -408,14 +408,16 @@ __device__ __noinline__ bool seq_order_ranks(const ct_record* R, uint32_t p, uin
   return ok;
 }
 
-// pairwise-distinct devices of the block of n records starting at ring position p
-__device__ __noinline__ bool devices_distinct(const ct_record* R, uint32_t p, uint32_t n) {
-  for (uint32_t m = 1; m < n; m++) {
+// devices of the block of n records at ring position p when some device is >= 32:
+// bit 0 = two records share a device, bit 1 = every device is < gcap
+__device__ __noinline__ uint32_t block_devices(const ct_record* R, uint32_t p, uint32_t n, uint32_t gcap) {
+  bool dup = false, below = true;
+  for (uint32_t m = 0; m < n; m++) {
     const uint32_t d = R[(p + m) & kRM].dev;
-    for (uint32_t m2 = 0; m2 < m; m2++)
-      if (R[(p + m2) & kRM].dev == d) return false;
+    below = below && d < gcap;
+    for (uint32_t m2 = 0; m2 < m; m2++) dup = dup || R[(p + m2) & kRM].dev == d;
   }
-  return true;
+  return (dup ? 1u : 0u) | (below ? 2u : 0u);
 }
 
 // p2p order: per (comm, src, dst) channel, send seqs and recv seqs non-decreasing in file
@@ -532,7 +534,7 @@ __device__ __forceinline__ void limb_add(uint32_t* L, unsigned long long v) {  /
 template <bool SH>
 __device__ __noinline__ uint32_t expand_direct(const FastParams& P, const ct_record* R, const Rec h, uint32_t p,
                                                uint64_t gidx, uint32_t j0, bool fastdev, bool packed,
-                                               unsigned long long devs, int algo) {
+                                               uint32_t devs, int algo) {
   Sink<SH> sk(P);
   const int n = (int)h.nranks, coll = h.coll();
   const unsigned long long base = min((unsigned long long)gidx, (1ull << 41) - 1) << 21;
@@ -562,10 +564,7 @@ __device__ __noinline__ uint32_t expand_direct(const FastParams& P, const ct_rec
   if (rmap && !P.ex.ring_valid) { sk.flags |= F_BAD_RING; return sk.flags; }
   // tree shares
   const uint64_t share1 = s - s / 2, share2 = s / 2;
-  const uint32_t dlo = (uint32_t)devs, dhi = (uint32_t)(devs >> 32);
-  auto devof = [&](int r) -> int {
-    return packed ? (int)(__byte_perm(dlo, dhi, (uint32_t)r) & 0xFF) : (int)R[(p + r) & kRM].dev;
-  };
+  auto devof = [&](int r) -> int { return packed ? (int)((devs >> (4 * r)) & 15u) : (int)R[(p + r) & kRM].dev; };
   int q = ring ? (int)j0 : 0;
   for (int i = 0; i < n; i++) {
     const int qn = q + 1 == n ? 0 : q + 1;
@@ -626,7 +625,7 @@ __device__ __noinline__ uint32_t expand_direct(const FastParams& P, const ct_rec
 template <bool SH>
 __device__ __forceinline__ void expand_block(const FastParams& P, Sink<SH>& sk, const ct_record* R, const Rec& h,
                                              uint32_t p, uint64_t gidx, uint32_t j0, bool fastdev, bool packed,
-                                             unsigned long long devs, RingAcc& ra, int slot, SAE* sa, SAReq& sq) {
+                                             uint32_t devs, RingAcc& ra, int slot, SAE* sa, SAReq& sq) {
   const int n = (int)h.nranks, coll = h.coll();
   const unsigned long long base = min((unsigned long long)gidx, (1ull << 41) - 1) << 21;
   if (CT_UNLIKELY((h.count >> 40) != 0)) {
@@ -907,7 +906,7 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
           uint32_t st = ST_NONE;
           bool fastdev = false, packed = false;  // all devices < gcap / held in ``devs``
           bool uniform = true;                    // every rank of the block carries the head's seq
-          unsigned long long devs = 0;          // device of rank j in byte j (n <= 8, devices < 64)
+          uint32_t devs = 0;                    // device of rank j in bits [4j, 4j+4) (n <= 8, devices < 16)
           uint64_t rseq = 0;
           uint32_t rdev = 0;
           const uint32_t j0 = n == 0 ? 0u : ((n & (n - 1)) == 0 ? (uint32_t)lane & (n - 1) : (uint32_t)lane % n);
@@ -918,10 +917,9 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
             const uint32_t hc0 = (uint32_t)h.count, hc1 = (uint32_t)(h.count >> 32);
             const uint32_t hw7 = h.aux2 | (h.kc << 16) | (h.ad << 24);
             const uint32_t rootm = h.has_root() ? 0xFFFF0000u : 0u, hw6 = h.aux << 16;
-            uint32_t badw = 0, incw = 0, useqw = 0;
+            uint32_t badw = 0, incw = 0, useqw = 0, m32 = 0;
             bool big = false, dup;
             const uint32_t hq0 = (uint32_t)h.seq, hq1 = (uint32_t)(h.seq >> 32);
-            unsigned long long dm = 0;
             auto vrec = [&](uint32_t j) {  // one member record (independent across j)
               const uint32_t ix = (p + j) & kRM;
               const uint4 wa = R4[2 * ix], wb = R4[2 * ix + 1];
@@ -930,9 +928,9 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
               incw |= (wa.x ^ hc0) | (wa.y ^ hc1) | (x7 & 0x3F780000u) | ((wb.z ^ hw6) & rootm);  // signature
               useqw |= (wa.z ^ hq0) | (wa.w ^ hq1);  // every rank carries the head's seq
               const uint32_t dv = wb.z & 0xFFFF;
-              big |= dv >= 64;
-              dm |= dv < 64 ? 1ull << dv : 0ull;
-              devs |= (unsigned long long)(dv & 0xFF) << (8 * (j & 7));
+              big |= dv >= 32;
+              m32 |= 1u << (dv & 31);
+              devs |= (dv & 15u) << (4 * (j & 7));
             };
             uint32_t j = j0;
             uint32_t i = 0;
@@ -945,9 +943,15 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
             if (i < n) vrec(j);
             if (badw) bad = true;
             uniform = useqw == 0;
-            dup = big ? !devices_distinct(R, p, n) : __popcll(dm) != (int)n;  // pairwise distinct devices
-            fastdev = !big && (P.gcap >= 64 || (dm >> P.gcap) == 0);
-            packed = !big && n <= 8;
+            if (CT_LIKELY(!big)) {  // devices < 32: the mask holds them all
+              dup = __popc(m32) != (int)n;  // pairwise distinct devices
+              fastdev = P.gcap >= 32 || (m32 >> P.gcap) == 0;
+            } else {
+              const uint32_t info = block_devices(R, p, n, (uint32_t)P.gcap);
+              dup = (info & 1u) != 0;
+              fastdev = (info & 2u) != 0;
+            }
+            packed = !big && n <= 8 && (m32 >> 16) == 0;
             st = incw ? ST_INCOMPAT : (dup ? ST_DUPDEV : ST_VALID);
           } else if (isS) {
             const Rec r = ring_rec(R, p + 1);
