@@ -20,7 +20,7 @@
 namespace ct {
 template <bool SH>
 __global__ void fast_kernel(FastParams P);
-__global__ void range_check_kernel(const ct_record* recs, const WarpSlot* slots, const P2PEntry* chans,
+__global__ void range_check_kernel(const ct_record* recs, const WarpSlot* slots, const Chans chans,
                                    uint32_t total_warps, GlobalState* st);
 int generate(int kind, uint64_t seed, uint64_t first, uint64_t n, ct_record* out, cudaStream_t st);
 uint64_t generate_boundary(int kind, uint64_t at);
@@ -44,7 +44,7 @@ struct ct_context {
   size_t tcf_cap = 0;
   WarpSlot* slots = nullptr;   // per (warp range, comm slot) order summaries
   size_t slots_cap = 0;
-  P2PEntry* chans = nullptr;   // per (warp range, p2p channel) order summaries
+  uint64_t* chans = nullptr;   // per (warp range, p2p channel) order summaries (Chans layout)
   size_t chans_cap = 0;
   uint32_t last_total_warps = 0;
   uint16_t* ring = nullptr;  // order then inverse
@@ -116,7 +116,7 @@ int run_fast(ct_context* c, const ct_record* recs, uint64_t n, int gcap, bool ex
   if (ensure(c, c->slots, sc, (size_t)total_warps * kCS)) return CT_ERR_CUDA;
   c->slots_cap = sc;
   size_t pc = c->chans_cap;
-  if (ensure(c, c->chans, pc, (size_t)total_warps * kPC)) return CT_ERR_CUDA;
+  if (ensure(c, c->chans, pc, (size_t)total_warps * kPC * kChanWords)) return CT_ERR_CUDA;
   c->chans_cap = pc;
   c->last_total_warps = total_warps;
 
@@ -147,7 +147,7 @@ int run_fast(ct_context* c, const ct_record* recs, uint64_t n, int gcap, bool ex
   P.type_comm_first = c->tcf;
   P.comm_first = c->tcf + 5 * (size_t)std::max<uint32_t>(n_comms, 1);
   P.slots = c->slots;
-  P.chans = c->chans;
+  P.chans = Chans{c->chans, (uint64_t)total_warps * kPC};
   P.total_warps = total_warps;
   P.n_chunks = n_chunks;
   P.dbg = getenv("CT_DEBUG_MODE") ? atoi(getenv("CT_DEBUG_MODE")) : 0;
@@ -163,7 +163,7 @@ int run_fast(ct_context* c, const ct_record* recs, uint64_t n, int gcap, bool ex
     CTX_TRY(c, cudaGetLastError());
     CTX_TRY(c, cudaEventRecord(c->ev[1], st));
     const uint64_t threads = (uint64_t)total_warps * (kCS + kPC);
-    range_check_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(recs, c->slots, c->chans, total_warps,
+    range_check_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(recs, c->slots, P.chans, total_warps,
                                                                           c->st);
     CTX_TRY(c, cudaGetLastError());
     launches += 2;
@@ -713,7 +713,7 @@ uint64_t partial_words(int g2, uint32_t n_comms) {
 // shard's warp ranges, each with its first and last occurrence (lowest / highest warp
 // range), found with shared-memory hash sets; then the boundary summaries the merge
 // checks across shards (first / last block records, first / last channel seqs).
-__global__ void __launch_bounds__(1024) k_shard_export(const WarpSlot* slots, const P2PEntry* chans,
+__global__ void __launch_bounds__(1024) k_shard_export(const WarpSlot* slots, const Chans chans,
                                                        uint32_t total_warps, const ct_record* recs, uint64_t* exp,
                                                        uint64_t* chx, uint64_t* overflow) {
   constexpr int TC = 2 * kExport, TH = 2 * kExportCh;
@@ -743,7 +743,7 @@ __global__ void __launch_bounds__(1024) k_shard_export(const WarpSlot* slots, co
     atomicMax(&cmax[h], i);
   }
   for (uint32_t i = tid; i < nq; i += blockDim.x) {
-    const unsigned long long key = chans[i].key;
+    const unsigned long long key = chans.key(i);
     if (key == ~0ull) continue;
     const int h = insert(hkey, TH, key);
     if (h < 0) { ovf = 1; continue; }
@@ -773,14 +773,12 @@ __global__ void __launch_bounds__(1024) k_shard_export(const WarpSlot* slots, co
     if (hkey[i] != ~0ull) {
       const int e = atomicAdd(&nh, 1);
       if (e >= kExportCh) { ovf = 1; continue; }
-      const P2PEntry& f = chans[hmin[i]];
-      const P2PEntry& l = chans[hmax[i]];
       uint64_t* o = chx + e * kChWords;
       o[0] = hkey[i];
-      o[1] = f.first_s;
-      o[2] = f.first_r;
-      o[3] = l.last_s;
-      o[4] = l.last_r;
+      o[1] = chans.first_s(hmin[i]);
+      o[2] = chans.first_r(hmin[i]);
+      o[3] = chans.last_s(hmax[i]);
+      o[4] = chans.last_r(hmax[i]);
     }
   __syncthreads();
   if (tid == 0 && ovf) *overflow = 1;
@@ -924,7 +922,8 @@ int ct_partial_export(ct_context* c, uint64_t* dev_out, uint64_t words, void* st
   CTX_TRY(c, cudaMemsetAsync(dev_out + words - 1, 0, 8, st));
   if (c->last.path == 1 && c->last_total_warps) {
     uint64_t* chx = dev_out + o_exp + kExport * kExpWords;
-    k_shard_export<<<1, 1024, 0, st>>>(c->slots, c->chans, c->last_total_warps, c->last_input, dev_out + o_exp, chx,
+    k_shard_export<<<1, 1024, 0, st>>>(c->slots, Chans{c->chans, (uint64_t)c->last_total_warps * kPC},
+                                       c->last_total_warps, c->last_input, dev_out + o_exp, chx,
                                        dev_out + words - 1);
     CTX_TRY(c, cudaGetLastError());
   }

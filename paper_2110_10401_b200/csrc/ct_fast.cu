@@ -424,7 +424,8 @@ __device__ __noinline__ uint32_t block_devices(const ct_record* R, uint32_t p, u
 // order (then FIFO-by-position pairing equals the reference's seq-sorted pairing).  Lanes
 // hold send/recv pairs in file order (lane = element).
 // REGION p2p
-__device__ __noinline__ uint32_t p2p_order(P2PEntry* chan, const Rec ra, uint64_t next_seq, bool sendA, int lane) {
+__device__ __noinline__ uint32_t p2p_order(const Chans ch, uint64_t off, const Rec ra, uint64_t next_seq, bool sendA,
+                                           int lane) {
   uint32_t wflags = 0;
   const unsigned lt = (1u << lane) - 1;
   const unsigned gt = lane == 31 ? 0u : ~((2u << lane) - 1);
@@ -447,9 +448,9 @@ __device__ __noinline__ uint32_t p2p_order(P2PEntry* chan, const Rec ra, uint64_
   if (first) {
     uint32_t h = (uint32_t)((key * 0x9E3779B97F4A7C15ull) >> 58) % kPC;
     for (int probe = 0; probe < kPC; probe++, h = (h + 1) % kPC) {
-      const uint64_t k = chan[h].key;
+      const uint64_t k = ch.key(off + h);
       if (k == key) {
-        if (sseq < chan[h].last_s || rseq < chan[h].last_r) wflags |= F_NONCANON;
+        if (sseq < ch.last_s(off + h) || rseq < ch.last_r(off + h)) wflags |= F_NONCANON;
         e = (int)h;
         break;
       }
@@ -462,10 +463,10 @@ __device__ __noinline__ uint32_t p2p_order(P2PEntry* chan, const Rec ra, uint64_
     if (lane == __ffs(todo) - 1) {
       uint32_t h = (uint32_t)((key * 0x9E3779B97F4A7C15ull) >> 58) % kPC;
       for (int probe = 0; probe < kPC; probe++, h = (h + 1) % kPC)
-        if (chan[h].key == kNone) {
-          chan[h].key = key;
-          chan[h].first_s = sseq; chan[h].first_r = rseq;
-          chan[h].last_s = sseq; chan[h].last_r = rseq;
+        if (ch.key(off + h) == kNone) {
+          ch.key(off + h) = key;
+          ch.first_s(off + h) = sseq; ch.first_r(off + h) = rseq;
+          ch.last_s(off + h) = sseq; ch.last_r(off + h) = rseq;
           e = (int)h;
           break;
         }
@@ -475,7 +476,7 @@ __device__ __noinline__ uint32_t p2p_order(P2PEntry* chan, const Rec ra, uint64_
   if (sendA && pl >= 0 && (sseq < ps || rseq < pr)) wflags |= F_NONCANON;
   const int e_grp = __shfl_sync(kFull, e, sendA ? __ffs(m) - 1 : lane);
   __syncwarp();
-  if (sendA && (m & gt) == 0 && e_grp >= 0) { chan[e_grp].last_s = sseq; chan[e_grp].last_r = rseq; }
+  if (sendA && (m & gt) == 0 && e_grp >= 0) { ch.last_s(off + e_grp) = sseq; ch.last_r(off + e_grp) = rseq; }
   __syncwarp();
   return wflags;
 }
@@ -731,7 +732,7 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
     for (int t = 0; t < 5; t++) W.tfirst[lane][t] = kNone;
   }
   const uint32_t gw = blockIdx.x * kWarps + warp;
-  for (int e = lane; e < kPC; e += 32) P.chans[(size_t)gw * kPC + e].key = kNone;
+  for (int e = lane; e < kPC; e += 32) P.chans.key((uint64_t)gw * kPC + e) = kNone;
   if (lane < kRing) mbar_init(&W.bar[lane], 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
@@ -973,7 +974,7 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
             }
           }
           if (CT_UNLIKELY(__any_sync(kFull, bad))) { wflags |= F_NONCANON; bail = true; break; }
-          if (__any_sync(kFull, isS)) wflags |= p2p_order(P.chans + (size_t)gw * kPC, h, rseq, isS, lane);
+          if (__any_sync(kFull, isS)) wflags |= p2p_order(P.chans, (uint64_t)gw * kPC, h, rseq, isS, lane);
           if (CT_UNLIKELY(st > ST_VALID)) count_diag(st);
 
           // REGION tables
@@ -1122,7 +1123,7 @@ template __global__ void fast_kernel<false>(FastParams);
 // collective comm slots (nranks equal and per-rank seq strictly increasing from the last
 // block of the nearest earlier range holding the comm to this range's first block), items
 // [kCS, kCS + kPC) the p2p channels (send and recv seqs non-decreasing across ranges).
-__global__ void range_check_kernel(const ct_record* recs, const WarpSlot* slots, const P2PEntry* chans,
+__global__ void range_check_kernel(const ct_record* recs, const WarpSlot* slots, const Chans chans,
                                    uint32_t total_warps, GlobalState* st) {
   const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   const uint32_t per = kCS + kPC;
@@ -1143,13 +1144,14 @@ __global__ void range_check_kernel(const ct_record* recs, const WarpSlot* slots,
       }
     return;
   }
-  const P2PEntry& me = chans[(size_t)w * kPC + (item - kCS)];
-  if (me.key == kNone) return;
+  const uint64_t me = (uint64_t)w * kPC + (item - kCS);
+  const uint64_t mk = chans.key(me);
+  if (mk == kNone) return;
   for (int32_t v = (int32_t)w - 1; v >= 0; v--)
     for (int q = 0; q < kPC; q++) {
-      const P2PEntry& o = chans[(size_t)v * kPC + q];
-      if (o.key != me.key) continue;
-      if (me.first_s < o.last_s || me.first_r < o.last_r) atomicOr(&st->flags, F_NONCANON);
+      const uint64_t o = (uint64_t)v * kPC + q;
+      if (chans.key(o) != mk) continue;
+      if (chans.first_s(me) < chans.last_s(o) || chans.first_r(me) < chans.last_r(o)) atomicOr(&st->flags, F_NONCANON);
       return;
     }
 }

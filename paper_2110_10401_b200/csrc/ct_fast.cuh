@@ -62,11 +62,19 @@ struct WarpSlot {
   uint64_t coll_last;
 };
 
-// Per (warp range, p2p channel) summary: first / last send and recv seq in the range.
-struct P2PEntry {
-  uint64_t key;         // comm << 32 | src << 16 | dst; ~0: unused
-  uint64_t first_s, first_r, last_s, last_r;
+// Per (warp range, p2p channel): the channel key (comm << 32 | src << 16 | dst; ~0 unused)
+// and its first / last send and recv seq in the range, as structure-of-arrays over one
+// buffer of 5 * n u64 (lookups touch only the keys and last seqs: 24 B per entry in L1).
+struct Chans {
+  uint64_t* base;
+  uint64_t n;  // entries (total warps * kPC)
+  __device__ __forceinline__ uint64_t& key(uint64_t i) const { return base[i]; }
+  __device__ __forceinline__ uint64_t& last_s(uint64_t i) const { return base[n + 2 * i]; }
+  __device__ __forceinline__ uint64_t& last_r(uint64_t i) const { return base[n + 2 * i + 1]; }
+  __device__ __forceinline__ uint64_t& first_s(uint64_t i) const { return base[3 * n + 2 * i]; }
+  __device__ __forceinline__ uint64_t& first_r(uint64_t i) const { return base[3 * n + 2 * i + 1]; }
 };
+constexpr int kChanWords = 5;  // u64 per channel entry
 
 struct FastParams {
   const ct_record* recs;      // analyzed array (device)
@@ -83,7 +91,7 @@ struct FastParams {
   unsigned long long* type_comm_first;  // [5][n_comms] first valid head per (type, comm)
   unsigned long long* comm_first;       // [n_comms] first collective head per comm
   WarpSlot* slots;            // [total warps][kCS]
-  P2PEntry* chans;            // [total warps][kPC]
+  Chans chans;                // [total warps][kPC] entries
   uint32_t total_warps;
   uint64_t n_chunks;          // ceil(n / 32)
   uint32_t sa_flush;          // slot accumulator write-out threshold (instances, <= 2^14)
