@@ -333,6 +333,13 @@ int ct_context_create(int device, ct_context** out) {
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
   for (int k = 0; k < 4 && e == cudaSuccess; k++) e = cudaEventCreate(&c->ev[k]);
   if (e == cudaSuccess) e = cudaMalloc(&c->st, sizeof(GlobalState));
+  if (e == cudaSuccess) {  // keep freed stream-ordered memory in the pool (exact-path scratch is large)
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t keep = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  }
   if (e != cudaSuccess) {
     delete c;
     return CT_ERR_CUDA;

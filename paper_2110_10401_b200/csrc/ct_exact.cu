@@ -28,10 +28,24 @@ __global__ void k_classify(const ct_record* recs, uint64_t n, uint8_t* fc, uint8
 
 __global__ void k_first_coll(const ct_record* recs, const uint64_t* idx, uint64_t m,
                              unsigned long long* first) {
-  for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < m;
-       p += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t i = idx[p];
-    atomicMin(first + recs[i].comm, (unsigned long long)i);
+  // per comm: the smallest record index.  Lanes of one comm combine first (one atomic per
+  // comm per warp), and an atomic is skipped when the cell already holds a smaller index.
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t p0 = blockIdx.x * (uint64_t)blockDim.x; p0 < m; p0 += stride) {
+    const uint64_t p = p0 + (threadIdx.x & ~31u) + (threadIdx.x & 31u);
+    const bool act = p < m;
+    const uint64_t i = act ? idx[p] : ~0ull;
+    const uint32_t c = act ? recs[i].comm : 0xFFFFFFFFu;
+    if (__all_sync(0xFFFFFFFFu, __match_any_sync(0xFFFFFFFFu, c) == 0xFFFFFFFFu)) {  // one comm: warp minimum
+      unsigned long long mn = i;
+      for (int o = 16; o; o >>= 1) {
+        const unsigned long long x = __shfl_xor_sync(0xFFFFFFFFu, mn, o);
+        mn = x < mn ? x : mn;
+      }
+      if ((threadIdx.x & 31u) == 0 && act && mn < first[c]) atomicMin(first + c, mn);
+    } else if (act && i < first[c]) {
+      atomicMin(first + c, (unsigned long long)i);
+    }
   }
 }
 
