@@ -222,17 +222,24 @@ __global__ void k_p2p_runs(const uint64_t* ukey, const int64_t* run_len, const i
 
 __global__ void k_emit_pairs(const ct_record* recs, const uint64_t* idx, const uint64_t* run_off,
                              const int64_t* run_len, const int* n_runs, const uint64_t* emit_off,
-                             const uint64_t* emit_len, uint64_t base, ct_record* out, uint64_t* src_map) {
+                             const uint64_t* emit_len, uint64_t base, uint64_t n_pairs, ct_record* out,
+                             uint64_t* src_map) {
+  // one thread per emitted pair: its channel run is the last run whose output offset is
+  // <= 2j (runs are laid out back to back in emit_off order)
   const int R = *n_runs;
-  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < R; k += gridDim.x * blockDim.x) {
-    if (!emit_len[k]) continue;
-    const uint64_t pairs = emit_len[k] / 2, soff = run_off[k], roff = run_off[k + 1];
-    const uint64_t o = base + emit_off[k];
-    for (uint64_t j = 0; j < pairs; j++) {
-      out[o + 2 * j] = recs[idx[soff + j]];
-      out[o + 2 * j + 1] = recs[idx[roff + j]];
-      if (src_map) { src_map[o + 2 * j] = idx[soff + j]; src_map[o + 2 * j + 1] = idx[roff + j]; }
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n_pairs;
+       j += (uint64_t)gridDim.x * blockDim.x) {
+    int lo = 0, hi = R - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) / 2;
+      if (emit_off[mid] <= 2 * j) lo = mid; else hi = mid - 1;
     }
+    const int k = lo;
+    const uint64_t local = j - emit_off[k] / 2, soff = run_off[k], roff = run_off[k + 1];
+    const uint64_t o = base + 2 * j;
+    out[o] = recs[idx[soff + local]];
+    out[o + 1] = recs[idx[roff + local]];
+    if (src_map) { src_map[o] = idx[soff + local]; src_map[o + 1] = idx[roff + local]; }
   }
 }
 
@@ -549,7 +556,8 @@ int exact_canonicalize(const ct_record* recs, uint64_t n, uint32_t n_comms, cuda
     res->n_unmatched_recv = hu[1];
     pair_out = pool.get<ct_record>(pair_total);
     uint64_t* pmap = materialize ? pool.get<uint64_t>(pair_total) : nullptr;
-    k_emit_pairs<<<grid_for(R), 256, 0, st>>>(recs, v2, roff, rlen, d_runs, eoff, elen, 0, pair_out, pmap);
+    k_emit_pairs<<<grid_for(pair_total / 2), 256, 0, st>>>(recs, v2, roff, rlen, d_runs, eoff, elen, 0, pair_total / 2,
+                                                          pair_out, pmap);
     L += 9;
     if (materialize) {
       // every p2p diagnostic, reference order is restored on the host

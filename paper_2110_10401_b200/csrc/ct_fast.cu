@@ -1147,10 +1147,15 @@ __global__ void range_check_kernel(const ct_record* recs, const WarpSlot* slots,
   const uint64_t me = (uint64_t)w * kPC + (item - kCS);
   const uint64_t mk = chans.key(me);
   if (mk == kNone) return;
+  // the nearest earlier range holding the channel: every table is open-addressed with the
+  // same hash, so membership is a short probe sequence (stops at an empty entry)
+  const uint32_t h0 = (uint32_t)((mk * 0x9E3779B97F4A7C15ull) >> 58) % kPC;
   for (int32_t v = (int32_t)w - 1; v >= 0; v--)
-    for (int q = 0; q < kPC; q++) {
-      const uint64_t o = (uint64_t)v * kPC + q;
-      if (chans.key(o) != mk) continue;
+    for (uint32_t probe = 0, h = h0; probe < (uint32_t)kPC; probe++, h = (h + 1) % kPC) {
+      const uint64_t o = (uint64_t)v * kPC + h;
+      const uint64_t k = chans.key(o);
+      if (k == kNone) break;
+      if (k != mk) continue;
       if (chans.first_s(me) < chans.last_s(o) || chans.first_r(me) < chans.last_r(o)) atomicOr(&st->flags, F_NONCANON);
       return;
     }
