@@ -998,13 +998,15 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
             const int sL = __shfl_sync(kFull, hs, L);
             if ((uint32_t)lane < nL) W.cpool[(W.cbase[sL] + lane) & (kCP - 1)] = R[(pL + lane) & kRM].seq;
           }
-          if (tf_pend) {  // first valid instance per (comm slot, type): only until recorded once
+          {  // first valid instance per (comm slot, type): only until recorded once
             const unsigned long long bit = (isC && st == ST_VALID) ? 1ull << (hs * 5 + h.coll()) : 0ull;
             const bool rec = (bit & tf_pend) != 0;
-            if (rec) note_min_smem(&W.tfirst[hs][h.coll()], rb0 + p);
-            const unsigned lo = __reduce_or_sync(kFull, rec ? (unsigned)bit : 0u);
-            const unsigned hi = __reduce_or_sync(kFull, rec ? (unsigned)(bit >> 32) : 0u);
-            tf_pend &= ~(((unsigned long long)hi << 32) | lo);
+            if (CT_UNLIKELY(__any_sync(kFull, rec))) {
+              if (rec) note_min_smem(&W.tfirst[hs][h.coll()], rb0 + p);
+              const unsigned lo = __reduce_or_sync(kFull, rec ? (unsigned)bit : 0u);
+              const unsigned hi = __reduce_or_sync(kFull, rec ? (unsigned)(bit >> 32) : 0u);
+              tf_pend &= ~(((unsigned long long)hi << 32) | lo);
+            }
           }
           __syncwarp();
 
