@@ -4,15 +4,18 @@
 //   * every warp owns a contiguous range of the packed trace, cut at element starts
 //     (a collective rank-0 record, a send, or a copy), and streams it through its own
 //     ring of 1 KB TMA bulk copies (cp.async.bulk + mbarrier, kRing slots deep);
-//   * scan (lane = record, one 32-record chunk at a time): element starts and lengths,
-//     the tiling check (element lengths sum to the range), copies expanded in place,
-//     collective blocks and send/recv pairs appended to a per-warp element queue;
-//   * join (lane = element, up to 32 queued elements at a time): each lane walks its
-//     block's records -- membership, signature (grouping.py:78-79, 132-155), distinct
-//     devices (grouping.py:156-167), per-(comm, rank) seq order against the comm's
-//     previous block (same batch: the ring; else the per-warp table) -- then expands the
-//     valid instance edge by edge (rank-attributed rules, ct_common.cuh) into the CTA's
-//     shared-memory histogram;
+//   * scan (lane = record, one 32-record chunk at a time): element heads appended to a
+//     per-warp element queue, copies expanded in place (one transfer each);
+//   * join (lane = element, up to 32 queued elements, run when the ring is full): each
+//     lane walks its block's records comparing raw words with the head -- membership,
+//     signature (grouping.py:78-79, 132-155), one seq per block or per rank against the
+//     comm's previous block (same batch: the ring; else the per-warp table), distinct
+//     devices (grouping.py:156-167) -- and the element lengths plus copies must tile the
+//     range exactly;
+//   * expansion of valid instances (rank-attributed rules, ct_common.cuh): repeated
+//     uniform-ring instances go to a per-lane register accumulator, repeated ring / tree
+//     / collnet / broadcast / reduce instances to per-warp shared slot accumulators, the
+//     rest edge by edge -- all into the CTA's shared-memory histogram (32-bit limbs);
 //   * each CTA merges its histogram and statistics into global memory once at the end.
 // Seq-order preconditions (exactly when the reference's seq-sorted grouping and FIFO
 // matching coincide with file order, grouping.py:118-131, decompose.py:357-361):
@@ -35,7 +38,7 @@ constexpr int kWarps = kThreads / 32;
 #endif
 constexpr int kRing = CT_RING_SLOTS;  // per-warp TMA ring slots of 32 records (1 KB each)
 constexpr int kCS = 8;          // collective communicator slots per warp
-constexpr int kPC = 64;         // p2p channel table entries per warp
+constexpr int kPC = 64;         // p2p channel table entries per warp (open addressing, global memory)
 constexpr int kMaxN = 32;       // largest communicator the fast path handles
 constexpr int kQ = 64;          // element queue entries per warp
 
