@@ -13,7 +13,7 @@ constexpr uint64_t kNone = ~0ull;
 constexpr uint32_t kEmptyTag = 0xFFFFFFFFu;
 constexpr unsigned kFull = 0xFFFFFFFFu;
 constexpr uint32_t kQM = kQ - 1;
-static_assert((kQ & (kQ - 1)) == 0 && kQ >= 64, "queue holds < 32 carried + 32 new heads");
+static_assert((kQ & (kQ - 1)) == 0 && kQ >= 96, "queue holds <= 32 carried + 2 chunks of new heads");
 
 // Shared-memory accumulator of repeated instances of one (comm slot, class): class 0 ring
 // allreduce (every block but the last full), 1 allgather, 2 reduce-scatter, 3 tree
@@ -780,35 +780,25 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
     uint32_t cnext = 0;             // next free entry of the seq-table pool
     const bool stream_only = (P.dbg & 4) != 0, no_expand = (P.dbg & 1) != 0;
     bool bail = false;
-    uint32_t q = 0;
-    for (; q < lastc && !bail; q++) {
+    uint32_t q = 0, waited = 0;  // next chunk to scan / chunks waited for
+    uint32_t ns = 1;              // chunks scanned this step (two when both are in the ring)
+    for (; q < lastc && !bail; q += ns) {
+      ns = q + 1 < min(freed + (uint32_t)kRing, lastc) ? 2u : 1u;
       mbar_wait(&W.bar[q % kRing], (q / kRing) & 1);
+      if (ns == 2) mbar_wait(&W.bar[(q + 1) % kRing], ((q + 1) / kRing) & 1);
+      waited = q + ns;
+      const uint32_t ql = q + ns - 1;  // last chunk of this step
       if (stream_only) {  // diagnostic: stream only (roofline experiments)
-        const uint32_t rel = q * 32 + lane;
-        if (rel < eo) my_max_dev = max(my_max_dev, (int)(R[rel & kRM].dev ^ R[rel & kRM].rank));
+        for (uint32_t k = 0; k < ns; k++) {
+          const uint32_t rel = (q + k) * 32 + lane;
+          if (rel < eo) my_max_dev = max(my_max_dev, (int)(R[rel & kRM].dev ^ R[rel & kRM].rank));
+        }
       } else {
         // REGION scan
-        // ================= scan (lane = record)
+        // ================= scan (lane = record; two chunks per step: records A and B)
         {
-          const uint32_t rel = q * 32 + lane;
-          const bool act = rel >= s0 && rel < eo;
-          const uint4 b = reinterpret_cast<const uint4*>(R + (rel & kRM))[1];  // any ring slot is readable
-          const int kind = act ? (int)((b.w >> 16) & 7) : 7;
-          const uint32_t nr = b.y & 0xFFFF, rk = b.y >> 16, dev = b.z & 0xFFFF;
-          my_max_dev = max(my_max_dev, act ? (int)dev : -1);
-          const bool isH = (kind == CT_KIND_COLLECTIVE && rk == 0) || kind == CT_KIND_SEND;
-          const bool isCp = (uint32_t)(kind - CT_KIND_MEMCPY) < 3u;
-          const uint32_t len = kind == CT_KIND_COLLECTIVE ? nr : 2u;  // of a head (checked by the join)
-          const unsigned hm = __ballot_sync(kFull, isH);
-          const unsigned cpm = __ballot_sync(kFull, isCp);
-          cover += lane == 0 ? __popc(cpm) : 0;
-          if (isH) W.q[(qt + __popc(hm & lt)) & kQM] = rel;
-          if (qt == qh && hm) u = q;  // the queue's oldest element now starts in this chunk
-          qt += __popc(hm);
-          // only the chunk's last element can extend past it (else the layout is not canonical
-          // and the tiling check fails): it waits for the next scan
-          cross = __any_sync(kFull, isH && rel + len > (q + 1) * 32) ? 1u : 0u;
-          if (isCp) {
+          // a copy: one transfer (decompose.py:397-406) and the first record of its kind
+          auto copy_rec = [&](uint32_t rel, const uint4& b, int kind) {
             const unsigned long long cnt = reinterpret_cast<const unsigned long long*>(R + (rel & kRM))[0];
             const int ck = (int)(b.w >> 30);
             const uint32_t aux = b.z >> 16, aux2 = b.w & 0xFFFF;
@@ -831,7 +821,33 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
               copy_seen |= bit;
               atomicMin(&C.copy_first[t], rb0 + rel);
             }
-          }
+          };
+          const uint32_t relA = q * 32 + lane, relB = relA + 32;
+          const bool actA = relA >= s0 && relA < eo, actB = ns == 2 && relB < eo;
+          const uint4 bA = reinterpret_cast<const uint4*>(R + (relA & kRM))[1];  // any ring slot is readable
+          const uint4 bB = reinterpret_cast<const uint4*>(R + (relB & kRM))[1];
+          const int kindA = actA ? (int)((bA.w >> 16) & 7) : 7, kindB = actB ? (int)((bB.w >> 16) & 7) : 7;
+          my_max_dev = max(my_max_dev, max(actA ? (int)(bA.z & 0xFFFF) : -1, actB ? (int)(bB.z & 0xFFFF) : -1));
+          const bool isHA = (kindA == CT_KIND_COLLECTIVE && (bA.y >> 16) == 0) || kindA == CT_KIND_SEND;
+          const bool isHB = (kindB == CT_KIND_COLLECTIVE && (bB.y >> 16) == 0) || kindB == CT_KIND_SEND;
+          const bool isCpA = (uint32_t)(kindA - CT_KIND_MEMCPY) < 3u, isCpB = (uint32_t)(kindB - CT_KIND_MEMCPY) < 3u;
+          const unsigned hmA = __ballot_sync(kFull, isHA), hmB = __ballot_sync(kFull, isHB);
+          const unsigned cpm = __popc(__ballot_sync(kFull, isCpA)) + __popc(__ballot_sync(kFull, isCpB));
+          cover += lane == 0 ? (int)cpm : 0;
+          const uint32_t nA = __popc(hmA);
+          if (isHA) W.q[(qt + __popc(hmA & lt)) & kQM] = relA;
+          if (isHB) W.q[(qt + nA + __popc(hmB & lt)) & kQM] = relB;
+          if (qt == qh && (hmA | hmB)) u = hmA ? q : q + 1;  // the queue's oldest element starts here
+          qt += nA + __popc(hmB);
+          // only the step's last element can extend past it (else the layout is not canonical
+          // and the tiling check fails): it waits for the next step
+          const bool lastH = ns == 2 ? isHB : isHA;
+          const uint32_t lrel = ns == 2 ? relB : relA;
+          const uint4& lb = ns == 2 ? bB : bA;
+          const uint32_t llen = (ns == 2 ? kindB : kindA) == CT_KIND_COLLECTIVE ? (lb.y & 0xFFFF) : 2u;
+          cross = __any_sync(kFull, lastH && lrel + llen > (ql + 1) * 32) ? 1u : 0u;
+          if (isCpA) copy_rec(relA, bA, kindA);
+          if (isCpB) copy_rec(relB, bB, kindB);
         }
         __syncwarp();
 
@@ -839,7 +855,7 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
         // ================= join + expand (lane = element), in batches of <= 32
         // elements wholly inside chunks <= q are joinable; join when 32 are ready or when
         // the ring is about to be full of unjoined records (the oldest one's chunk u)
-        const bool pressure = q + 1 + kDrainSlack >= u + kRing || q + 1 == lastc;
+        const bool pressure = ql + 1 + kDrainSlack >= u + kRing || ql + 1 == lastc;
         while (qt - qh - cross >= 32 || (pressure && qt - qh - cross > 0)) {
           const uint32_t nb = min(32u, qt - qh - cross);
           const bool act = (uint32_t)lane < nb;
@@ -1037,7 +1053,7 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
 
       // REGION release
       // ---- release chunks no element still needs; their slots refill
-      const uint32_t keep = qt != qh ? u : q + 1;
+      const uint32_t keep = qt != qh ? u : ql + 1;
       if (keep > freed) {
         __syncwarp();
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -1054,7 +1070,7 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
       if (tot != (int)(eo - s0)) wflags |= F_NONCANON;
     }
     const uint32_t issued = min(freed + (uint32_t)kRing, lastc);
-    for (uint32_t c = bail ? q + 1 : q; c < issued; c++)  // drain outstanding bulk copies
+    for (uint32_t c = waited; c < issued; c++)  // drain outstanding bulk copies
       mbar_wait(&W.bar[c % kRing], (c / kRing) & 1);
   }
 

@@ -40,7 +40,7 @@ constexpr int kRing = CT_RING_SLOTS;  // per-warp TMA ring slots of 32 records (
 constexpr int kCS = 8;          // collective communicator slots per warp
 constexpr int kPC = 64;         // p2p channel table entries per warp (open addressing, global memory)
 constexpr int kMaxN = 32;       // largest communicator the fast path handles
-constexpr int kQ = 64;          // element queue entries per warp
+constexpr int kQ = 128;         // element queue entries per warp (< 32 carried + 2 chunks of heads)
 
 struct GlobalState {
   uint32_t flags;
