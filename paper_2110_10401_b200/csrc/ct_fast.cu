@@ -673,11 +673,21 @@ __device__ __forceinline__ void expand_block(const FastParams& P, Sink<SH>& sk, 
           0x80000000u | (uint32_t)slot | (cls << 3) | ((uint32_t)coll << 6) | ((uint32_t)n << 9) | (root << 13);
       SAE& E = sa[e];
       if (E.key == key && E.devs == devs) {
-        limb_add(E.g, tree ? s - s / 2 : (ring && !rooted ? (simple ? gen : fixed) : s));
-        if (tree || simple) limb_add(E.d, tree ? s / 2 : dlt);
-        limb_add(E.s, s);
+        // low limbs and the count first (independent atomics in flight), then the carries
+        const unsigned long long vg = tree ? s - s / 2 : (ring && !rooted ? (simple ? gen : fixed) : s);
+        const unsigned long long vd = tree ? s / 2 : (simple ? dlt : 0ull);
+        const uint32_t og = atomicAdd(&E.g[0], (uint32_t)vg);
+        const uint32_t od = atomicAdd(&E.d[0], (uint32_t)vd);
+        const uint32_t os = atomicAdd(&E.s[0], (uint32_t)s);
+        const uint32_t oc = atomicAdd(&E.cnt, 1u);
         if (tree && s / 2 != 0) atomicAdd(&E.cnt2, 1u);
-        if (atomicAdd(&E.cnt, 1u) + 1 == P.sa_flush) { sq.e = e; sq.key = 0; sq.act = true; }  // write out after the batch
+        const uint32_t hg = (uint32_t)(vg >> 32) + (og + (uint32_t)vg < og ? 1u : 0u);
+        const uint32_t hd = (uint32_t)(vd >> 32) + (od + (uint32_t)vd < od ? 1u : 0u);
+        const uint32_t hs = (uint32_t)(s >> 32) + (os + (uint32_t)s < os ? 1u : 0u);
+        if (hg) atomicAdd(&E.g[1], hg);
+        if (hd) atomicAdd(&E.d[1], hd);
+        if (hs) atomicAdd(&E.s[1], hs);
+        if (oc + 1 == P.sa_flush) { sq.e = e; sq.key = 0; sq.act = true; }  // write out after the batch
         return;
       }
       sq.e = e; sq.key = key; sq.act = true;  // re-key after the batch; this instance is expanded now
