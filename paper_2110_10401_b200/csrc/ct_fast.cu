@@ -370,6 +370,16 @@ struct RingAcc {
   }
 };
 
+// a copy transfer with an endpoint outside the table or >= 2^63 bytes
+template <bool SH>
+__device__ __noinline__ uint32_t copy_edge_slow(const FastParams& P, unsigned long long gidx, int type, int src, int dst,
+                                                unsigned long long cnt) {
+  Sink<SH> sk(P);
+  sk.rec_key = (2ull << 62) | (min(gidx, (1ull << 41) - 1) << 21);
+  sk.edge(type, src, dst, (unsigned __int128)cnt);
+  return sk.flags;
+}
+
 // device of a record held in the warp's ring, by ring-relative position
 struct WinDev {
   const ct_record* R;
@@ -820,9 +830,8 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
               if (src < P.gcap && dst < P.gcap && (cnt >> 63) == 0) {
                 const int a = src < 0 ? kHost : src + 2, bb = dst < 0 ? kHost : dst + 2;
                 sk.add((uint32_t)(((CT_T_EXPLICIT + t) * P.g2 + a) * P.g2 + bb), cnt);
-              } else {
-                sk.rec_key = (2ull << 62) | (min((unsigned long long)(rb0 + rel), (1ull << 41) - 1) << 21);
-                sk.edge(CT_T_EXPLICIT + t, src, dst, (unsigned __int128)cnt);
+              } else {  // an endpoint outside the table or >= 2^63 bytes (out of line)
+                sk.flags |= copy_edge_slow<SH>(P, rb0 + rel, CT_T_EXPLICIT + t, src, dst, cnt);
               }
             }
             // first record of each copy kind: positions only grow, so a lane's first is its min
