@@ -397,6 +397,26 @@ __device__ __noinline__ uint32_t expand_wide(const FastParams& P, const ct_recor
   return sk.flags;
 }
 
+// allocate comm slots for the lanes whose comm is new to this range (warp-collective, one
+// comm at a time); -2: more comms than slots in one range
+__device__ __noinline__ int alloc_slots(WarpMem& W, bool need, uint32_t comm, int slot, int lane) {
+  bool full = false;
+  while (true) {
+    const unsigned miss = __ballot_sync(kFull, need && slot < 0);
+    if (!miss) break;
+    const uint32_t cm = __shfl_sync(kFull, comm, __ffs(miss) - 1);
+    int free_s = -1;
+    for (int s = kCS - 1; s >= 0; s--)
+      if (W.tag[s] == kEmptyTag) free_s = s;
+    __syncwarp();
+    if (free_s < 0) { full = true; break; }
+    if (lane == 0) W.tag[free_s] = cm;
+    __syncwarp();
+    if (need && slot < 0 && comm == cm) slot = free_s;
+  }
+  return full && need && slot < 0 ? -2 : slot;
+}
+
 __device__ __forceinline__ int find_slot(const WarpMem& W, uint32_t comm) {
   int s = -1;
 #pragma unroll
@@ -890,18 +910,9 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
             if (h.comm >= P.n_comms) { wflags |= F_COMM_RANGE; bad = true; }
             slot = h.comm == sc_comm ? sc_slot : find_slot(W, h.comm);
           }
-          while (true) {  // allocate slots for unseen comms (rare, warp-serial)
-            const unsigned miss = __ballot_sync(kFull, isC && slot < 0);
-            if (CT_LIKELY(!miss)) break;
-            const uint32_t cm = __shfl_sync(kFull, h.comm, __ffs(miss) - 1);
-            int free_s = -1;
-            for (int s = kCS - 1; s >= 0; s--)
-              if (W.tag[s] == kEmptyTag) free_s = s;
-            __syncwarp();
-            if (free_s < 0) { bad = true; break; }  // more comms than slots in one range
-            if (lane == 0) W.tag[free_s] = cm;
-            __syncwarp();
-            if (isC && slot < 0 && h.comm == cm) slot = free_s;
+          if (CT_UNLIKELY(__any_sync(kFull, isC && slot < 0))) {  // unseen comms (rare)
+            slot = alloc_slots(W, isC && slot < 0, h.comm, slot, lane);
+            if (slot == -2) { bad = true; slot = -1; }
           }
           if (isC) { sc_comm = h.comm; sc_slot = slot; }
           const int hs = slot < 0 ? 0 : slot;
