@@ -726,7 +726,7 @@ __device__ __forceinline__ void expand_block(const FastParams& P, Sink<SH>& sk, 
   sk.flags |= expand_direct<SH>(P, R, h, p, gidx, j0, fastdev, packed, devs, algo);
 }
 
-__device__ __forceinline__ void count_diag(uint32_t st) {
+__device__ __noinline__ void count_diag(uint32_t st) {
   if (st == ST_INCOMPAT) atomicAdd(&cta_mem().diag[CT_DIAG_INCOMPATIBLE], 1u);
   else if (st == ST_DUPDEV) atomicAdd(&cta_mem().diag[CT_DIAG_DUPLICATE_DEVICE], 1u);
   else if (st == ST_MISMATCH) atomicAdd(&cta_mem().diag[CT_DIAG_MISMATCHED_P2P], 1u);
