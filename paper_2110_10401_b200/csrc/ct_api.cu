@@ -218,11 +218,13 @@ int summarize_state(ct_context* c, const GlobalState& gs, int gcap, int64_t d, i
   out->diag[CT_DIAG_INCOMPLETE] += extra_diag[0];
   out->diag[CT_DIAG_UNMATCHED_SEND] += extra_diag[1];
   out->diag[CT_DIAG_UNMATCHED_RECV] += extra_diag[2];
+  std::vector<unsigned long long> h(2 * ncell);  // cells (bytes, then frequencies)
   // per_primitive dict order (matrix.py:334-335): collectives by (comm first-seen,
   // first valid instance), then sendrecv, then copies by first event
   {
     std::vector<unsigned long long> tcf(6 * (size_t)n_comms);
     CTX_TRY(c, cudaMemcpyAsync(tcf.data(), c->tcf, tcf.size() * 8, cudaMemcpyDeviceToHost, st));
+    CTX_TRY(c, cudaMemcpyAsync(h.data(), c->cells, 2 * ncell * 8, cudaMemcpyDeviceToHost, st));  // one sync for both
     CTX_TRY(c, cudaStreamSynchronize(st));
     const unsigned long long* cf = tcf.data() + 5 * (size_t)n_comms;
     std::vector<std::pair<std::pair<uint64_t, uint64_t>, int>> order;
@@ -246,9 +248,6 @@ int summarize_state(ct_context* c, const GlobalState& gs, int gcap, int64_t d, i
       out->type_first[CT_T_EXPLICIT + copies[k].second] = copies[k].first == ~0ull ? ~0ull : (uint64_t)(6 + k);
   }
   // cells, net flags, combined 63-bit bound (matrix.py:110-113)
-  std::vector<unsigned long long> h(2 * ncell);
-  CTX_TRY(c, cudaMemcpyAsync(h.data(), c->cells, 2 * ncell * 8, cudaMemcpyDeviceToHost, st));
-  CTX_TRY(c, cudaStreamSynchronize(st));
   // copy statistics: every copy adds exactly one transfer of its byte count to its type
   // (decompose.py:397-406), so calls / payload are the plane's frequency / byte sums
   // (the fast kernel does not count them separately)
