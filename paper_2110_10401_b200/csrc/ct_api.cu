@@ -748,13 +748,25 @@ __global__ void __launch_bounds__(1024) k_shard_export(const WarpSlot* slots, co
     atomicMin(&cmin[h], i);
     atomicMax(&cmax[h], i);
   }
-  for (uint32_t i = tid; i < nq; i += blockDim.x) {
-    const unsigned long long key = chans.key(i);
-    if (key == ~0ull) continue;
-    const int h = insert(hkey, TH, key);
-    if (h < 0) { ovf = 1; continue; }
-    atomicMin(&hmin[h], i);
-    atomicMax(&hmax[h], i);
+  // channel keys are contiguous: each thread takes 4 adjacent keys per step (two 16-byte
+  // loads in flight) so the scan is not one dependent load per iteration
+  for (uint32_t i0 = 4 * tid; i0 < nq; i0 += 4 * blockDim.x) {
+    unsigned long long k4[4];
+    if (i0 + 4 <= nq) {
+      const ulonglong2 a = *reinterpret_cast<const ulonglong2*>(&chans.key(i0));
+      const ulonglong2 b = *reinterpret_cast<const ulonglong2*>(&chans.key(i0 + 2));
+      k4[0] = a.x; k4[1] = a.y; k4[2] = b.x; k4[3] = b.y;
+    } else {
+      for (int k = 0; k < 4; k++) k4[k] = i0 + k < nq ? chans.key(i0 + k) : ~0ull;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      if (k4[k] == ~0ull) continue;
+      const int h = insert(hkey, TH, k4[k]);
+      if (h < 0) { ovf = 1; continue; }
+      atomicMin(&hmin[h], i0 + k);
+      atomicMax(&hmax[h], i0 + k);
+    }
   }
   __syncthreads();
   // compact into the export lists (any order: the merge matches entries by key)
