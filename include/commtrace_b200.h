@@ -188,6 +188,42 @@ int ct_partial_export(ct_context *ctx, uint64_t *dev_out, uint64_t words, void *
 int ct_partial_merge(ct_context *ctx, const uint64_t *dev_in, int world, uint64_t words,
                      ct_summary *out, void *stream);
 
+/* ---------------------------------------------------------------- JSONL loader
+ * Device loader for the reference wire format, replacing
+ *   parse_trace(source)            pkg/src/commtrace/events.py:352-384
+ * (field readers events.py:294-349, TraceEvent.validate events.py:166-236) plus the
+ * packing of the events into ct_record (comm ids in first-seen order).  Lines follow
+ * str.splitlines(); blank lines are skipped.  A line the device cannot prove the
+ * reference accepts unchanged (non-ASCII, escapes, floats/bools/null/huge ints in
+ * consulted keys, grammar or validation failures) is "deferred": its record slot is
+ * zero and the caller must parse that line with the reference reader, which raises
+ * the reference's error for the first bad line (device-accepted lines never raise).
+ * A deferred line that turns out blank must be dropped by the caller. */
+typedef struct ct_jsonl ct_jsonl;
+typedef struct ct_jsonl_info {
+  uint64_t n_lines;     /* lines per str.splitlines()                               */
+  uint64_t n_records;   /* non-blank lines = record slots (deferred ones included)   */
+  uint64_t n_deferred;  /* lines left to the caller (ct_jsonl_deferred)              */
+  uint64_t n_comms;     /* distinct comm names among device-parsed lines            */
+  uint64_t comm_bytes;  /* total bytes of those names                               */
+  uint32_t non_ascii;   /* 1: the text holds bytes >= 0x80 (UTF-8 check is the caller's) */
+  float ms_device;      /* device time of the parse (CUDA events)                   */
+} ct_jsonl_info;
+/* Parse ``size`` bytes (host or device memory).  *out is always set (free it with
+ * ct_jsonl_free, also on error; message via ct_jsonl_error). */
+int ct_jsonl_parse(int device, const char *text, uint64_t size, int on_device, ct_jsonl **out,
+                   ct_jsonl_info *info);
+/* n_records records to device memory (comm ids final for device lines); optional
+ * n_records int64 timestamps to host memory. */
+int ct_jsonl_records(ct_jsonl *j, ct_record *dev_out, int64_t *host_ts);
+/* n_deferred rows of 4 uint64: {1-based line number, record slot, byte offset, byte length}. */
+int ct_jsonl_deferred(ct_jsonl *j, uint64_t *rows);
+/* n_comms rows of 3 uint64 {first record slot, offset into names, length} in comm-id
+ * order, and comm_bytes of names. */
+int ct_jsonl_comms(ct_jsonl *j, uint64_t *rows, char *names);
+const char *ct_jsonl_error(const ct_jsonl *j);
+void ct_jsonl_free(ct_jsonl *j);
+
 #ifdef __cplusplus
 }
 #endif

@@ -96,7 +96,28 @@ _SIGNATURES = {
     "ct_partial_export": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]),
     "ct_partial_merge": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_uint64, C.POINTER(CtSummary),
                                    C.c_void_p]),
+    "ct_jsonl_parse": (C.c_int, [C.c_int, C.c_void_p, C.c_uint64, C.c_int, C.POINTER(C.c_void_p),
+                                 C.c_void_p]),
+    "ct_jsonl_records": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "ct_jsonl_deferred": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "ct_jsonl_comms": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "ct_jsonl_error": (C.c_char_p, [C.c_void_p]),
+    "ct_jsonl_free": (None, [C.c_void_p]),
 }
+
+
+class CtJsonlInfo(C.Structure):
+    """ct_jsonl_info (include/commtrace_b200.h)."""
+
+    _fields_ = [
+        ("n_lines", C.c_uint64),
+        ("n_records", C.c_uint64),
+        ("n_deferred", C.c_uint64),
+        ("n_comms", C.c_uint64),
+        ("comm_bytes", C.c_uint64),
+        ("non_ascii", C.c_uint32),
+        ("ms_device", C.c_float),
+    ]
 
 
 def load():

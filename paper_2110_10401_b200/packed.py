@@ -116,8 +116,10 @@ class PackedTrace:
         """The TraceEvent for record ``i`` (original object when available)."""
         if self.events is not None:
             return self.events[i]
-        return unpack_record(self.records[i], self.comms,
-                             0 if self.ts is None else self.ts[i])
+        rec = self.records[i]
+        if not isinstance(rec, np.void):  # device records (torch tensor rows)
+            rec = np.frombuffer(rec.cpu().numpy().tobytes(), dtype=RECORD_DTYPE)[0]
+        return unpack_record(rec, self.comms, 0 if self.ts is None else self.ts[i])
 
 
 def _check_range(val: int, hi: int, what: str) -> int:
