@@ -4,7 +4,8 @@
 // events.py:294-349, validate events.py:166-236) followed by the record packing of
 // packed.pack_events.  Three phases, all on the device:
 //   1. line breaks: every byte position that starts a str.splitlines() terminator
-//      (\n, \r, \r\n, \v, \f, \x1c-\x1e, U+0085, U+2028, U+2029) -> ordered list
+//      (\n, \r, \r\n, \v, \f, \x1c-\x1e, U+0085, U+2028, U+2029) -> ordered list;
+//      16 bytes per thread, per-tile counts, a scan, then in-order writes
 //   2. one thread per line: JSON grammar, the reference's key/type reading order and
 //      TraceEvent.validate rules, packed-range checks -> record + ts, or "blank", or
 //      "deferred"
@@ -35,23 +36,108 @@ enum : uint8_t { L_BLANK = 0, L_OK = 1, L_DEFER = 2 };
 
 // ---------------------------------------------------------------- phase 1: breaks
 
-struct BreakPred {
-  const uint8_t* s;
-  uint64_t n;
-  __device__ __forceinline__ bool operator()(uint64_t i) const {
-    const uint8_t b = s[i];
-    if (b == '\n') return i == 0 || s[i - 1] != '\r';  // \r\n is one terminator
-    if (b == '\r' || b == 0x0b || b == 0x0c || b == 0x1c || b == 0x1d || b == 0x1e) return true;
-    if (b == 0xC2) return i + 1 < n && s[i + 1] == 0x85;
-    if (b == 0xE2) return i + 2 < n && s[i + 1] == 0x80 && (s[i + 2] == 0xA8 || s[i + 2] == 0xA9);
-    return false;
-  }
-};
+// 16 bytes at i0 (i0 % 16 == 0): bit j set iff a terminator starts at i0 + j; non-ASCII
+// bytes noted.  Neighbour bytes outside the 16 are read only for the rare cases.
+constexpr int kTileThreads = 256;
+constexpr int kTileReps = 1;  // 16-byte chunks per thread (4 measured slower)
+constexpr uint64_t kChunkRow = kTileThreads * 16;
+constexpr uint64_t kTileBytes = kChunkRow * kTileReps;
 
-struct BreakCount {
-  BreakPred p;
-  __device__ __forceinline__ uint64_t operator()(uint64_t i) const { return p(i) ? 1u : 0u; }
-};
+__device__ __forceinline__ uint4 load16(const uint8_t* s, uint64_t n, uint64_t i0, bool aligned) {
+  if (aligned && i0 + 16 <= n) return *reinterpret_cast<const uint4*>(s + i0);
+  return make_uint4(0, 0, 0, 0);  // handled bytewise in break_mask16
+}
+
+// 16 bytes at i0 (i0 % 16 == 0, pre-loaded in v when aligned and in range): bit j set
+// iff a terminator starts at i0 + j; non-ASCII bytes noted.  Neighbour bytes outside
+// the 16 are read only for the rare cases.
+__device__ __forceinline__ uint32_t break_mask16(const uint8_t* s, uint64_t n, uint64_t i0, bool aligned,
+                                                 const uint4 v, bool& non_ascii) {
+  non_ascii = false;
+  if (i0 >= n) return 0;
+  uint8_t b[16];
+  if (aligned && i0 + 16 <= n) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    // candidates are bytes < 0x20 or >= 0x80: most 16-byte chunks have none
+    uint32_t any = 0;
+#pragma unroll
+    for (int q = 0; q < 4; q++) any |= ((w[q] - 0x20202020u) & ~w[q]) | w[q];
+    if (!(any & 0x80808080u)) return 0;
+#pragma unroll
+    for (int j = 0; j < 16; j++) b[j] = (uint8_t)(w[j >> 2] >> (8 * (j & 3)));
+  } else {
+#pragma unroll
+    for (int j = 0; j < 16; j++) b[j] = i0 + j < n ? s[i0 + j] : (uint8_t)'x';
+  }
+  uint32_t m = 0;
+  bool hi = false;
+#pragma unroll
+  for (int j = 0; j < 16; j++) {
+    const uint8_t c = b[j];
+    hi |= c >= 0x80;
+    if (c < 0x20 || c >= 0xC2) {  // candidates only
+      const uint64_t i = i0 + j;
+      if (i >= n) continue;
+      bool brk;
+      if (c == '\n') brk = j > 0 ? b[j - 1] != '\r' : (i == 0 || s[i - 1] != '\r');
+      else if (c == '\r' || c == 0x0b || c == 0x0c || c == 0x1c || c == 0x1d || c == 0x1e) brk = true;
+      else if (c == 0xC2) brk = i + 1 < n && (j + 1 < 16 ? b[j + 1] : s[i + 1]) == 0x85;
+      else if (c == 0xE2) brk = i + 2 < n && (j + 1 < 16 ? b[j + 1] : s[i + 1]) == 0x80 &&
+                                ((j + 2 < 16 ? b[j + 2] : s[i + 2]) == 0xA8 || (j + 2 < 16 ? b[j + 2] : s[i + 2]) == 0xA9);
+      else brk = false;
+      if (brk) m |= 1u << j;
+    }
+  }
+  non_ascii = hi;
+  return m;
+}
+
+__global__ void __launch_bounds__(kTileThreads) k_brk_count(const uint8_t* s, uint64_t n, bool aligned,
+                                                            uint32_t* tile_cnt, unsigned int* flags) {
+  using BR = cub::BlockReduce<uint32_t, kTileThreads>;
+  __shared__ typename BR::TempStorage tmp;
+  const uint64_t base = blockIdx.x * kTileBytes + threadIdx.x * 16ull;
+  uint4 v[kTileReps];
+#pragma unroll
+  for (int r = 0; r < kTileReps; r++) v[r] = load16(s, n, base + r * kChunkRow, aligned);
+  uint32_t c = 0;
+  bool hi = false;
+#pragma unroll
+  for (int r = 0; r < kTileReps; r++) {
+    bool h;
+    c += __popc(break_mask16(s, n, base + r * kChunkRow, aligned, v[r], h));
+    hi |= h;
+  }
+  if (__any_sync(0xffffffffu, hi) && (threadIdx.x & 31) == 0) atomicOr(flags + 1, 1u);
+  const uint32_t tot = BR(tmp).Sum(c);
+  if (threadIdx.x == 0) tile_cnt[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(kTileThreads) k_brk_write(const uint8_t* s, uint64_t n, bool aligned,
+                                                            const uint64_t* tile_off, uint64_t* brk) {
+  using BS = cub::BlockScan<uint32_t, kTileThreads>;
+  __shared__ typename BS::TempStorage tmp;
+  const uint64_t base = blockIdx.x * kTileBytes + threadIdx.x * 16ull;
+  uint4 v[kTileReps];
+#pragma unroll
+  for (int r = 0; r < kTileReps; r++) v[r] = load16(s, n, base + r * kChunkRow, aligned);
+  uint64_t o0 = tile_off[blockIdx.x];
+#pragma unroll
+  for (int r = 0; r < kTileReps; r++) {  // rows of chunks in text order
+    bool h;
+    uint32_t m = break_mask16(s, n, base + r * kChunkRow, aligned, v[r], h);
+    uint32_t before, total;
+    BS(tmp).ExclusiveSum((uint32_t)__popc(m), before, total);
+    __syncthreads();
+    uint64_t o = o0 + before;
+    while (m) {
+      const int j = __ffs(m) - 1;
+      m &= m - 1;
+      brk[o++] = base + r * kChunkRow + j;
+    }
+    o0 += total;
+  }
+}
 
 __device__ __forceinline__ uint64_t break_len(const uint8_t* s, uint64_t n, uint64_t i) {
   const uint8_t b = s[i];
@@ -63,33 +149,100 @@ __device__ __forceinline__ uint64_t break_len(const uint8_t* s, uint64_t n, uint
 
 // ---------------------------------------------------------------- phase 2: parse
 
+// Strings are compared as (length, first 16 bytes packed little-endian): every name the
+// reader knows is <= 13 bytes, so two 64-bit compares against immediates decide it.
+constexpr uint64_t pk8(const char* str, int off) {
+  uint64_t v = 0;
+  int n = 0;
+  while (str[n]) n++;
+  for (int i = 0; i < 8 && off + i < n; i++) v |= (uint64_t)(uint8_t)str[off + i] << (8 * i);
+  return v;
+}
+constexpr uint32_t slen(const char* str) { return str[0] ? 1 + slen(str + 1) : 0; }
+
+struct Str {
+  uint32_t len;
+  uint64_t w0, w1;
+};
+
+#define CT_IS(x, lit) ((x).len == slen(lit) && (x).w0 == pk8(lit, 0) && (x).w1 == pk8(lit, 8))
+
 // top-level keys the reader consults (events.py:294-349)
 enum Key : int { K_SEQ, K_TS, K_KIND, K_COMM, K_NRANKS, K_RANK, K_DEV, K_COLL, K_ALGO, K_COUNT,
                  K_DTYPE, K_ROOT, K_PEER, K_CKIND, K_SRC, K_DST, K_BYTES, K_N };
 
-__constant__ char kKeyNames[K_N][8] = {"seq", "ts", "kind", "comm", "nranks", "rank", "dev", "coll",
-                                       "algo", "count", "dtype", "root", "peer", "ckind", "src",
-                                       "dst", "bytes"};
-__constant__ char kKinds[6][12] = {"collective", "send", "recv", "memcpy", "um", "zerocopy"};
-__constant__ char kColls[5][14] = {"allreduce", "broadcast", "reduce", "reducescatter", "allgather"};
-__constant__ char kAlgos[4][8] = {"ring", "tree", "collnet", "auto"};
-__constant__ char kDtypes[10][9] = {"int8", "uint8", "int32", "uint32", "int64", "uint64",
-                                    "float16", "bfloat16", "float32", "float64"};
-__constant__ char kCkinds[3][4] = {"h2d", "d2h", "d2d"};
-__constant__ char kEpKinds[3][5] = {"host", "gpu", "net"};
+__device__ __forceinline__ int key_of(const Str& k) {
+  if (k.len > 6) return -1;
+  if (CT_IS(k, "seq")) return K_SEQ;
+  if (CT_IS(k, "ts")) return K_TS;
+  if (CT_IS(k, "kind")) return K_KIND;
+  if (CT_IS(k, "comm")) return K_COMM;
+  if (CT_IS(k, "nranks")) return K_NRANKS;
+  if (CT_IS(k, "rank")) return K_RANK;
+  if (CT_IS(k, "dev")) return K_DEV;
+  if (CT_IS(k, "coll")) return K_COLL;
+  if (CT_IS(k, "algo")) return K_ALGO;
+  if (CT_IS(k, "count")) return K_COUNT;
+  if (CT_IS(k, "dtype")) return K_DTYPE;
+  if (CT_IS(k, "root")) return K_ROOT;
+  if (CT_IS(k, "peer")) return K_PEER;
+  if (CT_IS(k, "ckind")) return K_CKIND;
+  if (CT_IS(k, "src")) return K_SRC;
+  if (CT_IS(k, "dst")) return K_DST;
+  if (CT_IS(k, "bytes")) return K_BYTES;
+  return -1;
+}
 
-// value types: absent, int >= 0 (fits u64), int < 0 (fits i64), plain string, endpoint
-// object, anything else (float, bool, null, array, other object, huge int)
-enum : uint8_t { V_NONE = 0, V_UINT, V_NINT, V_STR, V_EP, V_OTHER };
+// enum codes (packed.py KIND_CODE / COLL_CODE / ALGO_CODE / DTYPE_CODE / CKIND_CODE)
+__device__ __forceinline__ int enum_of(int key, const Str& v) {
+  switch (key) {
+    case K_KIND:
+      if (CT_IS(v, "collective")) return 0;
+      if (CT_IS(v, "send")) return 1;
+      if (CT_IS(v, "recv")) return 2;
+      if (CT_IS(v, "memcpy")) return 3;
+      if (CT_IS(v, "um")) return 4;
+      if (CT_IS(v, "zerocopy")) return 5;
+      return -1;
+    case K_COLL:
+      if (CT_IS(v, "allreduce")) return 0;
+      if (CT_IS(v, "broadcast")) return 1;
+      if (CT_IS(v, "reduce")) return 2;
+      if (CT_IS(v, "reducescatter")) return 3;
+      if (CT_IS(v, "allgather")) return 4;
+      return -1;
+    case K_ALGO:
+      if (CT_IS(v, "ring")) return 0;
+      if (CT_IS(v, "tree")) return 1;
+      if (CT_IS(v, "collnet")) return 2;
+      if (CT_IS(v, "auto")) return 3;
+      return -1;
+    case K_DTYPE:
+      if (CT_IS(v, "float32")) return 8;
+      if (CT_IS(v, "bfloat16")) return 7;
+      if (CT_IS(v, "float16")) return 6;
+      if (CT_IS(v, "int8")) return 0;
+      if (CT_IS(v, "uint8")) return 1;
+      if (CT_IS(v, "int32")) return 2;
+      if (CT_IS(v, "uint32")) return 3;
+      if (CT_IS(v, "int64")) return 4;
+      if (CT_IS(v, "uint64")) return 5;
+      if (CT_IS(v, "float64")) return 9;
+      return -1;
+    case K_CKIND:
+      if (CT_IS(v, "h2d")) return 0;
+      if (CT_IS(v, "d2h")) return 1;
+      if (CT_IS(v, "d2d")) return 2;
+      return -1;
+    default:
+      return -1;
+  }
+}
 
-struct Val {
-  uint8_t t;
-  uint64_t u;        // V_UINT value / V_NINT two's complement
-  uint32_t off, len;  // V_STR
-  // V_EP: endpoint kind code (-1 invalid / absent) and index (-1 invalid / absent)
-  int ep_kind;
-  int64_t ep_idx;
-};
+// value types: absent, int >= 0 (fits u64), int < 0 (fits i64), enum code, comm name,
+// endpoint object, anything else (float, bool, null, array, other object, other
+// string, huge int)
+enum : uint8_t { V_NONE = 0, V_UINT, V_NINT, V_ENUM, V_NAME, V_EP, V_OTHER };
 
 __device__ __forceinline__ bool is_ws(uint8_t c) { return c == ' ' || c == '\t'; }
 
@@ -98,14 +251,27 @@ __device__ __forceinline__ uint64_t skip_ws(const uint8_t* s, uint64_t p, uint64
   return p;
 }
 
-template <int N, int W>
-__device__ __forceinline__ int match(const uint8_t* s, uint32_t off, uint32_t len, const char (&tab)[N][W]) {
-  for (int k = 0; k < N; k++) {
-    uint32_t j = 0;
-    while (j < len && j < (uint32_t)W && tab[k][j] != 0 && (uint8_t)tab[k][j] == s[off + j]) j++;
-    if (j == len && (j == (uint32_t)W || tab[k][j] == 0)) return k;
+// string body after the opening quote, packing its first 16 bytes: position after the
+// closing quote, or 0 on failure (the line holds no backslash / control / non-ASCII
+// byte; a raw tab is invalid in a strict JSON string)
+__device__ __forceinline__ uint64_t scan_str(const uint8_t* s, uint64_t p, uint64_t e, Str& out) {
+  const uint64_t p0 = p;
+  uint64_t w0 = 0, w1 = 0;
+  while (p < e) {
+    const uint8_t c = s[p];
+    if (c == '"') {
+      out.len = (uint32_t)(p - p0);
+      out.w0 = w0;
+      out.w1 = w1;
+      return p + 1;
+    }
+    if (c == '\t') return 0;
+    const uint64_t i = p - p0;
+    if (i < 8) w0 |= (uint64_t)c << (8 * i);
+    else if (i < 16) w1 |= (uint64_t)c << (8 * (i - 8));
+    p++;
   }
-  return -1;
+  return 0;
 }
 
 // string body after the opening quote (the line holds no backslash / control byte /
@@ -217,15 +383,24 @@ after:
   return 0;
 }
 
-// A value of a consulted key: scalar types recorded, anything else skipped as V_OTHER.
-__device__ uint64_t read_value(const uint8_t* s, uint64_t p, uint64_t e, Val& v) {
+// A value of a consulted key -> (type, payload): ints as values, enum strings as codes,
+// the comm name as (offset | length << 40), anything else skipped as V_OTHER.
+__device__ uint64_t read_value(const uint8_t* s, uint64_t p, uint64_t e, int key, uint8_t& t, uint64_t& v) {
   p = skip_ws(s, p, e);
   if (p >= e) return 0;
   const uint8_t c = s[p];
   if (c == '"') {
-    const uint64_t q = skip_string(s, p + 1, e);
+    Str x;
+    const uint64_t q = scan_str(s, p + 1, e, x);
     if (!q) return 0;
-    v.t = V_STR; v.off = (uint32_t)(p + 1); v.len = (uint32_t)(q - p - 2);
+    if (key == K_COMM) {
+      t = V_NAME;
+      v = (p + 1) | ((uint64_t)x.len << 40);
+    } else {
+      const int code = enum_of(key, x);
+      t = code >= 0 ? V_ENUM : V_OTHER;
+      v = (uint64_t)code;
+    }
     return q;
   }
   if (c == '-' || (c >= '0' && c <= '9')) {
@@ -233,52 +408,60 @@ __device__ uint64_t read_value(const uint8_t* s, uint64_t p, uint64_t e, Val& v)
     uint64_t mag;
     const uint64_t q = scan_number(s, p, e, is_int, mag, neg, fits);
     if (!q) return 0;
-    if (!is_int || !fits) v.t = V_OTHER;
-    else if (!neg || mag == 0) { v.t = V_UINT; v.u = mag; }      // "-0" is the int 0
-    else if (mag <= (1ull << 63)) { v.t = V_NINT; v.u = 0ull - mag; }
-    else v.t = V_OTHER;
+    if (!is_int || !fits) t = V_OTHER;
+    else if (!neg || mag == 0) { t = V_UINT; v = mag; }      // "-0" is the int 0
+    else if (mag <= (1ull << 63)) { t = V_NINT; v = 0ull - mag; }
+    else t = V_OTHER;
     return q;
   }
-  v.t = V_OTHER;
+  t = V_OTHER;
   return skip_value(s, p, e);
 }
 
-// Endpoint object {"kind": <str>, "idx": <int>} (events.py:271-284); other members
-// are grammar-checked and ignored; duplicate keys: last wins (json.loads).
-__device__ uint64_t read_endpoint(const uint8_t* s, uint64_t p, uint64_t e, Val& v) {
+// Endpoint object {"kind": <str>, "idx": <int>} (events.py:271-284) -> V_EP with
+// payload kind code (host 0, gpu 1, net 2; 0xFF absent/invalid) | idx << 8 (idx
+// 0xFFFFFFFF absent/invalid/too large); other members grammar-checked and ignored;
+// duplicate keys: last wins (json.loads).
+__device__ uint64_t read_endpoint(const uint8_t* s, uint64_t p, uint64_t e, uint8_t& t, uint64_t& v) {
   p = skip_ws(s, p, e);
   if (p >= e) return 0;
-  if (s[p] != '{') { v.t = V_OTHER; return skip_value(s, p, e); }
-  v.t = V_EP; v.ep_kind = -2; v.ep_idx = -2;  // -2: absent, -1: wrong type / value
+  if (s[p] != '{') { t = V_OTHER; return skip_value(s, p, e); }
+  uint32_t kind = 0xFF, idx = 0xFFFFFFFFu;
   p = skip_ws(s, p + 1, e);
-  if (p < e && s[p] == '}') return p + 1;
+  if (p < e && s[p] == '}') { t = V_EP; v = kind | ((uint64_t)idx << 8); return p + 1; }
   while (true) {
     p = skip_ws(s, p, e);
     if (p >= e || s[p] != '"') return 0;
-    const uint64_t k0 = p + 1;
-    p = skip_string(s, k0, e);
+    Str k;
+    p = scan_str(s, p + 1, e, k);
     if (!p) return 0;
-    const uint32_t klen = (uint32_t)(p - k0 - 1);
     p = skip_ws(s, p, e);
     if (p >= e || s[p] != ':') return 0;
     p++;
-    const bool is_kind = klen == 4 && s[k0] == 'k' && s[k0 + 1] == 'i' && s[k0 + 2] == 'n' && s[k0 + 3] == 'd';
-    const bool is_idx = klen == 3 && s[k0] == 'i' && s[k0 + 1] == 'd' && s[k0 + 2] == 'x';
-    if (is_kind || is_idx) {
-      Val w;
-      w.t = V_NONE;
-      p = read_value(s, p, e, w);
-      if (!p) return 0;
-      if (is_kind) v.ep_kind = w.t == V_STR ? match(s, w.off, w.len, kEpKinds) : -1;
-      else v.ep_idx = w.t == V_UINT && w.u < (1ull << 62) ? (int64_t)w.u : -1;
+    if (CT_IS(k, "kind")) {
+      p = skip_ws(s, p, e);
+      if (p < e && s[p] == '"') {
+        Str x;
+        p = scan_str(s, p + 1, e, x);
+        if (!p) return 0;
+        kind = CT_IS(x, "host") ? 0 : CT_IS(x, "gpu") ? 1 : CT_IS(x, "net") ? 2 : 0xFF;
+      } else {
+        p = skip_value(s, p, e);
+        kind = 0xFF;
+      }
+    } else if (CT_IS(k, "idx")) {
+      uint8_t wt = V_NONE;
+      uint64_t wv = 0;
+      p = read_value(s, p, e, -1, wt, wv);
+      idx = wt == V_UINT && wv <= 0xFFFF ? (uint32_t)wv : 0xFFFFFFFFu;
     } else {
       p = skip_value(s, p, e);
-      if (!p) return 0;
     }
+    if (!p) return 0;
     p = skip_ws(s, p, e);
     if (p >= e) return 0;
     if (s[p] == ',') { p++; continue; }
-    if (s[p] == '}') return p + 1;
+    if (s[p] == '}') { t = V_EP; v = kind | ((uint64_t)idx << 8); return p + 1; }
     return 0;
   }
 }
@@ -287,25 +470,59 @@ struct LineOut {
   ct_record r;
   int64_t ts;
   uint64_t hash;
-  uint32_t comm_off, comm_len;
+  uint64_t comm;  // name offset | length << 40
 };
 
-// Parse line [b, e) of s; L_OK with `o` filled, L_BLANK, or L_DEFER.
-__device__ uint8_t parse_line(const uint8_t* s, uint64_t b, uint64_t e, LineOut& o) {
-  // blank per str.strip (the ASCII whitespace left inside a line: space, tab, \x1f);
-  // anything the device does not decode itself defers the line
-  bool blank = true, plain = true;
-  for (uint64_t p = b; p < e; p++) {
-    const uint8_t c = s[p];
-    if (c != ' ' && c != '\t' && c != 0x1f) blank = false;
-    if (c >= 0x80 || c == '\\' || (c < 0x20 && c != '\t')) plain = false;
-  }
-  if (blank) return L_BLANK;
-  if (!plain) return L_DEFER;
+__device__ __forceinline__ bool byte_blank(uint8_t c) { return c == ' ' || c == '\t' || c == 0x1f; }
+__device__ __forceinline__ bool byte_odd(uint8_t c) { return c >= 0x80 || c == '\\' || (c < 0x20 && c != '\t'); }
 
-  Val v[K_N];
-#pragma unroll
-  for (int k = 0; k < K_N; k++) v[k].t = V_NONE;
+// Line class before parsing: 0 blank (str.strip: the ASCII whitespace left inside a
+// line is space, tab, \x1f), 1 plain (no byte the device does not decode itself:
+// non-ASCII, backslash, control other than tab), 2 otherwise.  4 bytes at a time where
+// the text is word-aligned.
+__device__ __forceinline__ int line_class(const uint8_t* s, uint64_t b, uint64_t e, bool words) {
+  bool blank = true, plain = true;
+  uint64_t p = b;
+  if (words) {
+    for (; p < e && (p & 3); p++) {
+      const uint8_t c = s[p];
+      blank &= byte_blank(c);
+      plain &= !byte_odd(c);
+    }
+    for (; p + 4 <= e; p += 4) {
+      const uint32_t w = *reinterpret_cast<const uint32_t*>(s + p);
+      const uint32_t ctl = (w - 0x20202020u) & ~w & 0x80808080u;  // some byte < 0x20 (or >= 0x80)
+      const uint32_t bs = w ^ 0x5C5C5C5Cu;
+      const uint32_t has_bs = (bs - 0x01010101u) & ~bs & 0x80808080u;
+      if ((w & 0x80808080u) | ctl | has_bs) {
+        for (int q = 0; q < 4; q++) {
+          const uint8_t c = (uint8_t)(w >> (8 * q));
+          blank &= byte_blank(c);
+          plain &= !byte_odd(c);
+        }
+      } else if (w != 0x20202020u) {
+        blank = false;
+      }
+    }
+  }
+  for (; p < e; p++) {
+    const uint8_t c = s[p];
+    blank &= byte_blank(c);
+    plain &= !byte_odd(c);
+  }
+  return blank ? 0 : plain ? 1 : 2;
+}
+
+// Parse line [b, e) of s; L_OK with `o` filled, L_BLANK, or L_DEFER.  ``fld`` is this
+// thread's field slots in shared memory (key k at fld[k * stride]).
+__device__ uint8_t parse_line(const uint8_t* s, uint64_t b, uint64_t e, bool words, uint64_t* fld, int stride,
+                              LineOut& o) {
+  const int cls = line_class(s, b, e, words);
+  if (cls == 0) return L_BLANK;
+  if (cls == 2) return L_DEFER;
+
+  // consulted fields: types 3 bits per key (register), payloads in shared memory
+  uint64_t types = 0;
   uint64_t p = skip_ws(s, b, e);
   if (p >= e || s[p] != '{') return L_DEFER;
   p = skip_ws(s, p + 1, e);
@@ -313,18 +530,21 @@ __device__ uint8_t parse_line(const uint8_t* s, uint64_t b, uint64_t e, LineOut&
   while (true) {
     p = skip_ws(s, p, e);
     if (p >= e || s[p] != '"') return L_DEFER;
-    const uint64_t k0 = p + 1;
-    p = skip_string(s, k0, e);
+    Str k;
+    p = scan_str(s, p + 1, e, k);
     if (!p) return L_DEFER;
-    const int key = match(s, (uint32_t)k0, (uint32_t)(p - k0 - 1), kKeyNames);
+    const int key = key_of(k);
     p = skip_ws(s, p, e);
     if (p >= e || s[p] != ':') return L_DEFER;
     p++;
     if (key < 0) {
       p = skip_value(s, p, e);
     } else {
-      v[key].t = V_NONE;
-      p = (key == K_SRC || key == K_DST) ? read_endpoint(s, p, e, v[key]) : read_value(s, p, e, v[key]);
+      uint8_t t = V_NONE;
+      uint64_t v = 0;
+      p = (key == K_SRC || key == K_DST) ? read_endpoint(s, p, e, t, v) : read_value(s, p, e, key, t, v);
+      types = (types & ~(7ull << (3 * key))) | ((uint64_t)t << (3 * key));
+      fld[key * stride] = v;
     }
     if (!p) return L_DEFER;
     p = skip_ws(s, p, e);
@@ -336,30 +556,27 @@ __device__ uint8_t parse_line(const uint8_t* s, uint64_t b, uint64_t e, LineOut&
   if (skip_ws(s, p, e) != e) return L_DEFER;  // "Extra data"
 
   // the reader's consulted keys and TraceEvent.validate, in effect (events.py:287-310)
-  auto str_code = [&](int k, int which) -> int {
-    if (v[k].t != V_STR) return -1;
-    switch (which) {
-      case 0: return match(s, v[k].off, v[k].len, kKinds);
-      case 1: return match(s, v[k].off, v[k].len, kColls);
-      case 2: return match(s, v[k].off, v[k].len, kAlgos);
-      case 3: return match(s, v[k].off, v[k].len, kDtypes);
-      default: return match(s, v[k].off, v[k].len, kCkinds);
-    }
-  };
-  const int kind = str_code(K_KIND, 0);
-  if (kind < 0) return L_DEFER;
-  if (v[K_SEQ].t != V_UINT || v[K_COMM].t != V_STR || v[K_NRANKS].t != V_UINT || v[K_RANK].t != V_UINT ||
-      v[K_DEV].t != V_UINT)
+  auto ty = [&](int key) -> uint32_t { return (uint32_t)(types >> (3 * key)) & 7; };
+  auto fv = [&](int key) -> uint64_t { return ty(key) == V_NONE ? 0 : fld[key * stride]; };
+  const uint64_t f_seq = fv(K_SEQ), f_ts = fv(K_TS), f_kind = fv(K_KIND), f_comm = fv(K_COMM),
+                 f_nranks = fv(K_NRANKS), f_rank = fv(K_RANK), f_dev = fv(K_DEV), f_coll = fv(K_COLL),
+                 f_algo = fv(K_ALGO), f_count = fv(K_COUNT), f_dtype = fv(K_DTYPE), f_root = fv(K_ROOT),
+                 f_peer = fv(K_PEER), f_ckind = fv(K_CKIND), f_src = fv(K_SRC), f_dst = fv(K_DST),
+                 f_bytes = fv(K_BYTES);
+  if (ty(K_KIND) != V_ENUM) return L_DEFER;
+  const int kind = (int)f_kind;
+  if (ty(K_SEQ) != V_UINT || ty(K_COMM) != V_NAME || ty(K_NRANKS) != V_UINT || ty(K_RANK) != V_UINT ||
+      ty(K_DEV) != V_UINT)
     return L_DEFER;
-  if (v[K_TS].t == V_UINT) {
-    if (v[K_TS].u >= (1ull << 63)) return L_DEFER;
-  } else if (v[K_TS].t != V_NINT) {
+  if (ty(K_TS) == V_UINT) {
+    if (f_ts >= (1ull << 63)) return L_DEFER;
+  } else if (ty(K_TS) != V_NINT) {
     return L_DEFER;
   }
-  const uint64_t n = v[K_NRANKS].u, rank = v[K_RANK].u, dev = v[K_DEV].u;
+  const uint64_t n = f_nranks, rank = f_rank, dev = f_dev;
   if (n < 1 || n > 0xFFFF || rank >= n || dev > 0xFFFF) return L_DEFER;
   ct_record& r = o.r;
-  r.seq = v[K_SEQ].u;
+  r.seq = f_seq;
   r.comm = 0;
   r.nranks = (uint16_t)n;
   r.rank = (uint16_t)rank;
@@ -367,61 +584,94 @@ __device__ uint8_t parse_line(const uint8_t* s, uint64_t b, uint64_t e, LineOut&
   r.aux = 0;
   r.aux2 = 0;
   if (kind == CT_KIND_COLLECTIVE) {
-    const int coll = str_code(K_COLL, 1), algo = str_code(K_ALGO, 2), dt = str_code(K_DTYPE, 3);
-    if (coll < 0 || algo < 0 || dt < 0 || v[K_COUNT].t != V_UINT) return L_DEFER;
+    if (ty(K_COLL) != V_ENUM || ty(K_ALGO) != V_ENUM || ty(K_DTYPE) != V_ENUM || ty(K_COUNT) != V_UINT)
+      return L_DEFER;
+    const int coll = (int)f_coll, algo = (int)f_algo, dt = (int)f_dtype;
     const bool rooted = coll == CT_COLL_BROADCAST || coll == CT_COLL_REDUCE;
-    if (v[K_ROOT].t != V_NONE || rooted) {
-      if (v[K_ROOT].t != V_UINT) return L_DEFER;
-      if (!rooted || v[K_ROOT].u >= n) return L_DEFER;  // root only for bcast/reduce, in [0, N)
-      r.aux = (uint16_t)v[K_ROOT].u;
+    if (ty(K_ROOT) != V_NONE || rooted) {
+      if (ty(K_ROOT) != V_UINT) return L_DEFER;
+      if (!rooted || f_root >= n) return L_DEFER;  // root only for bcast/reduce, in [0, N)
+      r.aux = (uint16_t)f_root;
     }
     if ((algo == CT_ALGO_TREE || algo == CT_ALGO_COLLNET) && coll != CT_COLL_ALLREDUCE) return L_DEFER;
-    r.count = v[K_COUNT].u;
+    r.count = f_count;
     r.kc = (uint8_t)(kind | (coll << 3) | (rooted ? 1 << 6 : 0));
     r.ad = (uint8_t)(algo | (dt << 2));
   } else if (kind == CT_KIND_SEND || kind == CT_KIND_RECV) {
-    const int dt = str_code(K_DTYPE, 3);
-    if (v[K_PEER].t != V_UINT || v[K_COUNT].t != V_UINT || dt < 0) return L_DEFER;
-    if (v[K_PEER].u == rank || v[K_PEER].u >= n) return L_DEFER;
-    r.aux = (uint16_t)v[K_PEER].u;
-    r.count = v[K_COUNT].u;
+    if (ty(K_PEER) != V_UINT || ty(K_COUNT) != V_UINT || ty(K_DTYPE) != V_ENUM) return L_DEFER;
+    if (f_peer == rank || f_peer >= n) return L_DEFER;
+    r.aux = (uint16_t)f_peer;
+    r.count = f_count;
     r.kc = (uint8_t)kind;
-    r.ad = (uint8_t)(dt << 2);
+    r.ad = (uint8_t)(f_dtype << 2);
   } else {
-    const int ck = str_code(K_CKIND, 4);
-    if (ck < 0 || v[K_SRC].t != V_EP || v[K_DST].t != V_EP || v[K_BYTES].t != V_UINT) return L_DEFER;
-    const Val &sv = v[K_SRC], &dv = v[K_DST];
-    if (sv.ep_kind < 0 || sv.ep_idx < 0 || dv.ep_kind < 0 || dv.ep_idx < 0) return L_DEFER;
-    const int want_s = ck == CT_CKIND_H2D ? 0 : 1, want_d = ck == CT_CKIND_D2H ? 0 : 1;  // host 0, gpu 1
-    if (sv.ep_kind != want_s || dv.ep_kind != want_d) return L_DEFER;
-    if ((want_s == 0 && sv.ep_idx != 0) || (want_d == 0 && dv.ep_idx != 0)) return L_DEFER;
-    if (sv.ep_idx > 0xFFFF || dv.ep_idx > 0xFFFF) return L_DEFER;
-    if (ck == CT_CKIND_D2D && sv.ep_idx == dv.ep_idx) return L_DEFER;
-    r.aux = (uint16_t)sv.ep_idx;
-    r.aux2 = (uint16_t)dv.ep_idx;
-    r.count = v[K_BYTES].u;
+    if (ty(K_CKIND) != V_ENUM || ty(K_SRC) != V_EP || ty(K_DST) != V_EP || ty(K_BYTES) != V_UINT) return L_DEFER;
+    const int ck = (int)f_ckind;
+    const uint32_t sk = (uint32_t)(f_src & 0xFF), dk = (uint32_t)(f_dst & 0xFF);
+    const uint32_t si = (uint32_t)(f_src >> 8), di = (uint32_t)(f_dst >> 8);
+    if (si == 0xFFFFFFFFu || di == 0xFFFFFFFFu) return L_DEFER;  // absent / negative / > 65535
+    const uint32_t want_s = ck == CT_CKIND_H2D ? 0 : 1, want_d = ck == CT_CKIND_D2H ? 0 : 1;  // host 0, gpu 1
+    if (sk != want_s || dk != want_d) return L_DEFER;
+    if ((want_s == 0 && si != 0) || (want_d == 0 && di != 0)) return L_DEFER;
+    if (ck == CT_CKIND_D2D && si == di) return L_DEFER;
+    r.aux = (uint16_t)si;
+    r.aux2 = (uint16_t)di;
+    r.count = f_bytes;
     r.kc = (uint8_t)kind;
     r.ad = (uint8_t)(ck << 6);
   }
-  o.ts = (int64_t)v[K_TS].u;
-  o.comm_off = v[K_COMM].off;
-  o.comm_len = v[K_COMM].len;
+  o.ts = (int64_t)f_ts;
+  if ((f_comm >> 40) >= (1ull << 23)) return L_DEFER;  // name length field
+  o.comm = f_comm;
   uint64_t h = 0xcbf29ce484222325ull;  // FNV-1a over the name bytes
-  for (uint32_t j = 0; j < o.comm_len; j++) h = (h ^ s[o.comm_off + j]) * 0x100000001b3ull;
+  const uint64_t coff = f_comm & ((1ull << 40) - 1), clen = f_comm >> 40;
+  for (uint64_t j = 0; j < clen; j++) h = (h ^ s[coff + j]) * 0x100000001b3ull;
   o.hash = h == kNoKey ? kNoKey - 1 : h;
   return L_OK;
 }
 
-__global__ void k_parse(const uint8_t* s, uint64_t size, const uint64_t* brk, uint64_t nb, uint64_t n_lines,
-                        uint8_t* status, LineOut* out) {
-  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n_lines;
-       k += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t b = k == 0 ? 0 : brk[k - 1] + break_len(s, size, brk[k - 1]);
-    const uint64_t e = k < nb ? brk[k] : size;
-    LineOut o;
-    const uint8_t st = parse_line(s, b, e, o);
-    status[k] = st;
-    if (st == L_OK) out[k] = o;
+// One thread per line; a block's lines are contiguous in the text, so the block first
+// copies their bytes into shared memory with 16-byte loads (when they fit) and every
+// thread parses from there.
+constexpr int kParseThreads = 128;
+constexpr uint32_t kStage = 32 * 1024;
+
+__global__ void __launch_bounds__(kParseThreads) k_parse(const uint8_t* s, uint64_t size, bool aligned,
+                                                         const uint64_t* brk, uint64_t nb, uint64_t n_lines,
+                                                         uint8_t* status, LineOut* out) {
+  extern __shared__ __align__(16) uint8_t stage[];
+  const uint64_t k0 = blockIdx.x * (uint64_t)kParseThreads;
+  const uint64_t k1 = min(k0 + kParseThreads, n_lines) - 1;  // last line of the block
+  auto line_begin = [&](uint64_t k) { return k == 0 ? 0 : brk[k - 1] + break_len(s, size, brk[k - 1]); };
+  auto line_end = [&](uint64_t k) { return k < nb ? brk[k] : size; };
+  const uint64_t span_b = line_begin(k0) & ~15ull, span_e = line_end(k1);
+  const bool staged = aligned && span_e - span_b <= kStage;
+  const uint8_t* src = s;
+  if (staged) {
+    const uint64_t nv = (span_e - span_b + 15) / 16;
+    for (uint64_t v = threadIdx.x; v < nv; v += kParseThreads) {
+      const uint64_t a = span_b + v * 16;
+      uint4 w;
+      if (a + 16 <= size) {
+        w = *reinterpret_cast<const uint4*>(s + a);
+      } else {
+        uint8_t t[16];
+        for (int q = 0; q < 16; q++) t[q] = a + q < size ? s[a + q] : 0;
+        memcpy(&w, t, 16);
+      }
+      *reinterpret_cast<uint4*>(stage + v * 16) = w;
+    }
+    src = stage - span_b;  // absolute positions index the staged copy
+  }
+  __syncthreads();
+  const uint64_t k = k0 + threadIdx.x;
+  if (k >= n_lines) return;
+  __shared__ uint64_t fields[K_N * kParseThreads];
+  LineOut o;
+  const uint8_t st = parse_line(src, line_begin(k), line_end(k), aligned, fields + threadIdx.x, kParseThreads, o);
+  status[k] = st;
+  if (st == L_OK) {
+    out[k] = o;
   }
 }
 
@@ -447,7 +697,7 @@ __global__ void k_scatter(uint64_t n_lines, const uint8_t* status, const LineOut
       recs[i] = lo[k].r;
       ts[i] = lo[k].ts;
       keys[i] = lo[k].hash;
-      coff[i] = ((uint64_t)lo[k].comm_len << 40) | lo[k].comm_off;
+      coff[i] = lo[k].comm;
     } else {
       recs[i] = ct_record{};
       ts[i] = 0;
@@ -540,13 +790,6 @@ __global__ void k_deferred_rows(uint64_t nd, const uint64_t* lines, const uint64
   }
 }
 
-__global__ void k_nonascii(const uint8_t* s, uint64_t n, unsigned int* flag) {
-  bool any = false;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
-    any |= s[i] >= 0x80;
-  if (__any_sync(0xffffffffu, any) && (threadIdx.x & 31) == 0) atomicOr(flag, 1u);
-}
-
 }  // namespace
 
 // ---------------------------------------------------------------- handle + C ABI
@@ -614,27 +857,28 @@ int run(ct_jsonl* j, const uint8_t* text, uint64_t size, int on_device) {
   JL_TRY(cudaMemsetAsync(scal, 0, 8 * sizeof(uint64_t), j->st));
   unsigned int* flags = reinterpret_cast<unsigned int*>(scal + 6);
 
-  // 1. terminators
+  // 1. terminators: per-tile counts, tile offsets, ordered positions
   thrust::counting_iterator<uint64_t> idx(0);
-  BreakPred bp{s, size};
-  auto cnt_it = thrust::make_transform_iterator(idx, BreakCount{bp});
+  const bool aligned = (reinterpret_cast<uintptr_t>(s) & 15) == 0;
+  const uint64_t n_tiles = (size + kTileBytes - 1) / kTileBytes;
+  uint32_t* tile_cnt = pool.alloc<uint32_t>(n_tiles + 1);
+  uint64_t* tile_off = pool.alloc<uint64_t>(n_tiles + 1);
+  JL_NN(tile_cnt); JL_NN(tile_off);
+  JL_TRY(cudaMemsetAsync(tile_cnt + n_tiles, 0, sizeof(uint32_t), j->st));
+  if (n_tiles) k_brk_count<<<(unsigned)n_tiles, kTileThreads, 0, j->st>>>(s, size, aligned, tile_cnt, flags);
+  JL_TRY(cudaGetLastError());
   size_t tb = 0;
-  JL_TRY(cub::DeviceReduce::Sum(nullptr, tb, cnt_it, scal, (int64_t)size, j->st));
+  JL_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tb, tile_cnt, tile_off, (int64_t)n_tiles + 1, j->st));
   void* t = pool.temp(tb);
   JL_NN(t);
-  JL_TRY(cub::DeviceReduce::Sum(t, tb, cnt_it, scal, (int64_t)size, j->st));
+  JL_TRY(cub::DeviceScan::ExclusiveSum(t, tb, tile_cnt, tile_off, (int64_t)n_tiles + 1, j->st));
   uint64_t nb = 0;
-  JL_TRY(cudaMemcpyAsync(&nb, scal, sizeof(uint64_t), cudaMemcpyDeviceToHost, j->st));
+  JL_TRY(cudaMemcpyAsync(&nb, tile_off + n_tiles, sizeof(uint64_t), cudaMemcpyDeviceToHost, j->st));
   JL_TRY(cudaStreamSynchronize(j->st));
   uint64_t* brk = pool.alloc<uint64_t>(nb);
   JL_NN(brk);
-  if (nb) {
-    tb = 0;
-    JL_TRY(cub::DeviceSelect::If(nullptr, tb, idx, brk, scal + 1, (int64_t)size, bp, j->st));
-    t = pool.temp(tb);
-    JL_NN(t);
-    JL_TRY(cub::DeviceSelect::If(t, tb, idx, brk, scal + 1, (int64_t)size, bp, j->st));
-  }
+  if (nb) k_brk_write<<<(unsigned)n_tiles, kTileThreads, 0, j->st>>>(s, size, aligned, tile_off, brk);
+  JL_TRY(cudaGetLastError());
   uint64_t last_end = 0;  // first byte after the last terminator
   if (nb) {
     uint64_t lb = 0;
@@ -651,7 +895,6 @@ int run(ct_jsonl* j, const uint8_t* text, uint64_t size, int on_device) {
   }
   const uint64_t n_lines = nb + (last_end < size ? 1 : 0);
   j->info.n_lines = n_lines;
-  k_nonascii<<<grid_for(size), 256, 0, j->st>>>(s, size, flags + 1);
 
   // 2. parse, one thread per line
   uint8_t* status = pool.alloc<uint8_t>(n_lines + 1);  // + a blank terminator for the scan
@@ -659,7 +902,11 @@ int run(ct_jsonl* j, const uint8_t* text, uint64_t size, int on_device) {
   uint64_t* ridx = pool.alloc<uint64_t>(n_lines + 1);
   JL_NN(status); JL_NN(lo); JL_NN(ridx);
   JL_TRY(cudaMemsetAsync(status + n_lines, L_BLANK, 1, j->st));
-  if (n_lines) k_parse<<<grid_for(n_lines, 128), 128, 0, j->st>>>(s, size, brk, nb, n_lines, status, lo);
+  if (n_lines) {
+    JL_TRY(cudaFuncSetAttribute(k_parse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kStage));
+    k_parse<<<(unsigned)((n_lines + kParseThreads - 1) / kParseThreads), kParseThreads, kStage, j->st>>>(
+        s, size, aligned, brk, nb, n_lines, status, lo);
+  }
   JL_TRY(cudaGetLastError());
   auto nb_it = thrust::make_transform_iterator(idx, NonBlank{status});
   tb = 0;
