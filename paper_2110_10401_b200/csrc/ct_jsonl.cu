@@ -634,7 +634,7 @@ __device__ uint8_t parse_line(const uint8_t* s, uint64_t b, uint64_t e, bool wor
 // copies their bytes into shared memory with 16-byte loads (when they fit) and every
 // thread parses from there.
 constexpr int kParseThreads = 128;
-constexpr uint32_t kStage = 32 * 1024;
+constexpr uint32_t kStage = 24 * 1024;
 
 __global__ void __launch_bounds__(kParseThreads) k_parse(const uint8_t* s, uint64_t size, bool aligned,
                                                          const uint64_t* brk, uint64_t nb, uint64_t n_lines,
