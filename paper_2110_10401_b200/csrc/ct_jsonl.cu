@@ -251,11 +251,60 @@ __device__ __forceinline__ uint64_t skip_ws(const uint8_t* s, uint64_t p, uint64
   return p;
 }
 
+__device__ __forceinline__ uint32_t has_byte(uint32_t w, uint32_t rep) {
+  const uint32_t x = w ^ rep;  // lowest set bit is exact (higher ones may be borrow artefacts)
+  return (x - 0x01010101u) & ~x & 0x80808080u;
+}
+
 // string body after the opening quote, packing its first 16 bytes: position after the
 // closing quote, or 0 on failure (the line holds no backslash / control / non-ASCII
-// byte; a raw tab is invalid in a strict JSON string)
-__device__ __forceinline__ uint64_t scan_str(const uint8_t* s, uint64_t p, uint64_t e, Str& out) {
+// byte; a raw tab is invalid in a strict JSON string).  ``wl``: bytes below wl may be
+// read as aligned 32-bit words (0: byte path only).
+__device__ __forceinline__ uint64_t scan_str(const uint8_t* s, uint64_t p, uint64_t e, Str& out, uint64_t wl) {
   const uint64_t p0 = p;
+  if (p0 + 24 <= wl) {
+    const uint64_t a = p0 & ~3ull;
+    const uint32_t sh = (uint32_t)(p0 & 3) * 8;
+    const uint32_t lowm = (1u << sh) - 1;
+    uint64_t q = a;
+    uint32_t w = (*reinterpret_cast<const uint32_t*>(s + a) & ~lowm) | (0x78787878u & lowm);
+    uint64_t pos = 0;
+    while (true) {
+      const uint32_t hit = has_byte(w, 0x22222222u) | has_byte(w, 0x09090909u);
+      if (hit) {
+        const uint32_t j = (uint32_t)(__ffs(hit) - 1) >> 3;
+        pos = q + j;
+        if (pos >= e || ((w >> (8 * j)) & 0xFF) != '"') return 0;
+        break;
+      }
+      q += 4;
+      if (q >= e) return 0;
+      if (q + 4 > wl) {  // long string near the readable limit: finish bytewise
+        pos = q;
+        while (pos < e && s[pos] != '"') {
+          if (s[pos] == '\t') return 0;
+          pos++;
+        }
+        if (pos >= e) return 0;
+        break;
+      }
+      w = *reinterpret_cast<const uint32_t*>(s + q);
+    }
+    const uint32_t* wp = reinterpret_cast<const uint32_t*>(s + a);
+    const uint64_t A = wp[0] | ((uint64_t)wp[1] << 32), B = wp[2] | ((uint64_t)wp[3] << 32), C4 = wp[4];
+    uint64_t lo = A, hi = B;
+    if (sh) {
+      lo = (A >> sh) | (B << (64 - sh));
+      hi = (B >> sh) | (C4 << (64 - sh));
+    }
+    const uint64_t len = pos - p0;
+    if (len < 8) { lo &= (1ull << (8 * len)) - 1; hi = 0; }
+    else if (len < 16) { hi &= (1ull << (8 * (len - 8))) - 1; }
+    out.len = (uint32_t)len;
+    out.w0 = lo;
+    out.w1 = hi;
+    return pos + 1;
+  }
   uint64_t w0 = 0, w1 = 0;
   while (p < e) {
     const uint8_t c = s[p];
@@ -296,10 +345,13 @@ __device__ uint64_t scan_number(const uint8_t* s, uint64_t p, uint64_t e, bool& 
   if (s[p] == '0') {
     p++;
   } else if (s[p] >= '1' && s[p] <= '9') {
+    int nd = 0;
     while (p < e && s[p] >= '0' && s[p] <= '9') {
       const uint64_t dgt = s[p] - '0';
-      if (mag > (~0ull - dgt) / 10) fits = false;
-      else mag = mag * 10 + dgt;
+      if (nd < 19) mag = mag * 10 + dgt;  // < 10^19 cannot overflow
+      else if (fits && mag <= (~0ull - dgt) / 10) mag = mag * 10 + dgt;
+      else fits = false;
+      nd++;
       p++;
     }
   } else {
@@ -385,13 +437,14 @@ after:
 
 // A value of a consulted key -> (type, payload): ints as values, enum strings as codes,
 // the comm name as (offset | length << 40), anything else skipped as V_OTHER.
-__device__ uint64_t read_value(const uint8_t* s, uint64_t p, uint64_t e, int key, uint8_t& t, uint64_t& v) {
+__device__ uint64_t read_value(const uint8_t* s, uint64_t p, uint64_t e, int key, uint8_t& t, uint64_t& v,
+                           uint64_t wl) {
   p = skip_ws(s, p, e);
   if (p >= e) return 0;
   const uint8_t c = s[p];
   if (c == '"') {
     Str x;
-    const uint64_t q = scan_str(s, p + 1, e, x);
+    const uint64_t q = scan_str(s, p + 1, e, x, wl);
     if (!q) return 0;
     if (key == K_COMM) {
       t = V_NAME;
@@ -422,7 +475,7 @@ __device__ uint64_t read_value(const uint8_t* s, uint64_t p, uint64_t e, int key
 // payload kind code (host 0, gpu 1, net 2; 0xFF absent/invalid) | idx << 8 (idx
 // 0xFFFFFFFF absent/invalid/too large); other members grammar-checked and ignored;
 // duplicate keys: last wins (json.loads).
-__device__ uint64_t read_endpoint(const uint8_t* s, uint64_t p, uint64_t e, uint8_t& t, uint64_t& v) {
+__device__ uint64_t read_endpoint(const uint8_t* s, uint64_t p, uint64_t e, uint8_t& t, uint64_t& v, uint64_t wl) {
   p = skip_ws(s, p, e);
   if (p >= e) return 0;
   if (s[p] != '{') { t = V_OTHER; return skip_value(s, p, e); }
@@ -433,7 +486,7 @@ __device__ uint64_t read_endpoint(const uint8_t* s, uint64_t p, uint64_t e, uint
     p = skip_ws(s, p, e);
     if (p >= e || s[p] != '"') return 0;
     Str k;
-    p = scan_str(s, p + 1, e, k);
+    p = scan_str(s, p + 1, e, k, wl);
     if (!p) return 0;
     p = skip_ws(s, p, e);
     if (p >= e || s[p] != ':') return 0;
@@ -442,7 +495,7 @@ __device__ uint64_t read_endpoint(const uint8_t* s, uint64_t p, uint64_t e, uint
       p = skip_ws(s, p, e);
       if (p < e && s[p] == '"') {
         Str x;
-        p = scan_str(s, p + 1, e, x);
+        p = scan_str(s, p + 1, e, x, wl);
         if (!p) return 0;
         kind = CT_IS(x, "host") ? 0 : CT_IS(x, "gpu") ? 1 : CT_IS(x, "net") ? 2 : 0xFF;
       } else {
@@ -452,7 +505,7 @@ __device__ uint64_t read_endpoint(const uint8_t* s, uint64_t p, uint64_t e, uint
     } else if (CT_IS(k, "idx")) {
       uint8_t wt = V_NONE;
       uint64_t wv = 0;
-      p = read_value(s, p, e, -1, wt, wv);
+      p = read_value(s, p, e, -1, wt, wv, wl);
       idx = wt == V_UINT && wv <= 0xFFFF ? (uint32_t)wv : 0xFFFFFFFFu;
     } else {
       p = skip_value(s, p, e);
@@ -515,8 +568,8 @@ __device__ __forceinline__ int line_class(const uint8_t* s, uint64_t b, uint64_t
 
 // Parse line [b, e) of s; L_OK with `o` filled, L_BLANK, or L_DEFER.  ``fld`` is this
 // thread's field slots in shared memory (key k at fld[k * stride]).
-__device__ uint8_t parse_line(const uint8_t* s, uint64_t b, uint64_t e, bool words, uint64_t* fld, int stride,
-                              LineOut& o) {
+__device__ uint8_t parse_line(const uint8_t* s, uint64_t b, uint64_t e, bool words, uint64_t wl, uint64_t* fld,
+                              int stride, LineOut& o) {
   const int cls = line_class(s, b, e, words);
   if (cls == 0) return L_BLANK;
   if (cls == 2) return L_DEFER;
@@ -531,7 +584,7 @@ __device__ uint8_t parse_line(const uint8_t* s, uint64_t b, uint64_t e, bool wor
     p = skip_ws(s, p, e);
     if (p >= e || s[p] != '"') return L_DEFER;
     Str k;
-    p = scan_str(s, p + 1, e, k);
+    p = scan_str(s, p + 1, e, k, wl);
     if (!p) return L_DEFER;
     const int key = key_of(k);
     p = skip_ws(s, p, e);
@@ -542,7 +595,7 @@ __device__ uint8_t parse_line(const uint8_t* s, uint64_t b, uint64_t e, bool wor
     } else {
       uint8_t t = V_NONE;
       uint64_t v = 0;
-      p = (key == K_SRC || key == K_DST) ? read_endpoint(s, p, e, t, v) : read_value(s, p, e, key, t, v);
+      p = (key == K_SRC || key == K_DST) ? read_endpoint(s, p, e, t, v, wl) : read_value(s, p, e, key, t, v, wl);
       types = (types & ~(7ull << (3 * key))) | ((uint64_t)t << (3 * key));
       fld[key * stride] = v;
     }
@@ -635,6 +688,7 @@ __device__ uint8_t parse_line(const uint8_t* s, uint64_t b, uint64_t e, bool wor
 // thread parses from there.
 constexpr int kParseThreads = 128;
 constexpr uint32_t kStage = 24 * 1024;
+constexpr uint32_t kStageSlack = 32;  // readable bytes past the stage (word scans)
 
 __global__ void __launch_bounds__(kParseThreads) k_parse(const uint8_t* s, uint64_t size, bool aligned,
                                                          const uint64_t* brk, uint64_t nb, uint64_t n_lines,
@@ -668,7 +722,10 @@ __global__ void __launch_bounds__(kParseThreads) k_parse(const uint8_t* s, uint6
   if (k >= n_lines) return;
   __shared__ uint64_t fields[K_N * kParseThreads];
   LineOut o;
-  const uint8_t st = parse_line(src, line_begin(k), line_end(k), aligned, fields + threadIdx.x, kParseThreads, o);
+  // word reads may run up to 24 bytes past a string start: the stage has that slack,
+  // the global text is read wordwise only away from its end
+  const uint64_t wl = !aligned ? 0 : staged ? span_b + kStage + kStageSlack : (size > 32 ? size - 8 : 0);
+  const uint8_t st = parse_line(src, line_begin(k), line_end(k), aligned, wl, fields + threadIdx.x, kParseThreads, o);
   status[k] = st;
   if (st == L_OK) {
     out[k] = o;
@@ -903,8 +960,8 @@ int run(ct_jsonl* j, const uint8_t* text, uint64_t size, int on_device) {
   JL_NN(status); JL_NN(lo); JL_NN(ridx);
   JL_TRY(cudaMemsetAsync(status + n_lines, L_BLANK, 1, j->st));
   if (n_lines) {
-    JL_TRY(cudaFuncSetAttribute(k_parse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kStage));
-    k_parse<<<(unsigned)((n_lines + kParseThreads - 1) / kParseThreads), kParseThreads, kStage, j->st>>>(
+    JL_TRY(cudaFuncSetAttribute(k_parse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kStage + kStageSlack)));
+    k_parse<<<(unsigned)((n_lines + kParseThreads - 1) / kParseThreads), kParseThreads, kStage + kStageSlack, j->st>>>(
         s, size, aligned, brk, nb, n_lines, status, lo);
   }
   JL_TRY(cudaGetLastError());

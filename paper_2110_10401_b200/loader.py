@@ -53,9 +53,9 @@ def load_trace(source, device: int | None = None) -> PackedTrace:
         device = _lib.context().device
     handle = C.c_void_p()
     info = _lib.CtJsonlInfo()
-    buf = C.create_string_buffer(data, len(data)) if data else None
-    rc = lib.ct_jsonl_parse(device, C.cast(buf, C.c_void_p) if buf else None, len(data), 0,
-                            C.byref(handle), C.byref(info))
+    # the bytes object's own buffer (no copy); the library copies it to the device
+    ptr = C.cast(C.c_char_p(data), C.c_void_p) if data else None
+    rc = lib.ct_jsonl_parse(device, ptr, len(data), 0, C.byref(handle), C.byref(info))
     try:
         if rc != _lib.CT_OK:
             msg = lib.ct_jsonl_error(handle)
