@@ -687,7 +687,10 @@ __device__ uint8_t parse_line(const uint8_t* s, uint64_t b, uint64_t e, bool wor
 // copies their bytes into shared memory with 16-byte loads (when they fit) and every
 // thread parses from there.
 constexpr int kParseThreads = 128;
-constexpr uint32_t kStage = 24 * 1024;
+#ifndef CT_JSONL_STAGE
+#define CT_JSONL_STAGE (24 * 1024)
+#endif
+constexpr uint32_t kStage = CT_JSONL_STAGE;
 constexpr uint32_t kStageSlack = 32;  // readable bytes past the stage (word scans)
 
 __global__ void __launch_bounds__(kParseThreads) k_parse(const uint8_t* s, uint64_t size, bool aligned,
