@@ -37,14 +37,21 @@ def _as_bytes(source) -> bytes:
 
 
 def load_trace(source, device: int | None = None) -> PackedTrace:
-    """JSONL (bytes / str / binary file) -> PackedTrace whose ``records`` is a CUDA
+    """JSONL (bytes / str / binary file / 1-D CUDA uint8 tensor) -> PackedTrace whose ``records`` is a CUDA
     uint8 tensor of shape (n, 32) on ``device``; ``ts`` is an int64 numpy array (a
     list when a timestamp does not fit int64); ``comms`` lists names by comm id."""
     import torch
 
+    dev_text = None
     if isinstance(source, str):
         text_str = source
         data = source.encode("utf-8", "surrogatepass")
+    elif isinstance(source, torch.Tensor):  # text already in device memory (uint8, 1-D)
+        if not source.is_cuda or source.dtype != torch.uint8 or source.dim() != 1:
+            raise TypeError("device text must be a 1-D CUDA uint8 tensor")
+        text_str, data, dev_text = None, None, source.contiguous()
+        if device is None:
+            device = dev_text.device.index
     else:
         text_str = None
         data = _as_bytes(source)
@@ -53,9 +60,14 @@ def load_trace(source, device: int | None = None) -> PackedTrace:
         device = _lib.context().device
     handle = C.c_void_p()
     info = _lib.CtJsonlInfo()
-    # the bytes object's own buffer (no copy); the library copies it to the device
-    ptr = C.cast(C.c_char_p(data), C.c_void_p) if data else None
-    rc = lib.ct_jsonl_parse(device, ptr, len(data), 0, C.byref(handle), C.byref(info))
+    if dev_text is not None:
+        torch.cuda.current_stream(dev_text.device).synchronize()  # the library uses its own stream
+        rc = lib.ct_jsonl_parse(device, C.c_void_p(dev_text.data_ptr() if dev_text.numel() else 0),
+                                dev_text.numel(), 1, C.byref(handle), C.byref(info))
+    else:
+        # the bytes object's own buffer (no copy); the library copies it to the device
+        ptr = C.cast(C.c_char_p(data), C.c_void_p) if data else None
+        rc = lib.ct_jsonl_parse(device, ptr, len(data), 0, C.byref(handle), C.byref(info))
     try:
         if rc != _lib.CT_OK:
             msg = lib.ct_jsonl_error(handle)
@@ -75,6 +87,8 @@ def load_trace(source, device: int | None = None) -> PackedTrace:
     finally:
         lib.ct_jsonl_free(handle)
 
+    if dev_text is not None and (nd or info.non_ascii):
+        data = dev_text.cpu().numpy().tobytes()  # host copy only for deferred lines / UTF-8 check
     # the reference decodes the whole text before reading any line (UnicodeDecodeError first)
     if info.non_ascii and text_str is None:
         data.decode("utf-8")

@@ -236,3 +236,28 @@ def test_first_seen_comm_order_with_deferred_lines():
     lines = [json.dumps(dict(BASE[1], comm="\\u0063\\u0031")).replace("\\\\", "\\"),
              json.dumps(BASE[0]), json.dumps(BASE[1]), json.dumps(dict(BASE[0], comm="zé"))]
     check_same("\n".join(lines) + "\n")
+
+
+def test_device_resident_text_aligned_and_unaligned():
+    """on_device=1 through the C ABI; an odd offset takes the unstaged byte path."""
+    import torch
+
+    rng = random.Random(7)
+    for trial in range(40):
+        text = fuzz_text(rng, rng.randrange(1, 300), [0.0, 0.05, 0.3][trial % 3], 0.1)
+        data = text.encode("utf-8", "surrogatepass")
+        ref, err = reference(data)
+        for off in (0, 1, 3):
+            buf = torch.zeros(len(data) + off, dtype=torch.uint8, device="cuda")
+            if data:
+                buf[off:] = torch.frombuffer(bytearray(data), dtype=torch.uint8).cuda()
+            src = buf[off:]
+            if err is not None:
+                with pytest.raises(type(err)) as got:
+                    load_trace(src)
+                assert str(got.value) == str(err)
+                continue
+            got = load_trace(src)
+            assert got.records.cpu().numpy().tobytes() == ref.records.tobytes()
+            assert got.comms == ref.comms
+            assert [int(t) for t in got.ts] == [int(t) for t in ref.ts]
