@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--seed", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-loader", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=64_000_000)
     ap.add_argument("--ref-sample", type=int, default=2_000_000)
     return ap.parse_args()
@@ -301,6 +302,10 @@ def main():
                "d2h_bytes_per_step": d2h, "ms_per_step": ems, "steps": e_steps,
                "source": "pinned host buffers through ct_analyze (H2D inside the timed region)"}
 
+    loader = None
+    if rank == 0 and world == 1 and not a.no_loader:
+        loader = loader_measure(ctx)
+
     if rank == 0:
         line = {
             "metric": "trace records/sec -> comm matrix (device-timed)",
@@ -319,10 +324,52 @@ def main():
             "gpu_launches": launches,
             "clocks": clocks,
             "result_check": check,
+            "loader": loader,
         }
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
+
+
+def loader_measure(ctx, blk=20_000, reps=50):
+    """Device JSONL loader (``load_trace``) on a generated C3 text: ``blk``
+    records written with the reference wire format (write_trace), repeated ``reps``
+    times, passed as host bytes.  Reported beside the headline, not part of it."""
+    try:
+        import numpy as np
+        import torch
+        from paper_2110_10401_b200.events import parse_trace, write_trace
+        from paper_2110_10401_b200.loader import load_trace
+        from paper_2110_10401_b200.packed import PackedTrace, RECORD_DTYPE, pack_events, unpack
+
+        buf = torch.empty(blk * RECORD_BYTES, dtype=torch.uint8, device="cuda")
+        rc = ctx.lib.ct_generate(ctx.handle, 3, 11, 0, blk, C.c_void_p(buf.data_ptr()), None)
+        assert rc == 0, ctx.error()
+        torch.cuda.synchronize()
+        rec = np.frombuffer(buf.cpu().numpy().tobytes(), dtype=RECORD_DTYPE).copy()
+        names = [f"comm{i}" for i in range(int(rec["comm"].max()) + 1)]
+        block = write_trace(unpack(PackedTrace(rec, names, list(range(blk)), None)))
+        text = block * reps
+        load_trace(block)  # warm-up
+        dev_ms, e2e_s = [], []
+        for _ in range(3):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            tr = load_trace(text)
+            torch.cuda.synchronize()
+            e2e_s.append(time.perf_counter() - t0)
+            dev_ms.append(tr.load_info["ms_device"])
+        n = len(tr)
+        assert n == blk * reps and tr.load_info["deferred"] == 0
+        want = pack_events(parse_trace(block))  # host reader on one block (comm ids in first-seen order)
+        assert tr.records[:blk].cpu().numpy().tobytes() == want.records.tobytes() and tr.comms == want.comms
+        ms, dt = statistics.median(dev_ms), statistics.median(e2e_s)
+        return {"records_per_s_device": n / (ms / 1e3), "jsonl_gb_per_s_device": len(text) / (ms / 1e3) / 1e9,
+                "ms_device": ms, "e2e_records_per_s": n / dt, "e2e_ms": dt * 1e3, "lines": n, "bytes": len(text),
+                "sample": f"C3 {blk} records x {reps} as JSONL, host bytes; median of 3",
+                "api": "load_trace (JSONL -> records in HBM; device time = CUDA events around ct_jsonl_parse)"}
+    except Exception as exc:  # reported, never fatal for the headline line
+        return {"error": repr(exc)[:300]}
 
 
 def cpu_baseline_c(buf, sample, kind, lib):
