@@ -32,7 +32,20 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+SHIM = os.path.join(OUT or PKG, "libcomscribe_shim.so")
+
+
+def build_shim(force: bool = False) -> str:
+    """LD_PRELOAD NCCL interposer (host C, no CUDA): csrc/comscribe_shim.c."""
+    src = os.path.join(CSRC, "comscribe_shim.c")
+    if force or not os.path.exists(SHIM) or os.path.getmtime(src) > os.path.getmtime(SHIM):
+        subprocess.run(["gcc", "-O2", "-shared", "-fPIC", "-fvisibility=hidden", "-Wall", "-o", SHIM, src,
+                        "-ldl", "-lpthread"], check=True)
+    return SHIM
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
+    build_shim(force)
     if not force and not _stale():
         return LIB
     objs = []

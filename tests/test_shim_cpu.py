@@ -1,0 +1,103 @@
+"""LD_PRELOAD NCCL interposer against a mock NCCL.
+
+A child process preloads ``libcomscribe_shim.so``, loads the mock library globally
+and calls the NCCL entry points through the global symbol namespace (so the shim
+intercepts, as it does for an application linked against libnccl).  The trace must
+parse with the reference-mirroring reader, group across the simulated ranks (comm
+ids from the shared ncclUniqueId) and analyse like the same calls written by hand.
+"""
+
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SHIM = os.path.join(ROOT, "paper_2110_10401_b200", "libcomscribe_shim.so")
+
+CHILD = r"""
+import ctypes as C, sys
+mock = C.CDLL(sys.argv[1], mode=C.RTLD_GLOBAL)
+g = C.CDLL(None)  # global lookup: the preloaded shim comes first
+class UID(C.Structure):
+    _fields_ = [("internal", C.c_char * 128)]
+g.ncclCommInitRank.argtypes = [C.POINTER(C.c_void_p), C.c_int, UID, C.c_int]
+uid = UID(); uid.internal = b"job-42"
+comms = []
+for r in range(4):
+    c = C.c_void_p(); assert g.ncclCommInitRank(C.byref(c), 4, uid, r) == 0; comms.append(c)
+V, S = C.c_void_p, C.c_size_t
+g.ncclAllReduce.argtypes = [V, V, S, C.c_int, C.c_int, V, V]
+g.ncclBroadcast.argtypes = [V, V, S, C.c_int, C.c_int, V, V]
+g.ncclReduce.argtypes = [V, V, S, C.c_int, C.c_int, C.c_int, V, V]
+g.ncclAllGather.argtypes = [V, V, S, C.c_int, V, V]
+g.ncclReduceScatter.argtypes = [V, V, S, C.c_int, C.c_int, V, V]
+g.ncclSend.argtypes = [V, S, C.c_int, C.c_int, V, V]
+g.ncclRecv.argtypes = [V, S, C.c_int, C.c_int, V, V]
+for c in comms: assert g.ncclAllReduce(None, None, 256, 7, 0, c, None) == 0      # float32
+for c in comms: assert g.ncclBroadcast(None, None, 1000, 9, 1, c, None) == 0     # bfloat16, root 1
+for c in comms: assert g.ncclReduce(None, None, 64, 8, 0, 2, c, None) == 0       # float64, root 2
+for c in comms: assert g.ncclAllGather(None, None, 32, 2, c, None) == 0          # int32
+for c in comms: assert g.ncclReduceScatter(None, None, 16, 6, 0, c, None) == 0   # float16
+assert g.ncclSend(None, 10, 4, 3, comms[0], None) == 0                            # int64 0 -> 3
+assert g.ncclRecv(None, 10, 4, 0, comms[3], None) == 0
+print(g.ncclAllReduce(None, None, 999, 7, 0, comms[1], None))                   # status passthrough
+"""
+
+
+def _mock(tmp_path):
+    lib = tmp_path / "libnccl_mock.so"
+    subprocess.run(["gcc", "-shared", "-fPIC", "-O1", "-o", str(lib),
+                    os.path.join(ROOT, "tests", "native", "nccl_mock.c")], check=True)
+    return str(lib)
+
+
+def _child(tmp_path, env_extra):
+    if not os.path.exists(SHIM):
+        pytest.skip("shim not built (run __graft_entry__.build())")
+    env = dict(os.environ, LD_PRELOAD=SHIM, **env_extra)
+    return subprocess.run([sys.executable, "-c", CHILD, _mock(tmp_path)], env=env, capture_output=True,
+                          text=True, timeout=120)
+
+
+def test_shim_lines_group_and_analyse(tmp_path):
+    sys.path.insert(0, ROOT)
+    from oracle import commtrace_oracle as O
+    from paper_2110_10401_b200.events import parse_trace, write_trace
+
+    out = tmp_path / "trace.jsonl"
+    p = _child(tmp_path, {"COMSCRIBE_OUT": str(out)})
+    assert p.returncode == 0, p.stderr
+    assert p.stdout.strip() == "5"  # forwarded status, verbatim
+    text = out.read_text()
+    lines = text.splitlines()
+    assert len(lines) == 4 * 5 + 2 + 1  # one line per call per rank
+    objs = [json.loads(l) for l in lines]
+    assert len({o["comm"] for o in objs}) == 1  # one communicator across the 4 ranks
+    evs = parse_trace(text)
+    assert write_trace(evs).decode() == text  # canonical key order and separators
+    for r in range(4):
+        mine = [o for o in objs if o["rank"] == r]
+        assert [o["seq"] for o in mine] == list(range(len(mine)))
+        assert all(o["dev"] == r + 10 and o["nranks"] == 4 for o in mine)
+    colls = [o for o in objs if o["kind"] == "collective"]
+    assert all(o["algo"] == "auto" for o in colls)
+    assert {(o["coll"], o["dtype"], o.get("root")) for o in colls} == {
+        ("allreduce", "float32", None), ("broadcast", "bfloat16", 1), ("reduce", "float64", 2),
+        ("allgather", "int32", None), ("reducescatter", "float16", None)}
+    send = [o for o in objs if o["kind"] == "send"][0]
+    assert (send["peer"], send["count"], send["dtype"], send["rank"]) == (3, 10, "int64", 0)
+    # the trace analyses: 5 complete instances + the unmatched extra allreduce on rank 1
+    res = O.analyze(evs[:-1])["result"]
+    assert res["instances"] == 5
+
+
+def test_shim_disable_and_unwritable_sink(tmp_path):
+    out = tmp_path / "t.jsonl"
+    p = _child(tmp_path, {"COMSCRIBE_OUT": str(out), "COMSCRIBE_DISABLE": "1"})
+    assert p.returncode == 0 and p.stdout.strip() == "5" and not out.exists()
+    p = _child(tmp_path, {"COMSCRIBE_OUT": str(tmp_path / "no" / "such" / "dir" / "t.jsonl")})
+    assert p.returncode == 0 and p.stdout.strip() == "5"  # calls still forward
+    assert p.stderr.count("cannot open trace sink") == 1
