@@ -11,6 +11,7 @@
  * Env: COMSCRIBE_OUT (sink, default comscribe_trace.jsonl; opened O_APPEND so the
  * processes of one job can share it, one write(2) per line), COMSCRIBE_DISABLE=1.
  * An unwritable sink disables logging with one warning; calls still forward.
+ * COMSCRIBE_NCCL_LIB names the real library when it is not in the global scope.
  *
  * Communicator ids: the spec derives them from the handle address + a process nonce,
  * which only groups ranks living in one process.  Here a communicator created by
@@ -82,9 +83,20 @@ static void emit(const char* line, size_t len) {
 
 /* ------------------------------------------------------- real symbols */
 
+/* The real symbol: the next definition in the global scope, else the already-loaded
+ * libnccl.so.2 (frameworks such as torch load it in a RTLD_LOCAL scope that RTLD_NEXT
+ * does not search), else COMSCRIBE_NCCL_LIB. */
 static void* real(const char* name) {
   void* f = dlsym(RTLD_NEXT, name);
-  if (!f) fprintf(stderr, "comscribe: %s not found in the next library\n", name);
+  if (f) return f;
+  static void* h = NULL;
+  if (!h) {
+    const char* lib = getenv("COMSCRIBE_NCCL_LIB");
+    h = dlopen(lib && *lib ? lib : "libnccl.so.2", RTLD_NOLOAD | RTLD_LAZY);
+    if (!h && lib && *lib) h = dlopen(lib, RTLD_LAZY);
+  }
+  if (h) f = dlsym(h, name);
+  if (!f) fprintf(stderr, "comscribe: %s not found (set COMSCRIBE_NCCL_LIB)\n", name);
   return f;
 }
 
