@@ -17,6 +17,10 @@ from tests.test_gpu_loader import _generated_text  # noqa: E402
 blk = int(sys.argv[1]) if len(sys.argv) > 1 else 20000
 rep = int(sys.argv[2]) if len(sys.argv) > 2 else 200
 block = _generated_text(3, blk, seed=7)
+if len(sys.argv) > 3 and sys.argv[3] == "bigts":  # nanosecond wall-clock timestamps, as the shim writes
+    import re
+    base = 1_760_000_000_000_000_000
+    block = re.sub(rb'"ts":(\d+)', lambda m: b'"ts":%d' % (base + 1000 * int(m.group(1))), block)
 t0 = time.perf_counter()
 ref = pack_events(parse_trace(block))
 t_host = time.perf_counter() - t0
