@@ -77,7 +77,7 @@ def ncu_traffic(workload, records):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks / throttle reasons sampled during the timed region (NVML, else nvidia-smi)."""
 
     def __init__(self, index=0):
         self.index = index
@@ -85,7 +85,36 @@ class ClockSampler:
         self._stop = threading.Event()
         self._t = None
 
+    def _nvml(self):
+        """NVML reader (≈1 ms per sample) or None; same fields as the nvidia-smi query."""
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.index)
+            reasons = getattr(N, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                N.nvmlDeviceGetCurrentClocksThrottleReasons
+            bits = (0x8, 0x40, 0x20, 0x4)  # hw_slowdown, hw_thermal, sw_thermal, sw_power_cap
+
+            def read():
+                r = reasons(h)
+                return [str(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)),
+                        str(N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM))] + \
+                    ["Active" if r & b else "Not Active" for b in bits]
+            read()
+            return read
+        except Exception:
+            return None
+
     def _run(self):
+        read = self._nvml()
+        if read is not None:
+            while not self._stop.is_set():
+                try:
+                    self.samples.append(read())
+                except Exception:
+                    pass
+                self._stop.wait(0.005)
+            return
         q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
