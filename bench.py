@@ -37,6 +37,8 @@ WORKLOADS = {  # name -> (generator kind, n_comms, description)
     "c5": (5, 7, "C5 ring vs tree allreduce sweep, n in 2..8, 1 KiB-1 GiB"),
 }
 RECORD_BYTES = 32
+# one metric string for both arms (the driver divides b200 by reference only when they match)
+METRIC = "trace records/sec -> comm matrix"
 
 
 def parse():
@@ -51,6 +53,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-loader", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=64_000_000)
     ap.add_argument("--ref-sample", type=int, default=2_000_000)
     return ap.parse_args()
@@ -65,15 +68,21 @@ def peaks():
 
 
 def ncu_traffic(workload, records):
-    """dram bytes/launch of the fast kernel (dram__bytes_read.sum + dram__bytes_write.sum from
-    the committed ``ncu --set full`` capture, per record, scaled to this launch), if any."""
+    """dram bytes/launch of the fast kernel: dram__bytes_read.sum + dram__bytes_write.sum per
+    record from the committed ``ncu --set full`` capture (profiles/ncu_traffic.json, taken
+    at the capture's own record count), EXTRAPOLATED linearly to this launch; the source
+    is reported next to it (``traffic_source``).  None when no capture exists."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as fh:
             e = json.load(fh).get(workload)
-        return None if e is None else e["bytes_per_record"] * records
+        if e is None:
+            return None, None
+        src = (f"extrapolated from profiles/ncu_traffic.json ({e.get('records_captured', '?')} records, "
+               f"{e['bytes_per_record']:.3f} B/record)")
+        return e["bytes_per_record"] * records, src
     except Exception:
-        return None
+        return None, None
 
 
 class ClockSampler:
@@ -151,30 +160,51 @@ class ClockSampler:
 
 # --------------------------------------------------------------------------- CPU side
 
+def _jsonl(evs) -> str:
+    """The reference wire format (write_trace, events.py:262-291 key order) of host events."""
+    lines = []
+    for e in evs:
+        o = {"seq": e.seq, "ts": e.ts_ns, "kind": e.kind.value, "comm": e.comm, "nranks": e.n_ranks,
+             "rank": e.rank, "dev": e.device}
+        if e.kind.value == "collective":
+            o.update(coll=e.collective.value, algo=e.algorithm.value, count=e.count, dtype=e.dtype.value)
+            if e.root is not None:
+                o["root"] = e.root
+        else:
+            o.update(ckind=e.copy_kind.value, src={"kind": e.copy_src.kind.value, "idx": e.copy_src.index},
+                     dst={"kind": e.copy_dst.kind.value, "idx": e.copy_dst.index}, bytes=e.bytes)
+        lines.append(json.dumps(o, separators=(",", ":")))
+    return "\n".join(lines) + "\n"
+
+
 def _cpu_worker(args):
     from oracle import commtrace_oracle as O
     from oracle import workload_oracle as W
 
-    lo, hi = args
+    lo, hi, parse = args
     evs = W.c4_events(hi, 8, lo)
-    t0 = time.perf_counter()
-    res = O.analyze(evs)
+    if parse:  # the reference's whole CPU path: parse_trace + analyze_events
+        text = _jsonl(evs).encode()
+        del evs
+        t0 = time.perf_counter()
+        res = O.analyze_flat(O.parse_jsonl(text))
+    else:      # analyze_events on already-parsed events (the drop-in boundary, matrix.py:316)
+        t0 = time.perf_counter()
+        res = O.analyze(evs)
     return time.perf_counter() - t0, hi - lo, res["result"]["instances"]
 
 
-def cpu_reference(sample: int, procs: int):
+def cpu_reference(sample: int, procs: int, parse: bool = False):
     """The reference algorithm (CPU oracle restatement, oracle/commtrace_oracle.py) on
     instance-aligned shards of the first ``sample`` C4 records, one process per core.
-    Returns (records/s, wall seconds)."""
+    Returns (records/s, busy seconds, records)."""
     import multiprocessing as mp
 
     step = (sample // procs) // 8 * 8
-    shards = [(k * step, (k + 1) * step) for k in range(procs)]
-    # events are rebuilt inside each worker (not timed); analysis time is timed
+    shards = [(k * step, (k + 1) * step, parse) for k in range(procs)]
+    # events (and their JSONL text) are built inside each worker, untimed; the path is timed
     with mp.get_context("fork").Pool(procs) as pool:
-        t0 = time.perf_counter()
         out = pool.map(_cpu_worker, shards)
-        wall = time.perf_counter() - t0
     busy = max(t for t, _, _ in out)
     n = sum(k for _, k, _ in out)
     return n / busy, busy, n
@@ -196,16 +226,23 @@ def run_reference(a):
         if time.perf_counter() - t_all > 240:
             break
     v = statistics.median(rates)
+    psample = max(procs * 8, min(sample, a.ref_sample // 4))
+    prate, pbusy, pn = cpu_reference(psample, procs, parse=True)
     line = {
-        "impl": "reference", "metric": "trace records/sec -> comm matrix", "value": v,
+        "impl": "reference", "metric": METRIC, "value": v,
         "unit": "records/s", "n_gpus": a.gpus, "steps": len(rates), "warmup": a.warmup,
         "ms_per_step": 1e3 * sample / v, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-        "config": {"workload": WORKLOADS[a.workload][2], "records_sample": sample},
+        "config": {"workload": WORKLOADS[a.workload][2], "records_sample": sample,
+                   "timed": "analyze_events on parsed events (group + decompose + accumulate); "
+                            "parse_trace excluded -- it is timed separately in parse_analyze"},
         "cpu_baseline": {"value": v, "unit": "records/s", "cores": procs, "kind": "port",
                          "sample": f"first {sample} C4 records (host-built, oracle/workload_oracle.py), "
                                    f"instance-aligned shards over {procs} processes; analysis timed"},
         "e2e": {"value": v, "unit": "records/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "parse_analyze": {"value": prate, "unit": "records/s", "records": pn, "busy_s": pbusy, "cores": procs,
+                          "sample": f"first {psample} C4 records as JSONL (reference wire format); "
+                                    "parse_trace + analyze_events restated (oracle parse_jsonl + analyze_flat)"},
     }
     print(json.dumps(line))
 
@@ -314,14 +351,25 @@ def main():
     check = {"instances": int(sum(result.calls[t] for t in range(5))), "diagnostics": int(sum(result.diag)),
              "d": int(result.d), "path": int(summ.path)}
 
+    timed_cells = None
+    if world == 1 and not a.no_parity:  # the timed step's own result, checked below
+        import numpy as np
+        g2 = summ.g_cap + 2
+        timed_cells = (np.zeros(9 * g2 * g2, np.uint64), np.zeros(9 * g2 * g2, np.uint64))
+        assert lib.ct_result_cells(ctx.handle, timed_cells[0].ctypes.data, timed_cells[1].ctypes.data,
+                                   timed_cells[0].size) == 0, ctx.error()
+        timed_summ = _lib.CtSummary.from_buffer_copy(summ)
+
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu:
         cpu = cpu_baseline_c(buf, min(n, a.cpu_sample), kind, lib)
 
-    e2e = None
-    if not a.no_e2e:
+    host = None
+    if not a.no_e2e or timed_cells is not None:
         host = torch.empty(max(n, 1) * RECORD_BYTES, dtype=torch.uint8, pin_memory=True)
         host.copy_(buf)
+    e2e = None
+    if not a.no_e2e:
         del buf
         torch.cuda.empty_cache()
         e_steps = max(1, min(a.steps, 5))
@@ -331,13 +379,19 @@ def main():
                "d2h_bytes_per_step": d2h, "ms_per_step": ems, "steps": e_steps,
                "source": "pinned host buffers through ct_analyze (H2D inside the timed region)"}
 
+    parity = None
+    if timed_cells is not None:
+        parity = parity_check(host, n, kind, lib, timed_summ, timed_cells)
+    del host
+
     loader = None
     if rank == 0 and world == 1 and not a.no_loader:
         loader = loader_measure(ctx)
 
+    traffic, traffic_src = ncu_traffic(a.workload, n)
     if rank == 0:
         line = {
-            "metric": "trace records/sec -> comm matrix (device-timed)",
+            "metric": METRIC,
             "value": value, "unit": "records/s", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "int64", "data": "synthetic",
@@ -345,7 +399,8 @@ def main():
                        "sharding": "record range, element-aligned", "l2": "inputs larger than L2 (32 GB at 1B records)",
                        "seed": a.seed},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak if achieved else None, "traffic": ncu_traffic(a.workload, n),
+                         "frac": achieved / peak if achieved else None, "traffic": traffic,
+                         "traffic_source": traffic_src,
                          "kernel": "ct::fast_kernel", "kernel_ms": kms, "peak_source": peak_kind,
                          "algorithmic_bytes_per_launch": n * RECORD_BYTES},
             "cpu_baseline": cpu,
@@ -353,6 +408,7 @@ def main():
             "gpu_launches": launches,
             "clocks": clocks,
             "result_check": check,
+            "parity": parity,
             "loader": loader,
         }
         print(json.dumps(line))
@@ -399,6 +455,35 @@ def loader_measure(ctx, blk=20_000, reps=50):
                 "api": "load_trace (JSONL -> records in HBM; device time = CUDA events around ct_jsonl_parse)"}
     except Exception as exc:  # reported, never fatal for the headline line
         return {"error": repr(exc)[:300]}
+
+
+def parity_check(host, n, kind, lib, summ, cells):
+    """The timed step's result (cells, frequencies, calls, 128-bit payloads, diagnostics,
+    d) against oracle/ct_oracle.c over the WHOLE trace, outside the timed region (all
+    host threads over element-aligned shards, merged exactly)."""
+    import numpy as np
+    from oracle import c_oracle as CO
+    from paper_2110_10401_b200.packed import RECORD_DTYPE
+
+    recs = host.numpy().view(RECORD_DTYPE)[:n]
+    threads = os.cpu_count() or 1
+    k = max(threads, 64)
+    bounds = sorted({0, n} | {lib.ct_generate_boundary(kind, n * j // k) for j in range(1, k)})
+    t0 = time.perf_counter()
+    want = CO.analyze_threads(recs, bounds, threads, gcap=summ.g_cap)
+    dt = time.perf_counter() - t0
+    cb, cf = cells
+    checks = {
+        "status": want["status"] == 0,
+        "d": int(summ.d) == int(want["d"]),
+        "cells": bool(np.array_equal(cb.astype(object), np.asarray(want["cells"], dtype=object))),
+        "freq": bool(np.array_equal(cf, want["freq"])),
+        "calls": [int(x) for x in summ.calls] == [int(x) for x in want["calls"]],
+        "payload": [int(summ.payload_lo[t]) + (int(summ.payload_hi[t]) << 64) for t in range(9)] == want["payload"],
+        "diag": [int(x) for x in summ.diag] == [int(x) for x in want["diag"]],
+    }
+    return {"ok": all(checks.values()), "checks": checks, "records": n, "oracle": "oracle/ct_oracle.c",
+            "oracle_s": round(dt, 2), "threads": threads}
 
 
 def cpu_baseline_c(buf, sample, kind, lib):

@@ -86,6 +86,124 @@ def flatten(events) -> list[Ev]:
     return out
 
 
+# ---------------------------------------------------------------- loader
+
+_KINDS = ("collective", "send", "recv", "memcpy", "um", "zerocopy")
+_COLLS = ("allreduce", "broadcast", "reduce", "reducescatter", "allgather")
+_ALGOS = ("ring", "tree", "collnet", "auto")
+_DTYPES = ("int8", "uint8", "int32", "uint32", "int64", "uint64", "float16", "bfloat16", "float32", "float64")
+_CKINDS = {"h2d": ("host", "gpu"), "d2h": ("gpu", "host"), "d2d": ("gpu", "gpu")}
+
+
+def _need(obj, key, typ, line_no):
+    """events.py:294-301: present, of the JSON type, and never a bool."""
+    if key not in obj:
+        raise OracleError("SchemaViolation", f"line {line_no}: field {key!r} missing")
+    v = obj[key]
+    if not isinstance(v, typ) or isinstance(v, bool):
+        raise OracleError("SchemaViolation", f"line {line_no}: field {key!r} expected {typ.__name__}")
+    return v
+
+
+def _need_enum(obj, key, values, line_no):
+    """events.py:304-309."""
+    v = _need(obj, key, str, line_no)
+    if v not in values:
+        raise OracleError("SchemaViolation", f"line {line_no}: field {key!r} unknown value {v!r}")
+    return v
+
+
+def _need_ep(obj, key, line_no):
+    """events.py:312-319 (Endpoint.__post_init__ events.py:52-56)."""
+    raw = _need(obj, key, dict, line_no)
+    kind = _need_enum(raw, "kind", ("host", "gpu", "net"), line_no)
+    idx = _need(raw, "idx", int, line_no)
+    if idx < 0 or (kind != "gpu" and idx != 0):
+        raise OracleError("SchemaViolation", f"line {line_no}: field {key!r} bad endpoint")
+    return (kind, idx)
+
+
+def _validate(e: "Ev", line_no):
+    """TraceEvent.validate (events.py:166-236), messages shortened."""
+    bad = None
+    if e.n < 1 or not 0 <= e.rank < e.n or e.seq < 0 or e.dev < 0:
+        bad = "rank / nranks / seq / dev"
+    elif e.kind == "collective":
+        if e.count < 0 or (e.algo in ("tree", "collnet") and e.coll != "allreduce"):
+            bad = "count / algo"
+        elif e.coll in ("broadcast", "reduce"):
+            if e.root is None or not 0 <= e.root < e.n:
+                bad = "root"
+        elif e.root is not None:
+            bad = "root"
+    elif e.kind in ("send", "recv"):
+        if e.peer == e.rank or not 0 <= e.peer < e.n or e.count < 0:
+            bad = "peer / count"
+    else:
+        if e.nbytes < 0 or (e.src[0], e.dst[0]) != _CKINDS[e.ckind] or (e.ckind == "d2d" and e.src == e.dst):
+            bad = "copy"
+    if bad:
+        raise OracleError("InvariantViolation", f"line {line_no}: {bad}")
+
+
+def parse_jsonl(text) -> list:
+    """parse_trace (events.py:352-384) restated to flat ``Ev`` rows: UTF-8 decode,
+    str.splitlines, skip blank lines, json.loads, the field readers of
+    _event_from_obj (events.py:322-349) and validate.  Used to time the reference's
+    whole CPU path (parse + analyze) in bench.py's reference arm."""
+    import json
+
+    if isinstance(text, (bytes, bytearray)):
+        text = text.decode("utf-8")
+    out = []
+    for line_no, line in enumerate(text.splitlines(), start=1):
+        if not line.strip():
+            continue
+        try:
+            obj = json.loads(line)
+        except json.JSONDecodeError as exc:
+            raise OracleError("MalformedLine", f"line {line_no}: not a valid JSON object ({exc.msg})") from None
+        if not isinstance(obj, dict):
+            raise OracleError("MalformedLine", f"line {line_no}: not a valid JSON object (not a JSON object)")
+        kind = _need_enum(obj, "kind", _KINDS, line_no)
+        seq = _need(obj, "seq", int, line_no)
+        _need(obj, "ts", int, line_no)
+        comm = _need(obj, "comm", str, line_no)
+        n = _need(obj, "nranks", int, line_no)
+        rank = _need(obj, "rank", int, line_no)
+        dev = _need(obj, "dev", int, line_no)
+        coll = algo = count = dtype = root = peer = src = dst = nbytes = ckind = None
+        if kind == "collective":
+            coll = _need_enum(obj, "coll", _COLLS, line_no)
+            algo = _need_enum(obj, "algo", _ALGOS, line_no)
+            count = _need(obj, "count", int, line_no)
+            dtype = _need_enum(obj, "dtype", _DTYPES, line_no)
+            if "root" in obj or coll in ("broadcast", "reduce"):
+                root = _need(obj, "root", int, line_no)
+        elif kind in ("send", "recv"):
+            peer = _need(obj, "peer", int, line_no)
+            count = _need(obj, "count", int, line_no)
+            dtype = _need_enum(obj, "dtype", _DTYPES, line_no)
+        else:
+            ckind = _need_enum(obj, "ckind", tuple(_CKINDS), line_no)
+            src = _need_ep(obj, "src", line_no)
+            dst = _need_ep(obj, "dst", line_no)
+            nbytes = _need(obj, "bytes", int, line_no)
+        e = Ev(len(out), kind, comm, n, rank, dev, seq, coll, algo, count, dtype, root, peer, src, dst, nbytes)
+        e.ckind = ckind
+        _validate(e, line_no)
+        out.append(e)
+    return out
+
+
+def analyze_flat(evs, d=None, ring_order=None, tree_threshold=1 << 20):
+    """``analyze`` on already-flat rows (from parse_jsonl)."""
+    try:
+        return _analyze(evs, d, ring_order, tree_threshold)
+    except OracleError as exc:
+        return {"error": {"type": exc.kind, "message": exc.message}}
+
+
 # ---------------------------------------------------------------- grouping
 
 def group(evs: list[Ev]):

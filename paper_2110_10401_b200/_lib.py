@@ -213,3 +213,11 @@ def records_pointer(records) -> tuple[int, int, int]:
         nbytes = records.numel() * records.element_size()
         return records.data_ptr(), nbytes // 32, 1
     raise TypeError("records must be a numpy RECORD_DTYPE array or a CUDA tensor of packed records")
+
+
+def torch_stream(tensor):
+    """torch's current stream on ``tensor``'s device as a ctypes handle: the library then
+    runs after every torch kernel already queued there (the records' producers)."""
+    import torch
+
+    return C.c_void_p(torch.cuda.current_stream(tensor.device).cuda_stream)

@@ -17,9 +17,13 @@
  * which only groups ranks living in one process.  Here a communicator created by
  * ncclCommInitRank[Config] is named after a hash of its ncclUniqueId (identical on
  * every rank of the communicator, so one-process-per-GPU jobs group correctly), a
- * ncclCommSplit child after (parent id, color), ncclCommInitAll after the nonce + the
+ * ncclCommSplit child after (parent id, color, k) with k the parent's split counter
+ * (splits are collective over the parent, so k agrees on every rank and repeated
+ * splits with one color get distinct ids), ncclCommInitAll after the nonce + the
  * first handle; a communicator the shim never saw created falls back to address +
- * nonce.  "algo" is "auto" (not observable at the API; the analyzer selects it).
+ * nonce.  Communicators are named when creation returns ncclSuccess or
+ * ncclInProgress (non-blocking init); ncclCommDestroy / ncclCommAbort free their
+ * table entry (a full table warns once and leaves new communicators unlogged).  "algo" is "auto" (not observable at the API; the analyzer selects it).
  * Thread safety: per-call formatting in a stack buffer, a mutex around the
  * communicator table, atomic per-communicator sequence counters.
  */
@@ -120,13 +124,19 @@ static int comm_int(const char* name, ncclComm_t comm) {
 /* ------------------------------------------------------- communicator table */
 
 #define TABLE_SIZE 4096
+#define NCCL_IN_PROGRESS 7 /* ncclInProgress: non-blocking creation still running */
+#define TOMBSTONE ((ncclComm_t)(uintptr_t)1)
 typedef struct {
-  ncclComm_t comm;
+  ncclComm_t comm;              /* NULL: never used; TOMBSTONE: freed */
   unsigned long long id;
   unsigned long long seq;
+  unsigned long long splits;    /* ncclCommSplit calls on this communicator */
 } Entry;
 static Entry g_table[TABLE_SIZE];
 static pthread_mutex_t g_mu = PTHREAD_MUTEX_INITIALIZER;
+static int g_full_warned = 0;
+
+static int created(ncclResult_t r) { return r == 0 || r == NCCL_IN_PROGRESS; }
 
 static unsigned long long mix(unsigned long long h, const void* p, size_t n) {
   const unsigned char* b = (const unsigned char*)p;
@@ -134,26 +144,49 @@ static unsigned long long mix(unsigned long long h, const void* p, size_t n) {
   return h;
 }
 
+/* open addressing with tombstones (entries of destroyed communicators); g_mu held */
 static Entry* slot(ncclComm_t comm, int create) {
   size_t h = (size_t)(((uintptr_t)comm >> 4) * 0x9E3779B97F4A7C15ull) % TABLE_SIZE;
+  Entry* reuse = NULL;
   for (size_t i = 0; i < TABLE_SIZE; i++) {
     Entry* e = &g_table[(h + i) % TABLE_SIZE];
     if (e->comm == comm) return e;
+    if (e->comm == TOMBSTONE) {
+      if (!reuse) reuse = e;
+      continue;
+    }
     if (!e->comm) {
-      if (!create) return NULL;
-      e->comm = comm;
-      e->id = mix(0xcbf29ce484222325ull ^ g_nonce, &comm, sizeof(comm));  /* fallback name */
-      e->seq = 0;
-      return e;
+      if (!reuse) reuse = e;
+      break;
     }
   }
-  return NULL;
+  if (!create) return NULL;
+  if (!reuse) {
+    if (!g_full_warned) {
+      g_full_warned = 1;
+      fprintf(stderr, "comscribe: communicator table full (%d live); calls on new communicators are not logged\n",
+              TABLE_SIZE);
+    }
+    return NULL;
+  }
+  reuse->comm = comm;
+  reuse->id = mix(0xcbf29ce484222325ull ^ g_nonce, &comm, sizeof(comm));  /* fallback name */
+  reuse->seq = 0;
+  reuse->splits = 0;
+  return reuse;
+}
+
+static void forget_comm(ncclComm_t comm) {
+  pthread_mutex_lock(&g_mu);
+  Entry* e = slot(comm, 0);
+  if (e) e->comm = TOMBSTONE;
+  pthread_mutex_unlock(&g_mu);
 }
 
 static void name_comm(ncclComm_t comm, unsigned long long id) {
   pthread_mutex_lock(&g_mu);
   Entry* e = slot(comm, 1);
-  if (e) { e->id = id; e->seq = 0; }
+  if (e) { e->id = id; e->seq = 0; e->splits = 0; }
   pthread_mutex_unlock(&g_mu);
 }
 
@@ -209,7 +242,7 @@ SHIM_EXPORT ncclResult_t ncclCommInitRank(ncclComm_t* comm, int nranks, ncclUniq
   REAL(ncclCommInitRank);
   if (!p_ncclCommInitRank) return 1;
   ncclResult_t r = p_ncclCommInitRank(comm, nranks, id, rank);
-  if (r == 0 && comm && *comm) name_comm(*comm, mix(0xcbf29ce484222325ull, id.internal, sizeof id.internal));
+  if (created(r) && comm && *comm) name_comm(*comm, mix(0xcbf29ce484222325ull, id.internal, sizeof id.internal));
   return r;
 }
 
@@ -218,7 +251,7 @@ SHIM_EXPORT ncclResult_t ncclCommInitRankConfig(ncclComm_t* comm, int nranks, nc
   REAL(ncclCommInitRankConfig);
   if (!p_ncclCommInitRankConfig) return 1;
   ncclResult_t r = p_ncclCommInitRankConfig(comm, nranks, id, rank, config);
-  if (r == 0 && comm && *comm) name_comm(*comm, mix(0xcbf29ce484222325ull, id.internal, sizeof id.internal));
+  if (created(r) && comm && *comm) name_comm(*comm, mix(0xcbf29ce484222325ull, id.internal, sizeof id.internal));
   return r;
 }
 
@@ -226,7 +259,7 @@ SHIM_EXPORT ncclResult_t ncclCommInitAll(ncclComm_t* comms, int ndev, const int*
   REAL(ncclCommInitAll);
   if (!p_ncclCommInitAll) return 1;
   ncclResult_t r = p_ncclCommInitAll(comms, ndev, devlist);
-  if (r == 0 && ndev > 0) {
+  if (created(r) && ndev > 0) {
     pthread_once(&g_once, shim_init);
     const unsigned long long id = mix(0xcbf29ce484222325ull ^ g_nonce, &comms[0], sizeof comms[0]);
     for (int i = 0; i < ndev; i++) name_comm(comms[i], id);
@@ -238,15 +271,26 @@ SHIM_EXPORT ncclResult_t ncclCommSplit(ncclComm_t comm, int color, int key, nccl
                                        ncclConfig_t* config) {
   REAL(ncclCommSplit);
   if (!p_ncclCommSplit) return 1;
-  unsigned long long parent = 0, unused = 0;
+  unsigned long long parent = 0, k = 0;
   pthread_mutex_lock(&g_mu);
   Entry* e = slot(comm, 1);
-  if (e) parent = e->id;
+  if (e) { parent = e->id; k = e->splits++; }
   pthread_mutex_unlock(&g_mu);
-  (void)unused;
   ncclResult_t r = p_ncclCommSplit(comm, color, key, newcomm, config);
-  if (r == 0 && newcomm && *newcomm) name_comm(*newcomm, mix(parent, &color, sizeof color));
+  if (created(r) && newcomm && *newcomm) name_comm(*newcomm, mix(mix(parent, &color, sizeof color), &k, sizeof k));
   return r;
+}
+
+SHIM_EXPORT ncclResult_t ncclCommDestroy(ncclComm_t comm) {
+  REAL(ncclCommDestroy);
+  forget_comm(comm);
+  return p_ncclCommDestroy ? p_ncclCommDestroy(comm) : 1;
+}
+
+SHIM_EXPORT ncclResult_t ncclCommAbort(ncclComm_t comm) {
+  REAL(ncclCommAbort);
+  forget_comm(comm);
+  return p_ncclCommAbort ? p_ncclCommAbort(comm) : 1;
 }
 
 /* ----------------------------------------------------------- collectives */

@@ -429,6 +429,7 @@ int ct_analyze(ct_context* c, const ct_record* recs, uint64_t n, int on_device, 
   bool ran_exact = false;
   auto do_exact = [&]() -> int {
     int e = exact_canonicalize(d_recs, n, n_comms, st, false, &ex_res);
+    if (e == kExactCapacity) return fail(c, CT_ERR_CAPACITY, "exact path: 2^32 or more collective records");
     if (e) return cuda_fail(c, (cudaError_t)e, "exact path");
     launches += ex_res.launches;
     ran_exact = true;
@@ -513,6 +514,7 @@ static int ensure_materialized(ct_context* c) {
   if (c->mat_valid) return 0;
   c->mat = ExactResult();
   int e = exact_canonicalize(c->last_input, c->last_n, c->last_comms, c->stream, true, &c->mat);
+  if (e == kExactCapacity) return fail(c, CT_ERR_CAPACITY, "materialize: 2^32 or more collective records");
   if (e) return cuda_fail(c, (cudaError_t)e, "materialize");
   if (c->mat.canon) cudaFreeAsync(c->mat.canon, c->stream);
   c->mat.canon = nullptr;

@@ -155,10 +155,10 @@ __global__ void k_comm_rank(const uint32_t* sorted_comms, uint64_t n, uint32_t* 
 
 // per group run: emitted length (n if complete), status for materialisation
 __global__ void k_group_runs(const ct_record* recs, const uint64_t* idx, const uint64_t* run_off,
-                             const int64_t* run_len, const int* n_runs, uint64_t* emit_len,
+                             const int64_t* run_len, const uint64_t* n_runs, uint64_t* emit_len,
                              uint64_t* status, unsigned long long* n_incomplete) {
-  const int R = *n_runs;
-  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < R; k += gridDim.x * blockDim.x) {
+  const uint64_t R = *n_runs;
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < R; k += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t off = run_off[k];
     const uint64_t len = (uint64_t)run_len[k];
     const ct_record& h = recs[idx[off]];
@@ -185,10 +185,10 @@ __global__ void k_group_runs(const ct_record* recs, const uint64_t* idx, const u
 }
 
 __global__ void k_emit_groups(const ct_record* recs, const uint64_t* idx, const uint64_t* run_off,
-                              const int64_t* run_len, const int* n_runs, const uint64_t* emit_off,
+                              const int64_t* run_len, const uint64_t* n_runs, const uint64_t* emit_off,
                               const uint64_t* emit_len, ct_record* out, uint64_t* src_map) {
-  const int R = *n_runs;
-  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < R; k += gridDim.x * blockDim.x) {
+  const uint64_t R = *n_runs;
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < R; k += (uint64_t)gridDim.x * blockDim.x) {
     if (!emit_len[k]) continue;
     const uint64_t off = run_off[k], len = (uint64_t)run_len[k], o = emit_off[k];
     for (uint64_t a = 0; a < len; a++) {
@@ -199,10 +199,10 @@ __global__ void k_emit_groups(const ct_record* recs, const uint64_t* idx, const 
 }
 
 // p2p channel runs: pair the k-th send with the k-th recv of each channel
-__global__ void k_p2p_runs(const uint64_t* ukey, const int64_t* run_len, const int* n_runs,
+__global__ void k_p2p_runs(const uint64_t* ukey, const int64_t* run_len, const uint64_t* n_runs,
                            uint64_t* emit_len, unsigned long long* n_us, unsigned long long* n_ur) {
-  const int R = *n_runs;
-  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < R; k += gridDim.x * blockDim.x) {
+  const uint64_t R = *n_runs;
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < R; k += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t key = ukey[k];
     uint64_t s = 0, r = 0;
     emit_len[k] = 0;
@@ -221,20 +221,20 @@ __global__ void k_p2p_runs(const uint64_t* ukey, const int64_t* run_len, const i
 }
 
 __global__ void k_emit_pairs(const ct_record* recs, const uint64_t* idx, const uint64_t* run_off,
-                             const int64_t* run_len, const int* n_runs, const uint64_t* emit_off,
+                             const int64_t* run_len, const uint64_t* n_runs, const uint64_t* emit_off,
                              const uint64_t* emit_len, uint64_t base, uint64_t n_pairs, ct_record* out,
                              uint64_t* src_map) {
   // one thread per emitted pair: its channel run is the last run whose output offset is
   // <= 2j (runs are laid out back to back in emit_off order)
-  const int R = *n_runs;
+  const uint64_t R = *n_runs;
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n_pairs;
        j += (uint64_t)gridDim.x * blockDim.x) {
-    int lo = 0, hi = R - 1;
+    int64_t lo = 0, hi = (int64_t)R - 1;
     while (lo < hi) {
-      const int mid = (lo + hi + 1) / 2;
+      const int64_t mid = (lo + hi + 1) / 2;
       if (emit_off[mid] <= 2 * j) lo = mid; else hi = mid - 1;
     }
-    const int k = lo;
+    const int64_t k = lo;
     const uint64_t local = j - emit_off[k] / 2, soff = run_off[k], roff = run_off[k + 1];
     const uint64_t o = base + 2 * j;
     out[o] = recs[idx[soff + local]];
@@ -245,10 +245,10 @@ __global__ void k_emit_pairs(const ct_record* recs, const uint64_t* idx, const u
 
 // materialisation: count/dtype disagreement of every FIFO pair (decompose.py:362)
 __global__ void k_pair_mismatch(const ct_record* recs, const uint64_t* idx, const uint64_t* run_off,
-                                const uint64_t* emit_len, const int* n_runs, uint8_t* mis,
+                                const uint64_t* emit_len, const uint64_t* n_runs, uint8_t* mis,
                                 const uint64_t* emit_off) {
-  const int R = *n_runs;
-  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < R; k += gridDim.x * blockDim.x) {
+  const uint64_t R = *n_runs;
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < R; k += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t pairs = emit_len[k] / 2, soff = run_off[k], roff = run_off[k + 1];
     for (uint64_t j = 0; j < pairs; j++) {
       const ct_record& a = recs[idx[soff + j]];
@@ -318,12 +318,39 @@ int select_flagged(Pool& pool, const uint8_t* flags, uint64_t n, uint64_t* out, 
   return 0;
 }
 
-int rle(Pool& pool, const uint64_t* keys, uint64_t m, uint64_t* uniq, int64_t* lens, int* d_runs) {
+// run-length encoding of sorted keys with 64-bit item and run counts (CUB's
+// DeviceRunLengthEncode takes an int item count): run heads are flagged and selected
+// (64-bit DeviceSelect), giving the unique keys, run lengths and run offsets at once
+__global__ void k_run_heads(const uint64_t* keys, uint64_t m, uint8_t* flag) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x)
+    flag[i] = i == 0 || keys[i] != keys[i - 1];
+}
+
+__global__ void k_run_fill(const uint64_t* keys, const uint64_t* heads, const uint64_t* n_runs, uint64_t m,
+                           uint64_t* uniq, int64_t* lens) {
+  const uint64_t R = *n_runs;
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < R; k += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t h = heads[k], nx = k + 1 < R ? heads[k + 1] : m;
+    uniq[k] = keys[h];
+    lens[k] = (int64_t)(nx - h);
+  }
+}
+
+
+int rle(Pool& pool, const uint64_t* keys, uint64_t m, uint64_t* uniq, int64_t* lens, uint64_t* offs,
+        uint64_t* d_runs, uint64_t* runs_host) {
+  uint8_t* flag = pool.get<uint8_t>(m);
+  if (!flag) return (int)cudaErrorMemoryAllocation;
+  k_run_heads<<<grid_for(m), 256, 0, pool.st>>>(keys, m, flag);
   size_t tmp = 0;
-  CT_TRY(cub::DeviceRunLengthEncode::Encode(nullptr, tmp, keys, uniq, lens, d_runs, (int)m, pool.st));
+  thrust::counting_iterator<uint64_t> it(0);
+  CT_TRY(cub::DeviceSelect::Flagged(nullptr, tmp, it, flag, offs, d_runs, (int64_t)m, pool.st));
   void* t = pool.get<uint8_t>(tmp);
   if (!t) return (int)cudaErrorMemoryAllocation;
-  CT_TRY(cub::DeviceRunLengthEncode::Encode(t, tmp, keys, uniq, lens, d_runs, (int)m, pool.st));
+  CT_TRY(cub::DeviceSelect::Flagged(t, tmp, it, flag, offs, d_runs, (int64_t)m, pool.st));
+  k_run_fill<<<grid_for(m), 256, 0, pool.st>>>(keys, offs, d_runs, m, uniq, lens);
+  CT_TRY(cudaMemcpyAsync(runs_host, d_runs, 8, cudaMemcpyDeviceToHost, pool.st));
+  CT_TRY(cudaStreamSynchronize(pool.st));
   return 0;
 }
 
@@ -347,7 +374,6 @@ int exact_canonicalize(const ct_record* recs, uint64_t n, uint32_t n_comms, cuda
                        bool materialize, ExactResult* res) {
   Pool pool{st, {}};
   uint32_t L = 0;
-  if (n > (uint64_t)INT32_MAX) return (int)cudaErrorInvalidValue;  // RLE item limit
   uint8_t* fc = pool.get<uint8_t>(n);
   uint8_t* fp = pool.get<uint8_t>(n);
   uint8_t* fx = pool.get<uint8_t>(n);
@@ -456,17 +482,17 @@ int exact_canonicalize(const ct_record* recs, uint64_t n, uint32_t n_comms, cuda
                                              cids_sorted, (uint64_t)n_comms, 0, 64, st));
     }
     k_comm_rank<<<grid_for(n_comms), 256, 0, st>>>(cids_sorted, n_comms, comm_rank);
+    if (nc >> 32) return kExactCapacity;  // ordinals are 32-bit in the group key
     k_group_keys<<<grid_for(nc), 256, 0, st>>>(recs, order, seg, nc, comm_rank, k1);
     uint64_t* gorder = pool.get<uint64_t>(nc);
     if ((e = sort_pairs(pool, k1, k2, order, gorder, nc, 64))) return e;
     L += 5;
     uint64_t* ukey = pool.get<uint64_t>(nc);
     int64_t* rlen = pool.get<int64_t>(nc);
-    int* d_runs = pool.get<int>(1);
-    if ((e = rle(pool, k2, nc, ukey, rlen, d_runs))) return e;
-    const int R = read1(d_runs, st);
-    uint64_t* roff = pool.get<uint64_t>(R + 1);
-    if ((e = excl_sum(pool, rlen, roff, R))) return e;
+    uint64_t* d_runs = pool.get<uint64_t>(1);
+    uint64_t* roff = pool.get<uint64_t>(nc + 1);
+    uint64_t R = 0;
+    if ((e = rle(pool, k2, nc, ukey, rlen, roff, d_runs, &R))) return e;
     uint64_t* elen = pool.get<uint64_t>(R + 1);
     uint64_t* eoff = pool.get<uint64_t>(R + 1);
     uint64_t* gstat = pool.get<uint64_t>(R + 1);
@@ -498,7 +524,7 @@ int exact_canonicalize(const ct_record* recs, uint64_t n, uint32_t n_comms, cuda
       cudaMemcpyAsync(h_sorted.data(), cids_sorted, (size_t)n_comms * 4, cudaMemcpyDeviceToHost, st);
       cudaStreamSynchronize(st);
       res->members = h_members;
-      for (int k = 0; k < R; k++) {
+      for (uint64_t k = 0; k < R; k++) {
         GroupRow g;
         g.comm = h_sorted[h_ukey[k] >> 32];
         g.ordinal = h_ukey[k] & 0xFFFFFFFFull;
@@ -536,11 +562,10 @@ int exact_canonicalize(const ct_record* recs, uint64_t n, uint32_t n_comms, cuda
     if ((e = sort_pairs(pool, k1, k2, v1, v2, np, 64))) return e;
     uint64_t* ukey = pool.get<uint64_t>(np);
     int64_t* rlen = pool.get<int64_t>(np);
-    int* d_runs = pool.get<int>(1);
-    if ((e = rle(pool, k2, np, ukey, rlen, d_runs))) return e;
-    const int R = read1(d_runs, st);
-    uint64_t* roff = pool.get<uint64_t>(R + 1);
-    if ((e = excl_sum(pool, rlen, roff, R))) return e;
+    uint64_t* d_runs = pool.get<uint64_t>(1);
+    uint64_t* roff = pool.get<uint64_t>(np + 1);
+    uint64_t R = 0;
+    if ((e = rle(pool, k2, np, ukey, rlen, roff, d_runs, &R))) return e;
     uint64_t* elen = pool.get<uint64_t>(R + 1);
     uint64_t* eoff = pool.get<uint64_t>(R + 1);
     unsigned long long* nus = pool.get<unsigned long long>(2);
@@ -578,7 +603,7 @@ int exact_canonicalize(const ct_record* recs, uint64_t n, uint32_t n_comms, cuda
         cudaMemcpyAsync(pair_map.data(), pmap, pair_total * 8, cudaMemcpyDeviceToHost, st);
       }
       cudaStreamSynchronize(st);
-      for (int k = 0; k < R; k++) {
+      for (uint64_t k = 0; k < R; k++) {
         const uint64_t key = h_ukey[k];
         uint64_t s = 0, r = 0, so = 0, ro = 0;
         if ((key & 1) == 0) {

@@ -44,6 +44,10 @@ struct ExactResult {
 
 // Returns cudaError_t as int; ``res`` filled.  ``materialize`` also returns the
 // group / diagnostic lists and the canonical->original index map.
+// exact_canonicalize's return value when a per-(comm, rank) ordinal would not fit the
+// 32-bit group key (>= 2^32 collective records): the caller reports CT_ERR_CAPACITY
+constexpr int kExactCapacity = 0x7FFF0001;
+
 int exact_canonicalize(const ct_record* recs, uint64_t n, uint32_t n_comms, cudaStream_t st,
                        bool materialize, ExactResult* res);
 

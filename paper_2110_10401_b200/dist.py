@@ -53,7 +53,14 @@ def analyze_sharded(records, n_comms: int = 1, d=None, dev_hint: int = 8, tree_t
     cfg = _lib.make_config(d=d, tree_threshold=tree_threshold, ring_order=ring_order, dev_hint=dev_hint,
                            n_comms=n_comms)
     s = _lib.CtSummary()
-    st = C.c_void_p(stream) if stream else None
+    # Everything runs on ONE stream -- torch's current one unless the caller names
+    # another: the async export, the NCCL all-gather (enqueued by torch on its current
+    # stream) and the merge are then ordered without extra events.
+    if stream is None:
+        stream = torch.cuda.current_stream().cuda_stream
+    elif stream != torch.cuda.current_stream().cuda_stream:
+        torch.cuda.current_stream().synchronize()  # records written by torch work
+    st = C.c_void_p(stream)
     rc = ctx.lib.ct_analyze(ctx.handle, C.c_void_p(ptr), n, on_dev, C.byref(cfg), C.byref(s), st)
     ctx.check(rc, "ct_analyze")
     words = C.c_uint64()
@@ -62,11 +69,17 @@ def analyze_sharded(records, n_comms: int = 1, d=None, dev_hint: int = 8, tree_t
     rc = ctx.lib.ct_partial_export(ctx.handle, C.c_void_p(part.data_ptr()), words.value, st)
     ctx.check(rc, "ct_partial_export")
     backend = dist.get_backend(group)
+    cur = torch.cuda.current_stream()
+    if stream != cur.cuda_stream:  # the export ran on the caller's stream: order the gather after it
+        ev = torch.cuda.ExternalStream(stream)
+        cur.wait_stream(ev)
     if backend == "nccl":
         allp = gather_partials(part, group)
     else:  # gloo and friends gather host tensors
         torch.cuda.synchronize()
         allp = gather_partials(part.cpu(), group).cuda()
+    if stream != cur.cuda_stream:  # and the merge after the gather
+        torch.cuda.ExternalStream(stream).wait_stream(cur)
     merged = _lib.CtSummary()
     rc = ctx.lib.ct_partial_merge(ctx.handle, C.c_void_p(allp.data_ptr()), dist.get_world_size(group),
                                   words.value, C.byref(merged), st)

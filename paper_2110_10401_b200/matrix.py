@@ -281,7 +281,10 @@ def analyze_packed(trace, d=None, config=None, *, device=None, force_path=_lib.F
     cfg = _lib.make_config(d=d, tree_threshold=config.tree_threshold, ring_order=config.ring_order,
                            force_path=force_path, dev_hint=dev_hint, n_comms=n_comms)
     summ = _lib.CtSummary()
-    rc = ctx.lib.ct_analyze(ctx.handle, C.c_void_p(ptr), n, on_dev, C.byref(cfg), C.byref(summ), None)
+    # CUDA records: run on torch's current stream so kernels that wrote them (clone,
+    # cat, index copies in cli / loader) are ordered before the analysis
+    stream = _lib.torch_stream(records) if on_dev else None
+    rc = ctx.lib.ct_analyze(ctx.handle, C.c_void_p(ptr), n, on_dev, C.byref(cfg), C.byref(summ), stream)
     ctx.check(rc, "ct_analyze")
     if rc != _lib.CT_OK:
         raise_status(summ, trace if isinstance(trace, PackedTrace) else None, config)
@@ -357,11 +360,29 @@ def _instances_trace(instances, events) -> PackedTrace:
     return pack_events(synth + others)
 
 
+def _list_type_order(instances, events, per: dict) -> dict:
+    """Re-key a per-type dict into the reference's first-occurrence order over the
+    caller's lists (matrix.py:225-247, 271-276): collective types by their first
+    instance in ``instances`` (list order), then sendrecv, then the copy types by their
+    first event -- not by the device's comm-major grouping order."""
+    rank = {}
+    for k, inst in enumerate(instances):
+        rank.setdefault(getattr(inst.collective, "value", inst.collective), k)
+    rank[SENDRECV] = len(instances)
+    copy_type = {"memcpy": EXPLICIT, "um": UNIFIED, "zerocopy": ZEROCOPY}
+    for k, ev in enumerate(events):
+        t = copy_type.get(getattr(ev.kind, "value", ev.kind))
+        if t is not None:
+            rank.setdefault(t, len(instances) + 1 + k)
+    return {t: per[t] for t in sorted(per, key=rank.__getitem__)}
+
+
 def split_by_primitive(instances, events, d=None, config: ModelConfig = ModelConfig()) -> dict:
     """One matrix per communication type present (matrix.py:261-276)."""
     if d is None:
         d = infer_device_count(events)
-    return analyze_packed(_instances_trace(instances, events), d=d, config=config).per_primitive
+    per = analyze_packed(_instances_trace(instances, events), d=d, config=config).per_primitive
+    return _list_type_order(instances, events, per)
 
 
 def summarize(instances, events, config: ModelConfig = ModelConfig(), diagnostics=None) -> StatsSummary:

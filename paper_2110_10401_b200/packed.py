@@ -32,7 +32,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .errors import InvariantViolation
+from .errors import RecordRangeError
 from .events import (
     Algorithm,
     CollectiveKind,
@@ -124,7 +124,7 @@ class PackedTrace:
 
 def _check_range(val: int, hi: int, what: str) -> int:
     if val < 0 or val > hi:
-        raise InvariantViolation(f"{what} {val} does not fit the packed record range [0, {hi}]")
+        raise RecordRangeError(f"{what} {val} does not fit the packed record range [0, {hi}]")
     return val
 
 

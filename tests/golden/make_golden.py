@@ -14,6 +14,13 @@ Fixtures (all gzip'd JSON):
   decomp_grid.json.gz acceptance grid N in [1,16] x S in [0,257] (test_acceptance.py:82-119)
   random_insts.json.gz 10,000 seeded instances (test_acceptance.py:130-163)
   loader.json.gz      loader error cases (events.py:352-384)
+  loader_fuzz.json.gz the seeded fuzz corpus of tests/loader_fuzz.py with the reference
+                      reader's events or exception per text (str and bytes input)
+  siblings.json.gz    split_by_primitive / summarize on caller-ordered instance lists
+                      (comm-major, shuffled, reversed), infer_device_count, merge and
+                      accumulate (matrix.py:157-301)
+
+    python tests/golden/make_golden.py [fixture ...]   (default: all)
 """
 
 from __future__ import annotations
@@ -33,9 +40,10 @@ from commtrace.events import (  # noqa: E402
     gpu, parse_trace, write_trace,
 )
 from commtrace.grouping import CollectiveInstance  # noqa: E402
+from commtrace.grouping import group_collectives  # noqa: E402
 from commtrace.matrix import (  # noqa: E402
-    ALL_TYPES, CommMatrix, ModelConfig, _typed_decompositions, analyze_events,
-    infer_device_count,
+    ALL_TYPES, CommMatrix, ModelConfig, _typed_decompositions, accumulate, analyze_events,
+    infer_device_count, merge, split_by_primitive, summarize,
 )
 from commtrace.workload import (  # noqa: E402
     TrainingConfig, generate_gnmt_trace, generate_training_trace, resnet_like_preset,
@@ -352,9 +360,141 @@ def dump(name, obj):
     print(name, os.path.getsize(path))
 
 
+def build_loader_fuzz():
+    """The reference reader on every text of the fuzz corpus (tests/loader_fuzz.py)."""
+    sys.path.insert(0, os.path.dirname(os.path.dirname(OUT)))
+    from tests.loader_fuzz import corpus, event_row
+
+    def ref(src):
+        try:
+            return {"events": [event_row(e) for e in parse_trace(src)]}
+        except (E.TraceError, UnicodeDecodeError) as exc:
+            return {"error": [type(exc).__name__, str(exc)]}
+
+    out = []
+    for group, text in corpus():
+        r_str = ref(text)
+        r_bytes = ref(text.encode("utf-8", "surrogatepass"))
+        row = {"g": group, "text": text, "str": r_str}
+        if r_bytes != r_str:
+            row["bytes"] = r_bytes
+        out.append(row)
+    return out
+
+
+def _inst_row(i):
+    return [i.comm, i.ordinal, i.collective.value, i.algorithm.value, i.n_ranks, i.count, i.dtype.value,
+            i.root, list(i.per_rank_devices)]
+
+
+def _mrows(m):
+    return [m.rows(), m.with_aggregator]
+
+
+def _err(exc):
+    return {"error": [type(exc).__name__, str(exc)]}
+
+
+def build_siblings():
+    """split_by_primitive / summarize (matrix.py:261-301) on instance lists in caller
+    order -- comm-major as grouped, shuffled, reversed -- plus infer_device_count
+    (matrix.py:250-258), merge (matrix.py:164-178) and accumulate (matrix.py:157-161)."""
+    cases = build_traces()
+    rng = random.Random(4321)
+    out = []
+    for case in cases:
+        if "result" not in case:
+            continue
+        events = parse_trace(case["jsonl"])
+        if not events:
+            continue
+        cfg = ModelConfig(ring_order=tuple(case["ring_order"]) if case["ring_order"] else None,
+                          tree_threshold=case["tree_threshold"])
+        instances, gdiags = group_collectives(events)
+        shuffled = list(instances)
+        rng.shuffle(shuffled)
+        orders = {"grouped": instances, "shuffled": shuffled, "reversed": instances[::-1]}
+        row = {"name": case["name"], "infer_d": infer_device_count(events), "orders": {}}
+        for oname, lst in orders.items():
+            rec = {"instances": [_inst_row(i) for i in lst]}
+            for dname, d in (("auto", None), ("given", case["d"])):
+                if dname == "given" and d is None:
+                    continue
+                try:
+                    sp = split_by_primitive(lst, events, d=d, config=cfg)
+                    rec["split_" + dname] = [[k, *_mrows(m)] for k, m in sp.items()]
+                except (E.TraceError, OverflowError) as exc:
+                    rec["split_" + dname] = _err(exc)
+            try:
+                sm = summarize(lst, events, config=cfg, diagnostics=gdiags)
+                rec["summary"] = {"types": {t: [v.call_count, v.payload_bytes, v.wire_bytes]
+                                            for t, v in sm.types.items()},
+                                  "instances": sm.instances, "diagnostics": sm.diagnostics}
+            except (E.TraceError, OverflowError) as exc:
+                rec["summary"] = _err(exc)
+            rec["summary_nodiag"] = summarize(lst, events, config=cfg).diagnostics
+            row["orders"][oname] = rec
+            if len(lst) < 2 and oname != "grouped":
+                break
+        # accumulate: every typed decomposition into one matrix (and into a too-small one)
+        typed, _ = _typed_decompositions(instances, events, cfg)
+        decs = [[[_ep_full(t.src), _ep_full(t.dst), t.bytes] for t in dec.transfers] for _, _, dec in typed]
+        row["decs"] = decs
+        for dname, d in (("infer", row["infer_d"]), ("small", max(row["infer_d"] - 1, 0))):
+            m = CommMatrix(d)
+            try:
+                for _, _, dec in typed:
+                    accumulate(m, dec)
+                row["acc_" + dname] = _mrows(m)
+            except (E.TraceError, OverflowError) as exc:
+                row["acc_" + dname] = _err(exc)
+        # merge: combined + each per-primitive matrix, in both orders, and a d mismatch
+        res = analyze_events(events, d=case["d"], config=cfg)
+        merges = []
+        mats = [res.combined] + list(res.per_primitive.values())
+        for a in mats[:3]:
+            for b in mats[:3]:
+                try:
+                    merges.append([_mrows(a), _mrows(b), _mrows(merge(a, b))])
+                except (E.TraceError, OverflowError) as exc:
+                    merges.append([_mrows(a), _mrows(b), _err(exc)])
+        other = CommMatrix(res.d + 1)
+        try:
+            merge(res.combined, other)
+        except E.TraceError as exc:
+            merges.append([_mrows(res.combined), [other.rows(), False], _err(exc)])
+        row["merges"] = merges
+        out.append(row)
+    # merge overflow (matrix.py:174-175)
+    a = CommMatrix(1)
+    a._cells[0][1] = (1 << 62)
+    b = CommMatrix(1)
+    b._cells[0][1] = (1 << 62) - 1
+    b.widen()
+    merges = [[_mrows(a), _mrows(b), _mrows(merge(a, b))]]
+    try:
+        merge(a, a)
+    except OverflowError as exc:
+        merges.append([_mrows(a), _mrows(a), _err(exc)])
+    out.append({"name": "merge_overflow", "merges": merges})
+    return out
+
+
+def _ep_full(ep):
+    return [ep.kind.value, ep.index]
+
+
+FIXTURES = {
+    "traces.json.gz": build_traces,
+    "decomp_grid.json.gz": build_grid,
+    "random_insts.json.gz": build_random_instances,
+    "loader.json.gz": build_loader_cases,
+    "loader_fuzz.json.gz": build_loader_fuzz,
+    "siblings.json.gz": build_siblings,
+}
+
+
 if __name__ == "__main__":
-    dump("traces.json.gz", build_traces())
-    dump("decomp_grid.json.gz", build_grid())
-    dump("random_insts.json.gz", build_random_instances())
-    dump("loader.json.gz", build_loader_cases())
+    for name in sys.argv[1:] or list(FIXTURES):
+        dump(name, FIXTURES[name]())
     _ = ALL_TYPES

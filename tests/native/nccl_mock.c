@@ -20,6 +20,14 @@ int ncclCommInitAll(ncclComm_t* comms, int ndev, const int* devlist) {
   }
   return 0;
 }
+int ncclCommSplit(ncclComm_t comm, int color, int key, ncclComm_t* newcomm, void* config) {
+  (void)color; (void)config;
+  *newcomm = (ncclComm_t)calloc(1, sizeof(struct ncclComm));
+  (*newcomm)->rank = key; (*newcomm)->nranks = comm->nranks; (*newcomm)->dev = comm->dev;
+  return 0;
+}
+int ncclCommDestroy(ncclComm_t comm) { free(comm); return 0; }
+int ncclCommAbort(ncclComm_t comm) { free(comm); return 0; }
 int ncclCommUserRank(const ncclComm_t c, int* r) { *r = c->rank; return 0; }
 int ncclCommCount(const ncclComm_t c, int* n) { *n = c->nranks; return 0; }
 int ncclCommCuDevice(const ncclComm_t c, int* d) { *d = c->dev; return 0; }

@@ -41,7 +41,8 @@ def _host(buf):
     return buf.cpu().numpy().view(RECORD_DTYPE)
 
 
-@pytest.mark.parametrize("name,n", [("c2", 10_000_000), ("c3", 2_000_000), ("c4", 2_000_000), ("c5", 2_000_000)])
+@pytest.mark.parametrize("name,n", [("c2", 10_000_000), ("c3", 100_000_000), ("c4", 2_000_000), ("c4", 100_000_000),
+                                    ("c5", 100_000_000)])
 def test_generated_trace_matches_c_oracle(name, n):
     import os
     from oracle import c_oracle as CO
@@ -54,6 +55,7 @@ def test_generated_trace_matches_c_oracle(name, n):
     s, cells, freq = _gpu_analyze(buf, n, n_comms)
     assert s.path == 1  # the generators emit the canonical layout
     recs = _host(buf)
+    del buf
     threads = os.cpu_count() or 4
     bounds = sorted({0, n} | {lib.ct_generate_boundary(kind, n * k // threads) for k in range(1, threads)})
     want = CO.analyze_threads(recs, bounds, threads, gcap=s.g_cap)

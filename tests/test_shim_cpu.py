@@ -101,3 +101,60 @@ def test_shim_disable_and_unwritable_sink(tmp_path):
     p = _child(tmp_path, {"COMSCRIBE_OUT": str(tmp_path / "no" / "such" / "dir" / "t.jsonl")})
     assert p.returncode == 0 and p.stdout.strip() == "5"  # calls still forward
     assert p.stderr.count("cannot open trace sink") == 1
+
+
+SPLIT_CHILD = r"""
+import ctypes as C, sys
+mock = C.CDLL(sys.argv[1], mode=C.RTLD_GLOBAL)
+g = C.CDLL(None)
+class UID(C.Structure):
+    _fields_ = [("internal", C.c_char * 128)]
+V, S = C.c_void_p, C.c_size_t
+g.ncclCommInitRank.argtypes = [C.POINTER(V), C.c_int, UID, C.c_int]
+g.ncclCommSplit.argtypes = [V, C.c_int, C.c_int, C.POINTER(V), V]
+g.ncclCommDestroy.argtypes = [V]
+g.ncclAllReduce.argtypes = [V, V, S, C.c_int, C.c_int, V, V]
+uid = UID(); uid.internal = b"job-7"
+world = []
+for r in range(2):
+    c = V(); assert g.ncclCommInitRank(C.byref(c), 2, uid, r) == 0; world.append(c)
+# two splits of the same parent with the same color (torch new_group over the same ranks)
+for round_ in range(2):
+    kids = []
+    for r in range(2):
+        k = V(); assert g.ncclCommSplit(world[r], 0, r, C.byref(k), None) == 0; kids.append(k)
+    for k in kids: assert g.ncclAllReduce(None, None, 8, 7, 0, k, None) == 0
+    for k in kids: assert g.ncclCommDestroy(k) == 0
+# many communicators created and destroyed: the table must not fill up
+for i in range(5000):
+    c = V(); u = UID(); u.internal = b"tmp-%d" % i
+    assert g.ncclCommInitRank(C.byref(c), 1, u, 0) == 0
+    assert g.ncclCommDestroy(c) == 0
+c = V(); u = UID(); u.internal = b"last"
+assert g.ncclCommInitRank(C.byref(c), 1, u, 0) == 0
+assert g.ncclAllReduce(None, None, 4, 7, 0, c, None) == 0
+"""
+
+
+def test_shim_split_ids_and_destroy(tmp_path):
+    """Repeated same-color splits get distinct communicator ids (each restarting at seq 0
+    without colliding); destroyed communicators free their table slots."""
+    if not os.path.exists(SHIM):
+        pytest.skip("shim not built (run __graft_entry__.build())")
+    out = tmp_path / "trace.jsonl"
+    env = dict(os.environ, LD_PRELOAD=SHIM, COMSCRIBE_OUT=str(out))
+    p = subprocess.run([sys.executable, "-c", SPLIT_CHILD, _mock(tmp_path)], env=env, capture_output=True,
+                       text=True, timeout=120)
+    assert p.returncode == 0, p.stderr
+    assert "table full" not in p.stderr
+    objs = [json.loads(l) for l in out.read_text().splitlines()]
+    assert len(objs) == 5
+    split = objs[:4]
+    ids = [o["comm"] for o in split]
+    assert ids[0] == ids[1] and ids[2] == ids[3] and ids[0] != ids[2]
+    assert [o["seq"] for o in split] == [0, 0, 0, 0]
+    sys.path.insert(0, ROOT)
+    from oracle import commtrace_oracle as O
+    from paper_2110_10401_b200.events import parse_trace
+    res = O.analyze(parse_trace(out.read_text()))["result"]
+    assert res["instances"] == 3  # two split allreduces + the last one, no duplicate-seq error
