@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-loader", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--no-object-api", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=64_000_000)
     ap.add_argument("--ref-sample", type=int, default=2_000_000)
     return ap.parse_args()
@@ -387,6 +388,9 @@ def main():
     loader = None
     if rank == 0 and world == 1 and not a.no_loader:
         loader = loader_measure(ctx)
+    object_api = None
+    if rank == 0 and world == 1 and not a.no_object_api:
+        object_api = object_api_measure(ctx)
 
     traffic, traffic_src = ncu_traffic(a.workload, n)
     if rank == 0:
@@ -410,6 +414,7 @@ def main():
             "result_check": check,
             "parity": parity,
             "loader": loader,
+            "object_api": object_api,
         }
         print(json.dumps(line))
     if world > 1:
@@ -484,6 +489,52 @@ def parity_check(host, n, kind, lib, summ, cells):
     }
     return {"ok": all(checks.values()), "checks": checks, "records": n, "oracle": "oracle/ct_oracle.c",
             "oracle_s": round(dt, 2), "threads": threads}
+
+
+def object_api_measure(ctx, n=1_000_000, ref_sample=100_000):
+    """The drop-in object API end to end: ``analyze_events(list[TraceEvent])`` (native
+    packer -> H2D -> ct_analyze -> result objects) on C1 (the reference's own training
+    trace, tests/golden) and on a 1M-event C3 trace, next to the reference algorithm's
+    CPU port (oracle/commtrace_oracle.analyze, one process) on the same event objects."""
+    try:
+        import numpy as np
+        import torch
+        from oracle import commtrace_oracle as O
+        from paper_2110_10401_b200.events import parse_trace
+        from paper_2110_10401_b200.matrix import analyze_events
+        from paper_2110_10401_b200.packed import PackedTrace, RECORD_DTYPE, unpack
+        from tests.golden_loader import load_case
+
+        out = {}
+        c1 = parse_trace(load_case("C1")["jsonl"])
+        buf = torch.empty(n * RECORD_BYTES, dtype=torch.uint8, device="cuda")
+        rc = ctx.lib.ct_generate(ctx.handle, 3, 13, 0, n, C.c_void_p(buf.data_ptr()), None)
+        assert rc == 0, ctx.error()
+        torch.cuda.synchronize()
+        rec = np.frombuffer(buf.cpu().numpy().tobytes(), dtype=RECORD_DTYPE).copy()
+        del buf
+        names = [f"comm{i}" for i in range(int(rec["comm"].max()) + 1)]
+        big = unpack(PackedTrace(rec, names, list(range(n)), None))  # TraceEvent objects (untimed)
+        for name, evs in (("C1", c1), ("C3_1M", big)):
+            analyze_events(evs[: min(len(evs), 10_000)])  # warm-up
+            ts = []
+            for _ in range(3):
+                t0 = time.perf_counter()
+                res = analyze_events(evs)
+                ts.append(time.perf_counter() - t0)
+            dt = statistics.median(ts)
+            k = min(len(evs), ref_sample)
+            t0 = time.perf_counter()
+            want = O.analyze(evs[:k])
+            rdt = time.perf_counter() - t0
+            out[name] = {"events": len(evs), "records_per_s": len(evs) / dt, "ms": dt * 1e3,
+                         "ref_port_records_per_s": k / rdt, "ref_port_sample": k, "ref_port_cores": 1,
+                         "instances": res.stats.instances, "ref_instances_in_sample": want["result"]["instances"]}
+        out["api"] = ("analyze_events(list[TraceEvent]) end to end (native packer, pinned-less H2D, device "
+                      "analysis, result objects); ref_port = reference algorithm CPU port on the same events")
+        return out
+    except Exception as exc:  # reported, never fatal for the headline line
+        return {"error": repr(exc)[:300]}
 
 
 def cpu_baseline_c(buf, sample, kind, lib):

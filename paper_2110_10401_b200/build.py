@@ -44,8 +44,21 @@ def build_shim(force: bool = False) -> str:
     return SHIM
 
 
+def build_pack(force: bool = False) -> str:
+    """Native TraceEvent packer (CPython C API, gcc): csrc/ct_pack.c -> _ctpack extension."""
+    import sysconfig
+
+    out = os.path.join(OUT or PKG, "_ctpack" + sysconfig.get_config_var("EXT_SUFFIX"))
+    src = os.path.join(CSRC, "ct_pack.c")
+    if force or not os.path.exists(out) or os.path.getmtime(src) > os.path.getmtime(out):
+        subprocess.run(["gcc", "-O2", "-shared", "-fPIC", "-Wall", "-I", sysconfig.get_paths()["include"], "-o", out,
+                        src], check=True)
+    return out
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     build_shim(force)
+    build_pack(force)
     if not force and not _stale():
         return LIB
     objs = []

@@ -132,14 +132,55 @@ def _endpoint_gpu(ep: Endpoint) -> int:
     return _check_range(ep.index, U16_MAX, "copy endpoint GPU") if ep.kind is EndpointKind.GPU else 0
 
 
+_NATIVE_CODES = (
+    {k.value: v for k, v in KIND_CODE.items()},
+    {k.value: v for k, v in COLL_CODE.items()},
+    {k.value: v for k, v in ALGO_CODE.items()},
+    {k.value: v for k, v in DTYPE_CODE.items()},
+    {k.value: v for k, v in CKIND_CODE.items()},
+    {"host": 0, "gpu": 1, "net": 2},
+)
+
+
+def _native():
+    try:
+        from . import _ctpack
+        return _ctpack
+    except ImportError:
+        return None
+
+
 def pack_events(events, comms: dict | None = None) -> PackedTrace:
     """TraceEvent list → PackedTrace.
 
     Events must satisfy ``TraceEvent.validate()`` (``parse_trace`` guarantees it);
     values must fit the record fields (u64 count/seq/bytes, u16 ranks/devices).
     Works on any object with the reference's TraceEvent attributes.
+
+    The native packer (``csrc/ct_pack.c``, CPython C API) does the work; it stops at
+    the first event failing validate() or a record range, and that event is then
+    checked here with the reference-mirroring code so the exception is exact.  An
+    event the native checks reject but Python accepts (an exotic duck type) sends the
+    whole list through the Python packer below.
     """
     events = list(events)
+    native = _native()
+    if native is not None:
+        comm_ids: dict[str, int] = {} if comms is None else dict(comms)
+        raw, ts, bad = native.pack(events, comm_ids, _NATIVE_CODES)
+        if bad < 0:
+            rec = np.frombuffer(raw, dtype=RECORD_DTYPE).copy() if events else np.zeros(0, RECORD_DTYPE)
+            ts_out = np.frombuffer(ts, dtype=np.int64).copy() if ts is not None else [e.ts_ns for e in events]
+            names = [None] * len(comm_ids)
+            for name, cid in comm_ids.items():
+                names[cid] = name
+            return PackedTrace(rec, names, ts_out, events)
+        _pack_python([events[bad]])  # raises the reference's exception (or RecordRangeError)
+    return _pack_python(events, comms)
+
+
+def _pack_python(events, comms: dict | None = None) -> PackedTrace:
+    """The reference-mirroring packer (validate + range checks, exact messages)."""
     n = len(events)
     rec = np.zeros(n, dtype=RECORD_DTYPE)
     comm_ids: dict[str, int] = {} if comms is None else dict(comms)

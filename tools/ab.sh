@@ -3,7 +3,7 @@
 # Usage: tools/ab.sh "c4 c3" [extra bench args]
 ws=${1:-c4}; shift
 for w in $ws; do
-  timeout 300 python bench.py --workload $w --steps 5 --warmup 3 --no-e2e --no-cpu --no-loader --no-parity "$@" 2>&1 | \
+  timeout 300 python bench.py --workload $w --steps 5 --warmup 3 --no-e2e --no-cpu --no-loader --no-parity --no-object-api "$@" 2>&1 | \
   python -c "
 import sys, json
 for l in sys.stdin:
