@@ -35,6 +35,7 @@ WORKLOADS = {  # name -> (generator kind, n_comms, description)
     "c3": (3, 3, "C3 collectives + send/recv pairs + memcpy/um/zerocopy incl. host"),
     "c4": (4, 1, "C4 ResNet-50 DP training: 25 MiB bucketed ring allreduce, n=8"),
     "c5": (5, 7, "C5 ring vs tree allreduce sweep, n in 2..8, 1 KiB-1 GiB"),
+    "c4i": (6, 1, "C4 in the capture layout of an LD_PRELOAD interposer (ranks interleaved, per-rank order kept)"),
 }
 RECORD_BYTES = 32
 # one metric string for both arms (the driver divides b200 by reference only when they match)

@@ -77,7 +77,8 @@ typedef struct ct_config {
   int64_t d;                  /* matrix GPU count; -1 = infer (matrix.py:250-258)      */
   uint64_t tree_threshold;    /* AUTO allreduce: tree below, ring at/above (decompose.py:44) */
   int32_t ring_len;           /* 0 = identity rings; else ring applies where N == ring_len */
-  int32_t force_path;         /* 0 auto, 1 fast (canonical layout only), 2 exact       */
+  int32_t force_path;         /* 0 auto, 1 fast (canonical layout only), 2 exact,      
+                                 3 counting canonicaliser (capture layout) + fast        */
   const uint16_t *ring_order; /* host pointer, ring_len entries (need not be a permutation:
                                  an invalid order raises InvalidConfig only when used)  */
   int32_t dev_hint;           /* >0: caller's bound on (max GPU id + 1); sizes histograms */
@@ -92,7 +93,8 @@ typedef struct ct_config {
  */
 typedef struct ct_summary {
   int32_t status;
-  int32_t path;               /* 1 = fast (canonical), 2 = exact (sort-based join)      */
+  int32_t path;               /* 1 = fast (canonical), 2 = exact (sort-based join),     
+                                 3 = counting canonicaliser (capture layout) + fast     */
   int64_t d;
   int32_t g_cap;              /* GPUs covered by the cell arrays                        */
   int32_t net_used;           /* bit t set: type t received a collnet transfer          */
@@ -164,7 +166,8 @@ int ct_emit_transfers(ct_context *ctx, const ct_record *recs, uint64_t n, int on
 
 /* Synthetic workload generators writing packed records on the
  * device: kind 2 = C2 mixed collectives, 3 = C3 mixed with p2p/copies,
- * 4 = C4 bucketed gradient allreduce, 5 = C5 ring/tree sweep.  Records
+ * 4 = C4 bucketed gradient allreduce, 5 = C5 ring/tree sweep, 6 = C4 in the capture
+ * layout of an LD_PRELOAD interposer (ranks interleaved, per-rank order kept).  Records
  * [first, first + n) of the infinite seeded stream are written to dev_out. */
 int ct_generate(ct_context *ctx, int kind, uint64_t seed, uint64_t first, uint64_t n,
                 ct_record *dev_out, void *stream);

@@ -31,7 +31,7 @@ CT_ERR_CUDA = 21
 CT_ERR_NOT_CANONICAL = 22
 CT_ERR_CAPACITY = 23
 
-FORCE_AUTO, FORCE_FAST, FORCE_EXACT = 0, 1, 2
+FORCE_AUTO, FORCE_FAST, FORCE_EXACT, FORCE_COUNT = 0, 1, 2, 3
 
 
 class CtConfig(C.Structure):

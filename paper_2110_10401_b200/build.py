@@ -15,7 +15,7 @@ OUT = os.environ.get("CT_BUILD_OUT", "")  # variant builds: alternate output dir
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(OUT or PKG, "libcommtrace_b200.so")
-SOURCES = ["ct_api.cu", "ct_fast.cu", "ct_exact.cu", "ct_emit.cu", "ct_gen.cu", "ct_jsonl.cu"]
+SOURCES = ["ct_api.cu", "ct_fast.cu", "ct_exact.cu", "ct_canon.cu", "ct_emit.cu", "ct_gen.cu", "ct_jsonl.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

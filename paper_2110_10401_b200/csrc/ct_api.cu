@@ -14,6 +14,7 @@
 #include <string>
 #include <vector>
 
+#include "ct_canon.cuh"
 #include "ct_exact.cuh"
 #include "ct_fast.cuh"
 
@@ -422,6 +423,7 @@ int ct_analyze(ct_context* c, const ct_record* recs, uint64_t n, int on_device, 
   RunOut ro{};
   uint32_t launches = 0;
   int path = 1;
+  bool counted = false;  // the counting canonicaliser produced the stream (already analysed)
   int max_dev = -1;
   const ct_record* arr = d_recs;
   uint64_t arr_n = n;
@@ -437,8 +439,42 @@ int ct_analyze(ct_context* c, const ct_record* recs, uint64_t n, int on_device, 
     return 0;
   };
 
+  // capture layout (ranks interleaved): counting canonicaliser; its stream must pass the
+  // fast kernel's order checks, else the exact path runs on the original records
+  auto do_counting = [&]() -> int {  // 1: canonical stream ready, 0: not applicable
+    ExactResult cr;
+    int md = -1;
+    const int e = count_canonicalize(d_recs, n, n_comms, c->num_sms, st, &cr, &md);
+    if (e == kCanonUnsupported) return 0;
+    if (e) return -cuda_fail(c, (cudaError_t)e, "counting canonicaliser");
+    launches += cr.launches;
+    RunOut probe{};
+    const int gprobe = explicit_d ? gcap : std::max(gcap, md + 1);
+    if (int e2 = run_fast(c, cr.canon, cr.m, gprobe, explicit_d, ex, n_comms, st, &probe)) {
+      cudaFreeAsync(cr.canon, st);
+      return -e2;
+    }
+    launches += probe.launches;
+    if (probe.gs.flags & F_NONCANON) {  // file order is not seq order somewhere: sort instead
+      cudaFreeAsync(cr.canon, st);
+      return 0;
+    }
+    ex_res = cr;
+    ro = probe;
+    gcap = gprobe;
+    max_dev = md;
+    ran_exact = true;
+    counted = true;
+    path = 3;
+    return 1;
+  };
+
   if (cfg->force_path == 2) {
     if (int e = do_exact()) return e;
+  } else if (cfg->force_path == 3) {
+    const int r = do_counting();
+    if (r < 0) return -r;
+    if (r == 0) return fail(c, CT_ERR_NOT_CANONICAL, "trace is outside the counting canonicaliser's scope");
   } else {
     if (int e = run_fast(c, d_recs, n, gcap, explicit_d, ex, n_comms, st, &ro)) return e;
     launches += ro.launches;
@@ -446,7 +482,10 @@ int ct_analyze(ct_context* c, const ct_record* recs, uint64_t n, int on_device, 
     if (ro.gs.flags & F_NONCANON) {
       if (cfg->force_path == 1) return fail(c, CT_ERR_NOT_CANONICAL, "trace is not in the canonical layout");
       max_dev = -1;  // the aborted pass may not have visited every record: re-infer d below
-      if (int e = do_exact()) return e;
+      const int r = do_counting();
+      if (r < 0) return -r;
+      if (r == 0)
+        if (int e = do_exact()) return e;
     }
   }
   if (ran_exact) {
@@ -475,9 +514,11 @@ int ct_analyze(ct_context* c, const ct_record* recs, uint64_t n, int on_device, 
     arr_n = ex_res.m;
     c->canon_keep = ex_res.canon;
     c->canon_n = ex_res.m;
-    if (int e = run_fast(c, arr, arr_n, gcap, explicit_d, ex, n_comms, st, &ro)) return e;
-    launches += ro.launches;
-    if (ro.gs.flags & F_NONCANON) return fail(c, CT_ERR_CUDA, "internal: canonical stream rejected");
+    if (!counted) {
+      if (int e = run_fast(c, arr, arr_n, gcap, explicit_d, ex, n_comms, st, &ro)) return e;
+      launches += ro.launches;
+      if (ro.gs.flags & F_NONCANON) return fail(c, CT_ERR_CUDA, "internal: canonical stream rejected");
+    }
   }
   const int64_t d = explicit_d ? cfg->d : (int64_t)max_dev + 1;
   if (!explicit_d && d > gcap) {

@@ -13,6 +13,7 @@
 //       25 MiB gradient buckets (workload.py:69-86, 166-195), one broadcast per
 //       parameter tensor at init, 8 x 192 KiB h2d copies per iteration
 //       (resnet_like_preset, workload.py:221-235, with the ResNet-50 tensor list).
+//   C4i C4 in the capture layout of an LD_PRELOAD interposer (kind 6, see capture_source).
 //   C5  ring vs tree allreduce sweep: groups of 35 records holding one block of every
 //       n in 2..8 (comm n-2) in a seeded order, algo ring|tree, bytes log-uniform
 //       [1 KiB, 1 GiB).
@@ -143,11 +144,62 @@ int c4_upload(cudaStream_t st) {
   return 0;
 }
 
+// ---------------------------------------------------------------- capture layout
+// C4 as an LD_PRELOAD interposer records it (kind 6): every process appends its own calls
+// in call order, the processes of one job interleave.  The C4 stream is a sequence of
+// rounds of 8 records, one per rank (an allreduce block or the 8 per-iteration copies);
+// in epochs of kEpochRounds rounds, rank r lags by delta_r(e) in [0, kMaxLag) rounds and
+// every round lists its ranks in a seeded order.  Each rank's records keep their order,
+// the ranks of one call spread over up to kMaxLag neighbouring calls, and an epoch
+// boundary (a multiple of 8 * kEpochRounds records) is a clean cut.
+constexpr uint64_t kEpochRounds = 16384;
+constexpr uint32_t kMaxLag = 8;
+
+// canonical C4 index of the record at capture position p
+__device__ uint64_t capture_source(uint64_t seed, uint64_t p) {
+  const uint64_t E = kEpochRounds, e = p / (8 * E), q = p % (8 * E);
+  uint32_t lag[8];
+#pragma unroll
+  for (int r = 0; r < 8; r++) lag[r] = (uint32_t)(h2(seed, 11, e * 8 + r) % kMaxLag);
+  auto start = [&](uint64_t t) -> uint64_t {  // records in rounds < t
+    uint64_t s = 0;
+#pragma unroll
+    for (int r = 0; r < 8; r++) s += t > lag[r] ? min(t - lag[r], E) : 0;
+    return s;
+  };
+  uint64_t lo = 0, hi = E + kMaxLag;  // last round t with start(t) <= q
+  while (hi - lo > 1) {
+    const uint64_t mid = (lo + hi) / 2;
+    if (start(mid) <= q) lo = mid; else hi = mid;
+  }
+  const uint64_t t = lo;
+  uint32_t within = (uint32_t)(q - start(t));
+  // ranks present in round t, in a seeded order: the within-th smallest hash key
+  uint64_t key[8];
+  bool here[8];
+#pragma unroll
+  for (int r = 0; r < 8; r++) {
+    here[r] = t >= lag[r] && t - lag[r] < E;
+    key[r] = (h2(seed, 12, (e << 24) ^ (t << 3) ^ (uint64_t)r) & ~7ull) | (uint64_t)r;
+  }
+  int pick = 0;
+#pragma unroll
+  for (int r = 0; r < 8; r++) {
+    if (!here[r]) continue;
+    uint32_t below = 0;
+#pragma unroll
+    for (int s = 0; s < 8; s++) below += here[s] && key[s] < key[r];
+    if (below == within) pick = r;
+  }
+  return e * 8 * E + 8 * (t - lag[pick]) + (uint64_t)pick;
+}
+
 // ---------------------------------------------------------------- kernels
-__global__ void k_gen(int kind, uint64_t seed, uint64_t first, uint64_t n, ct_record* out) {
+__global__ void k_gen(int kind_in, uint64_t seed, uint64_t first, uint64_t n, ct_record* out) {
+  const int kind = kind_in == 6 ? 4 : kind_in;  // capture layout of C4: C4 records, permuted
   for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n;
        k += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t i = first + k;
+    const uint64_t i = kind_in == 6 ? capture_source(seed, first + k) : first + k;
     ct_record* o = out + k;
     if (kind == 2) {
       mixed_collective(o, seed, i / 8, (uint32_t)(i % 8), 0, i / 8);
@@ -240,8 +292,8 @@ __global__ void k_gen(int kind, uint64_t seed, uint64_t first, uint64_t n, ct_re
 }  // namespace
 
 int generate(int kind, uint64_t seed, uint64_t first, uint64_t n, ct_record* out, cudaStream_t st) {
-  if (kind < 2 || kind > 5) return 1;
-  if (kind == 4 && c4_upload(st)) return 1;
+  if (kind < 2 || kind > 6) return 1;
+  if ((kind == 4 || kind == 6) && c4_upload(st)) return 1;
   if (!n) return 0;
   uint64_t g = (n + 255) / 256;
   if (g > 148 * 64) g = 148 * 64;
@@ -257,7 +309,7 @@ uint64_t generate_boundary(int kind, uint64_t at) {
       if (s >= off) return g * 40 + s;
     return (g + 1) * 40;
   }
-  const uint64_t q = kind == 5 ? 35 : 8;
+  const uint64_t q = kind == 5 ? 35 : (kind == 6 ? 8 * kEpochRounds : 8);
   return (at + q - 1) / q * q;
 }
 

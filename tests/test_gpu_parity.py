@@ -32,6 +32,25 @@ def test_golden_traces(golden_traces, force):
     assert not bad, bad
 
 
+def test_golden_traces_counting_canonicaliser(golden_traces):
+    """force_path=3: the counting canonicaliser (capture layout) on every golden trace it
+    accepts -- rank-major files keep per-(comm, rank) order and must go through it; a
+    trace outside its scope (file order != seq order) is refused, never misanalysed."""
+    bad, taken = [], 0
+    for case in golden_traces:
+        try:
+            got, _ = run_case(case, _analyze(3))
+        except RuntimeError as exc:
+            assert "status 22" in str(exc), exc
+            continue
+        taken += 1
+        want = {k: case[k] for k in ("error", "result") if k in case}
+        if got != want:
+            bad.append(case["name"])
+    assert not bad, bad
+    assert taken > 100, taken
+
+
 def test_fast_path_taken_on_canonical(golden_traces):
     from paper_2110_10401_b200 import matrix
     from paper_2110_10401_b200.events import parse_trace
