@@ -277,24 +277,45 @@ def main():
     ctx = _lib.context(device)
     lib = ctx.lib
     total = lib.ct_generate_boundary(kind, a.records)
-    lo = lib.ct_generate_boundary(kind, total * rank // world)
-    hi = lib.ct_generate_boundary(kind, total * (rank + 1) // world) if rank + 1 < world else total
+    # capture layouts (kind 6) shard by plain record ranges and route records to the rank
+    # owning their canonical position (dist.route_any_layout); canonical ones cut at
+    # element boundaries and need no exchange beyond the partials
+    any_layout = kind == 6 and world > 1
+    if any_layout:
+        lo, hi = total * rank // world, total * (rank + 1) // world
+    else:
+        lo = lib.ct_generate_boundary(kind, total * rank // world)
+        hi = lib.ct_generate_boundary(kind, total * (rank + 1) // world) if rank + 1 < world else total
     n = hi - lo
     buf = torch.empty(max(n, 1) * RECORD_BYTES, dtype=torch.uint8, device="cuda")
     stream = torch.cuda.current_stream()
     rc = lib.ct_generate(ctx.handle, kind, a.seed, lo, n, C.c_void_p(buf.data_ptr()), C.c_void_p(stream.cuda_stream))
     assert rc == 0, ctx.error()
     torch.cuda.synchronize()
-    cfg = _lib.make_config(d=None, dev_hint=8, n_comms=n_comms)
+    cfg = _lib.make_config(d=None, dev_hint=8, n_comms=n_comms, force_path=_lib.FORCE_FAST if any_layout else 0)
     summ = _lib.CtSummary()
     merged = _lib.CtSummary()
 
     pbuf = None
 
+    dev_shard = None
+
     def step(ptr, on_device):
         """One pass of the path over this rank's shard (+ the partial exchange)."""
-        nonlocal pbuf
-        rc = lib.ct_analyze(ctx.handle, C.c_void_p(ptr), n, on_device, C.byref(cfg), C.byref(summ),
+        nonlocal pbuf, dev_shard
+        n_step = n
+        if any_layout:  # global grouping: two small all-gathers + one all-to-all, then a canonical slice
+            from paper_2110_10401_b200.dist import route_any_layout
+            if on_device:
+                src = buf
+            else:  # host shard: H2D inside the step
+                if dev_shard is None:
+                    dev_shard = torch.empty(max(n, 1) * RECORD_BYTES, dtype=torch.uint8, device="cuda")
+                dev_shard.copy_(host_shard, non_blocking=True)
+                src = dev_shard
+            part = route_any_layout(src[: n * RECORD_BYTES], n_comms, stream=stream.cuda_stream)
+            ptr, on_device, n_step = part.data_ptr(), 1, part.shape[0]
+        rc = lib.ct_analyze(ctx.handle, C.c_void_p(ptr), n_step, on_device, C.byref(cfg), C.byref(summ),
                             C.c_void_p(stream.cuda_stream))
         if rc != 0:
             raise RuntimeError(f"ct_analyze status {rc}: {ctx.error()}")
@@ -371,9 +392,11 @@ def main():
         host = torch.empty(max(n, 1) * RECORD_BYTES, dtype=torch.uint8, pin_memory=True)
         host.copy_(buf)
     e2e = None
+    host_shard = host
     if not a.no_e2e:
-        del buf
-        torch.cuda.empty_cache()
+        if not any_layout:
+            del buf
+            torch.cuda.empty_cache()
         e_steps = max(1, min(a.steps, 5))
         ems, _, _, _ = timed(host.data_ptr(), 0, e_steps)
         d2h = (2 * 9 * 10 * 10 * 8 + 6 * n_comms * 8 + 512) * world

@@ -191,6 +191,40 @@ int ct_partial_export(ct_context *ctx, uint64_t *dev_out, uint64_t words, void *
 int ct_partial_merge(ct_context *ctx, const uint64_t *dev_in, int world, uint64_t words,
                      ct_summary *out, void *stream);
 
+/* Multi-GPU for traces in ANY layout (capture layouts included): canonicalise globally,
+ * then shard.  Each rank holds a record range (shard) of the trace, in rank order.
+ *   1. ct_shard_meta    -> meta_words uint64 (device); all-gather them (rank order)
+ *   2. ct_shard_count   (gathered metas) -> count_words uint64; all-gather them
+ *   3. ct_shard_route   (both gathered lists): the global canonical layout (what
+ *      ct_analyze's counting canonicaliser would build for the whole trace), this
+ *      shard's records sorted by global canonical position into dev_out_pos /
+ *      dev_out_rec (room for n), grouped by destination rank: send_counts[world],
+ *      recv_counts[world] (host) and this rank's part length
+ *   4. all-to-all of positions and records with those counts (NCCL)
+ *   5. ct_shard_assemble -> the part (a slice of the global canonical stream)
+ *   6. ct_analyze(part, force_path = 1), ct_partial_export, all-gather, ct_partial_merge
+ *      (the export adds the diagnostics of records no part holds, on rank 0).
+ * Scope as the counting canonicaliser (ct_analyze force_path 3); outside it the calls
+ * return CT_ERR_NOT_CANONICAL.  Replaces group_collectives / match_p2p over the whole
+ * trace (grouping.py:82-183, decompose.py:342-394) before the per-rank merge
+ * (matrix.py:164-178). */
+int ct_shard_words(int32_t n_comms, uint64_t *meta_words, uint64_t *count_words);
+int ct_shard_meta(ct_context *ctx, const ct_record *recs, uint64_t n, int32_t n_comms, uint64_t *dev_out,
+                  void *stream);
+int ct_shard_count(ct_context *ctx, const ct_record *recs, uint64_t n, int32_t n_comms, const uint64_t *dev_metas,
+                   int world, uint64_t *dev_out, void *stream);
+int ct_shard_route(ct_context *ctx, int32_t n_comms, const uint64_t *dev_metas, const uint64_t *dev_counts,
+                   int world, int rank, uint64_t *dev_out_pos, ct_record *dev_out_rec, uint64_t *send_counts,
+                   uint64_t *recv_counts, uint64_t *part_len, void *stream);
+int ct_shard_assemble(ct_context *ctx, const uint64_t *dev_in_pos, const ct_record *dev_in_rec, uint64_t n_in,
+                      ct_record *dev_part, void *stream);
+/* First element start (collective rank-0 record, send, copy) at or after record ``at``
+ * of a canonical-layout trace (n when none follows): element-aligned cut points for
+ * record-range shards of any canonical trace.  CT_ERR_NOT_CANONICAL when no element
+ * starts within the next 64 records. */
+int ct_element_boundary(ct_context *ctx, const ct_record *recs, uint64_t n, int on_device, uint64_t at,
+                        uint64_t *out);
+
 /* ---------------------------------------------------------------- JSONL loader
  * Device loader for the reference wire format, replacing
  *   parse_trace(source)            pkg/src/commtrace/events.py:352-384

@@ -96,6 +96,16 @@ _SIGNATURES = {
     "ct_partial_export": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]),
     "ct_partial_merge": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_uint64, C.POINTER(CtSummary),
                                    C.c_void_p]),
+    "ct_shard_words": (C.c_int, [C.c_int32, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+    "ct_shard_meta": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_int32, C.c_void_p, C.c_void_p]),
+    "ct_shard_count": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_int32, C.c_void_p, C.c_int, C.c_void_p,
+                                 C.c_void_p]),
+    "ct_shard_route": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_void_p,
+                                 C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
+                                 C.c_void_p]),
+    "ct_shard_assemble": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p]),
+    "ct_element_boundary": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_int, C.c_uint64,
+                                      C.POINTER(C.c_uint64)]),
     "ct_jsonl_parse": (C.c_int, [C.c_int, C.c_void_p, C.c_uint64, C.c_int, C.POINTER(C.c_void_p),
                                  C.c_void_p]),
     "ct_jsonl_records": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
@@ -171,8 +181,16 @@ class Context:
 
 def context(device: int | None = None) -> Context:
     if device is None:
-        device = int(os.environ.get("LOCAL_RANK", "0")) if os.environ.get("CT_DEVICE") is None \
-            else int(os.environ["CT_DEVICE"])
+        if os.environ.get("CT_DEVICE") is not None:
+            device = int(os.environ["CT_DEVICE"])
+        else:  # torch's current device (set_device per rank), else LOCAL_RANK
+            device = int(os.environ.get("LOCAL_RANK", "0"))
+            try:
+                import torch
+                if torch.cuda.is_available():
+                    device = torch.cuda.current_device()
+            except Exception:  # noqa: BLE001 - torch is optional for the C-ABI user
+                pass
     with _lock:
         ctx = _contexts.get(device)
     if ctx is None:

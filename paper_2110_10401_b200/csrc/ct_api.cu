@@ -63,6 +63,7 @@ struct ct_context {
   ct_record* canon_keep = nullptr;  // exact-path canonical stream of the last call
   bool last_explicit = false;
   uint64_t canon_n = 0;
+  ShardState shard;  // multi-GPU canonicalise-then-shard state (ct_shard_*)
 };
 
 namespace {
@@ -975,6 +976,14 @@ int ct_partial_export(ct_context* c, uint64_t* dev_out, uint64_t words, void* st
     hdr[kHdr + 18 + t] = gs.pay_hi[t];
   }
   for (int k = 0; k < CT_NDIAG; k++) hdr[kHdr + 27 + k] = c->last.diag[k];
+  if (c->shard.valid && c->last_input == c->shard.part) {
+    // a routed part (ct_shard_*): the diagnostics of records that never reach a part
+    // (incomplete groups, unmatched p2p: counted once, on rank 0) and d over ALL records
+    hdr[kHdr + 27 + CT_DIAG_INCOMPLETE] += c->shard.extra_diag[0];
+    hdr[kHdr + 27 + CT_DIAG_UNMATCHED_SEND] += c->shard.extra_diag[1];
+    hdr[kHdr + 27 + CT_DIAG_UNMATCHED_RECV] += c->shard.extra_diag[2];
+    hdr[5] = std::max<uint64_t>(hdr[5], (uint64_t)(c->shard.global_max_dev + 1));
+  }
   const uint64_t o_tcf = kHdr + kStats, o_cells = o_tcf + 6ull * nc, o_exp = o_cells + 2 * ncell;
   CTX_TRY(c, cudaMemcpyAsync(dev_out, hdr.data(), hdr.size() * 8, cudaMemcpyHostToDevice, st));
   CTX_TRY(c, cudaMemcpyAsync(dev_out + o_tcf, c->tcf, 6ull * nc * 8, cudaMemcpyDeviceToDevice, st));
@@ -1044,3 +1053,85 @@ int ct_partial_merge(ct_context* c, const uint64_t* dev_in, int world, uint64_t 
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------ multi-GPU, any layout
+extern "C" {
+
+int ct_shard_words(int32_t n_comms, uint64_t* meta_words, uint64_t* count_words) {
+  if (!meta_words || !count_words || n_comms < 1) return CT_ERR_ARGUMENT;
+  *meta_words = shard_meta_words((uint32_t)n_comms);
+  *count_words = shard_count_words();
+  return CT_OK;
+}
+
+static int shard_status(ct_context* c, int e, const char* where) {
+  if (e == 0) return CT_OK;
+  if (e == kCanonUnsupported)
+    return fail(c, CT_ERR_NOT_CANONICAL, std::string(where) + ": trace outside the sharded canonicaliser's scope");
+  return cuda_fail(c, (cudaError_t)e, where);
+}
+
+int ct_shard_meta(ct_context* c, const ct_record* recs, uint64_t n, int32_t n_comms, uint64_t* dev_out, void* stream) {
+  if (!c || !dev_out || (n && !recs) || n_comms < 1) return fail(c, CT_ERR_ARGUMENT, "bad argument");
+  CTX_TRY(c, cudaSetDevice(c->device));
+  cudaStream_t st = stream ? (cudaStream_t)stream : c->stream;
+  return shard_status(c, shard_meta(recs, n, (uint32_t)n_comms, c->num_sms, st, dev_out), "ct_shard_meta");
+}
+
+int ct_shard_count(ct_context* c, const ct_record* recs, uint64_t n, int32_t n_comms, const uint64_t* dev_metas,
+                   int world, uint64_t* dev_out, void* stream) {
+  if (!c || !dev_out || !dev_metas || world < 1 || (n && !recs) || n_comms < 1)
+    return fail(c, CT_ERR_ARGUMENT, "bad argument");
+  CTX_TRY(c, cudaSetDevice(c->device));
+  cudaStream_t st = stream ? (cudaStream_t)stream : c->stream;
+  return shard_status(c, shard_count(&c->shard, recs, n, (uint32_t)n_comms, dev_metas, world, c->num_sms, st, dev_out),
+                      "ct_shard_count");
+}
+
+int ct_shard_route(ct_context* c, int32_t n_comms, const uint64_t* dev_metas, const uint64_t* dev_counts, int world,
+                   int rank, uint64_t* dev_out_pos, ct_record* dev_out_rec, uint64_t* send_counts,
+                   uint64_t* recv_counts, uint64_t* part_len, void* stream) {
+  if (!c || !dev_metas || !dev_counts || world < 1 || rank < 0 || rank >= world || !send_counts || !recv_counts ||
+      !part_len || n_comms < 1)
+    return fail(c, CT_ERR_ARGUMENT, "bad argument");
+  CTX_TRY(c, cudaSetDevice(c->device));
+  cudaStream_t st = stream ? (cudaStream_t)stream : c->stream;
+  return shard_status(c, shard_route(&c->shard, (uint32_t)n_comms, dev_metas, dev_counts, world, rank, c->num_sms, st,
+                                     dev_out_pos, dev_out_rec, send_counts, recv_counts, part_len),
+                      "ct_shard_route");
+}
+
+int ct_shard_assemble(ct_context* c, const uint64_t* dev_in_pos, const ct_record* dev_in_rec, uint64_t n_in,
+                      ct_record* dev_part, void* stream) {
+  if (!c || (n_in && (!dev_in_pos || !dev_in_rec)) || !dev_part) return fail(c, CT_ERR_ARGUMENT, "bad argument");
+  CTX_TRY(c, cudaSetDevice(c->device));
+  cudaStream_t st = stream ? (cudaStream_t)stream : c->stream;
+  return shard_status(c, shard_assemble(&c->shard, dev_in_pos, dev_in_rec, n_in, dev_part, st), "ct_shard_assemble");
+}
+
+}  // extern "C"
+
+extern "C" int ct_element_boundary(ct_context* c, const ct_record* recs, uint64_t n, int on_device, uint64_t at,
+                                   uint64_t* out) {
+  if (!c || !out || (n && !recs)) return fail(c, CT_ERR_ARGUMENT, "null argument");
+  if (at >= n) { *out = n; return CT_OK; }
+  const uint64_t k = std::min<uint64_t>(64, n - at);
+  ct_record buf[64];
+  if (on_device) {
+    CTX_TRY(c, cudaSetDevice(c->device));
+    CTX_TRY(c, cudaMemcpyAsync(buf, recs + at, k * sizeof(ct_record), cudaMemcpyDeviceToHost, c->stream));
+    CTX_TRY(c, cudaStreamSynchronize(c->stream));
+  } else {
+    memcpy(buf, recs + at, k * sizeof(ct_record));
+  }
+  for (uint64_t i = 0; i < k; i++) {
+    const int kind = buf[i].kc & 7;
+    if ((kind == CT_KIND_COLLECTIVE && buf[i].rank == 0) || kind == CT_KIND_SEND ||
+        (kind >= CT_KIND_MEMCPY && kind <= CT_KIND_ZEROCOPY)) {
+      *out = at + i;
+      return CT_OK;
+    }
+  }
+  if (at + k == n) { *out = n; return CT_OK; }
+  return fail(c, CT_ERR_NOT_CANONICAL, "no element start within 64 records");
+}

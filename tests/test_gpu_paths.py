@@ -252,10 +252,10 @@ def test_capacity_fallbacks_match():
     rng = np.random.default_rng(11)
     g = Gen(rng, n_comms=12, max_n=4).mixed(20_000, p_pair=0.0, p_copy=0.0)
     s = _check_any_path(g.array(), n_comms=12)
-    assert s.path == 2
+    assert s.path in (2, 3)  # the counting canonicaliser or the exact join
     g = Gen(rng, n_comms=3, max_n=32, dev_pool=32)
     g.n = [32, 32, 32]
     g.devs = [g._perm(32) for _ in range(3)]
     g.mixed(20_000, p_pair=0.0, p_copy=0.0)
     s = _check_any_path(g.array(), n_comms=3)
-    assert s.path == 2
+    assert s.path in (2, 3)
