@@ -32,7 +32,9 @@ namespace {
 
 constexpr uint64_t kNoKey = ~0ull;  // sort key of records without a device comm name
 
-enum : uint8_t { L_BLANK = 0, L_OK = 1, L_DEFER = 2 };
+// L_ESC: the line holds backslash escapes; the main parse leaves it to k_parse_esc (the
+// same parser with escape decoding compiled in), so the common path carries no escape code
+enum : uint8_t { L_BLANK = 0, L_OK = 1, L_DEFER = 2, L_ESC = 3 };
 
 // ---------------------------------------------------------------- phase 1: breaks
 
@@ -163,7 +165,122 @@ constexpr uint32_t slen(const char* str) { return str[0] ? 1 + slen(str + 1) : 0
 struct Str {
   uint32_t len;
   uint64_t w0, w1;
+  bool esc = false;  // the JSON text held escapes (len / w0 / w1 are the decoded string's)
 };
+
+// Comm names are referenced as (offset | length << 40); names decoded from escapes live
+// in a side buffer, marked by kSideBit in the offset (texts are < 2^39 bytes).
+constexpr uint64_t kSideBit = 1ull << 39;
+constexpr uint64_t kOffMask = (1ull << 40) - 1;
+constexpr uint32_t kMaxEscName = 256;  // longest escaped comm name decoded on the device
+
+__device__ __forceinline__ const uint8_t* name_ptr(const uint8_t* s, const uint8_t* side, uint64_t c) {
+  const uint64_t off = c & kOffMask;
+  return (off & kSideBit) ? side + (off & (kSideBit - 1)) : s + off;
+}
+
+struct Side {  // decoded comm names (escapes): bump-allocated, a full buffer defers the line
+  uint8_t* buf;
+  unsigned long long* used;
+  uint64_t cap;
+};
+
+__device__ __forceinline__ int hexv(uint8_t c) {
+  return c >= '0' && c <= '9' ? c - '0' : (c | 0x20) >= 'a' && (c | 0x20) <= 'f' ? (c | 0x20) - 'a' + 10 : -1;
+}
+
+// String body after the opening quote, WITH escapes (json.loads, strict): the decoded
+// string's first 16 bytes / length in ``out`` and, when ``buf`` is given, its UTF-8
+// bytes (up to ``cap``; lone surrogates encoded like Python's "surrogatepass").
+// Position after the closing quote, 0 on failure (invalid escape, raw control byte).
+struct EscOut {
+  uint64_t pos, w0, w1;
+  uint32_t len;
+};
+
+__device__ __noinline__ EscOut scan_str_esc_impl(const uint8_t* s, uint64_t p, uint64_t e, uint8_t* buf,
+                                                 uint32_t cap) {
+  EscOut r{0, 0, 0, 0};
+  uint32_t n = 0;
+  uint64_t w0 = 0, w1 = 0;
+  auto put = [&](uint32_t b) {
+    if (n < 8) w0 |= (uint64_t)b << (8 * n);
+    else if (n < 16) w1 |= (uint64_t)b << (8 * (n - 8));
+    if (buf && n < cap) buf[n] = (uint8_t)b;
+    n++;
+  };
+  auto hex4 = [&](uint64_t q) -> int {
+    if (q + 4 > e) return -1;
+    int v = 0;
+    for (int k = 0; k < 4; k++) {
+      const int h = hexv(s[q + k]);
+      if (h < 0) return -1;
+      v = v * 16 + h;
+    }
+    return v;
+  };
+  while (p < e) {
+    const uint8_t c = s[p];
+    if (c == '"') {
+      r.pos = p + 1;
+      r.w0 = w0;
+      r.w1 = w1;
+      r.len = n;
+      return r;
+    }
+    if (c < 0x20) return r;  // raw control characters are invalid in strict JSON strings
+    if (c != '\\') { put(c); p++; continue; }
+    if (p + 1 >= e) return r;
+    const uint8_t x = s[p + 1];
+    p += 2;
+    switch (x) {
+      case '"': put('"'); break;
+      case '\\': put('\\'); break;
+      case '/': put('/'); break;
+      case 'b': put(8); break;
+      case 'f': put(12); break;
+      case 'n': put(10); break;
+      case 'r': put(13); break;
+      case 't': put(9); break;
+      case 'u': {
+        int cp = hex4(p);
+        if (cp < 0) return r;
+        p += 4;
+        if (cp >= 0xD800 && cp <= 0xDBFF && p + 6 <= e && s[p] == '\\' && s[p + 1] == 'u') {
+          const int lo = hex4(p + 2);
+          if (lo >= 0xDC00 && lo <= 0xDFFF) {  // a surrogate pair is one code point
+            cp = 0x10000 + ((cp - 0xD800) << 10) + (lo - 0xDC00);
+            p += 6;
+          }
+        }
+        if (cp < 0x80) {
+          put((uint32_t)cp);
+        } else if (cp < 0x800) {
+          put(0xC0 | (cp >> 6)); put(0x80 | (cp & 0x3F));
+        } else if (cp < 0x10000) {
+          put(0xE0 | (cp >> 12)); put(0x80 | ((cp >> 6) & 0x3F)); put(0x80 | (cp & 0x3F));
+        } else {
+          put(0xF0 | (cp >> 18)); put(0x80 | ((cp >> 12) & 0x3F)); put(0x80 | ((cp >> 6) & 0x3F));
+          put(0x80 | (cp & 0x3F));
+        }
+        break;
+      }
+      default:
+        return r;
+    }
+  }
+  return r;
+}
+
+__device__ __forceinline__ uint64_t scan_str_esc(const uint8_t* s, uint64_t p, uint64_t e, Str& out, uint8_t* buf,
+                                                 uint32_t cap) {
+  const EscOut r = scan_str_esc_impl(s, p, e, buf, cap);
+  out.len = r.len;
+  out.w0 = r.w0;
+  out.w1 = r.w1;
+  out.esc = true;
+  return r.pos;
+}
 
 #define CT_IS(x, lit) ((x).len == slen(lit) && (x).w0 == pk8(lit, 0) && (x).w1 == pk8(lit, 8))
 
@@ -260,6 +377,7 @@ __device__ __forceinline__ uint32_t has_byte(uint32_t w, uint32_t rep) {
 // closing quote, or 0 on failure (the line holds no backslash / control / non-ASCII
 // byte; a raw tab is invalid in a strict JSON string).  ``wl``: bytes below wl may be
 // read as aligned 32-bit words (0: byte path only).
+template <bool ESC>
 __device__ __forceinline__ uint64_t scan_str(const uint8_t* s, uint64_t p, uint64_t e, Str& out, uint64_t wl) {
   const uint64_t p0 = p;
   if (p0 + 24 <= wl) {
@@ -270,11 +388,14 @@ __device__ __forceinline__ uint64_t scan_str(const uint8_t* s, uint64_t p, uint6
     uint32_t w = (*reinterpret_cast<const uint32_t*>(s + a) & ~lowm) | (0x78787878u & lowm);
     uint64_t pos = 0;
     while (true) {
-      const uint32_t hit = has_byte(w, 0x22222222u) | has_byte(w, 0x09090909u);
+      const uint32_t hit = has_byte(w, 0x22222222u) | has_byte(w, 0x09090909u) | has_byte(w, 0x5C5C5C5Cu);
       if (hit) {
         const uint32_t j = (uint32_t)(__ffs(hit) - 1) >> 3;
         pos = q + j;
-        if (pos >= e || ((w >> (8 * j)) & 0xFF) != '"') return 0;
+        if (pos >= e) return 0;
+        const uint32_t c = (w >> (8 * j)) & 0xFF;
+        if (c == '\\') return ESC ? scan_str_esc(s, p0, e, out, nullptr, 0) : 0;
+        if (c != '"') return 0;
         break;
       }
       q += 4;
@@ -283,6 +404,7 @@ __device__ __forceinline__ uint64_t scan_str(const uint8_t* s, uint64_t p, uint6
         pos = q;
         while (pos < e && s[pos] != '"') {
           if (s[pos] == '\t') return 0;
+          if (s[pos] == '\\') return ESC ? scan_str_esc(s, p0, e, out, nullptr, 0) : 0;
           pos++;
         }
         if (pos >= e) return 0;
@@ -315,6 +437,7 @@ __device__ __forceinline__ uint64_t scan_str(const uint8_t* s, uint64_t p, uint6
       return p + 1;
     }
     if (c == '\t') return 0;
+    if (c == '\\') return ESC ? scan_str_esc(s, p0, e, out, nullptr, 0) : 0;
     const uint64_t i = p - p0;
     if (i < 8) w0 |= (uint64_t)c << (8 * i);
     else if (i < 16) w1 |= (uint64_t)c << (8 * (i - 8));
@@ -326,11 +449,18 @@ __device__ __forceinline__ uint64_t scan_str(const uint8_t* s, uint64_t p, uint6
 // string body after the opening quote (the line holds no backslash / control byte /
 // non-ASCII byte; a raw tab is invalid in a strict JSON string): position after the
 // closing quote, or 0 on failure
+template <bool ESC>
 __device__ __forceinline__ uint64_t skip_string(const uint8_t* s, uint64_t p, uint64_t e) {
+  const uint64_t p0 = p;
   while (p < e) {
     const uint8_t c = s[p++];
     if (c == '"') return p;
     if (c == '\t') return 0;
+    if (c == '\\') {  // escapes are validated by the decoding scanner
+      if (!ESC) return 0;
+      Str x;
+      return scan_str_esc(s, p0, e, x, nullptr, 0);
+    }
   }
   return 0;
 }
@@ -380,6 +510,7 @@ __device__ __forceinline__ uint64_t skip_literal(const uint8_t* s, uint64_t p, u
 }
 
 // Any JSON value (grammar-checked, nesting <= 64): position after it, 0 on failure.
+template <bool ESC>
 __device__ uint64_t skip_value(const uint8_t* s, uint64_t p, uint64_t e) {
   uint64_t stack = 0;  // bit d: container at depth d is an object
   int depth = 0;
@@ -402,7 +533,7 @@ value:
       stack &= ~(1ull << depth); depth++;
       goto value;
     case '"':
-      p = skip_string(s, p + 1, e);
+      p = skip_string<ESC>(s, p + 1, e);
       if (!p) return 0;
       goto after;
     case 't': case 'f': case 'n':
@@ -417,7 +548,7 @@ value:
 key:
   p = skip_ws(s, p, e);
   if (p >= e || s[p] != '"') return 0;
-  p = skip_string(s, p + 1, e);
+  p = skip_string<ESC>(s, p + 1, e);
   if (!p) return 0;
   p = skip_ws(s, p, e);
   if (p >= e || s[p] != ':') return 0;
@@ -437,18 +568,31 @@ after:
 
 // A value of a consulted key -> (type, payload): ints as values, enum strings as codes,
 // the comm name as (offset | length << 40), anything else skipped as V_OTHER.
+template <bool ESC>
 __device__ uint64_t read_value(const uint8_t* s, uint64_t p, uint64_t e, int key, uint8_t& t, uint64_t& v,
-                           uint64_t wl) {
+                           uint64_t wl, const Side* side = nullptr) {
   p = skip_ws(s, p, e);
   if (p >= e) return 0;
   const uint8_t c = s[p];
   if (c == '"') {
     Str x;
-    const uint64_t q = scan_str(s, p + 1, e, x, wl);
+    const uint64_t q = scan_str<ESC>(s, p + 1, e, x, wl);
     if (!q) return 0;
     if (key == K_COMM) {
       t = V_NAME;
       v = (p + 1) | ((uint64_t)x.len << 40);
+      if (ESC && x.esc) {  // decoded name into the side buffer (too long / buffer full: the host reads the line)
+        t = V_OTHER;
+        if (side && x.len <= kMaxEscName) {
+          const unsigned long long off = atomicAdd(side->used, (unsigned long long)x.len);
+          if (off + x.len <= side->cap) {  // decode again, straight into the side buffer
+            Str y;
+            scan_str_esc(s, p + 1, e, y, side->buf + off, x.len);
+            t = V_NAME;
+            v = (off | kSideBit) | ((uint64_t)x.len << 40);
+          }
+        }
+      }
     } else {
       const int code = enum_of(key, x);
       t = code >= 0 ? V_ENUM : V_OTHER;
@@ -468,17 +612,18 @@ __device__ uint64_t read_value(const uint8_t* s, uint64_t p, uint64_t e, int key
     return q;
   }
   t = V_OTHER;
-  return skip_value(s, p, e);
+  return skip_value<ESC>(s, p, e);
 }
 
 // Endpoint object {"kind": <str>, "idx": <int>} (events.py:271-284) -> V_EP with
 // payload kind code (host 0, gpu 1, net 2; 0xFF absent/invalid) | idx << 8 (idx
 // 0xFFFFFFFF absent/invalid/too large); other members grammar-checked and ignored;
 // duplicate keys: last wins (json.loads).
+template <bool ESC>
 __device__ uint64_t read_endpoint(const uint8_t* s, uint64_t p, uint64_t e, uint8_t& t, uint64_t& v, uint64_t wl) {
   p = skip_ws(s, p, e);
   if (p >= e) return 0;
-  if (s[p] != '{') { t = V_OTHER; return skip_value(s, p, e); }
+  if (s[p] != '{') { t = V_OTHER; return skip_value<ESC>(s, p, e); }
   uint32_t kind = 0xFF, idx = 0xFFFFFFFFu;
   p = skip_ws(s, p + 1, e);
   if (p < e && s[p] == '}') { t = V_EP; v = kind | ((uint64_t)idx << 8); return p + 1; }
@@ -486,7 +631,7 @@ __device__ uint64_t read_endpoint(const uint8_t* s, uint64_t p, uint64_t e, uint
     p = skip_ws(s, p, e);
     if (p >= e || s[p] != '"') return 0;
     Str k;
-    p = scan_str(s, p + 1, e, k, wl);
+    p = scan_str<ESC>(s, p + 1, e, k, wl);
     if (!p) return 0;
     p = skip_ws(s, p, e);
     if (p >= e || s[p] != ':') return 0;
@@ -495,20 +640,20 @@ __device__ uint64_t read_endpoint(const uint8_t* s, uint64_t p, uint64_t e, uint
       p = skip_ws(s, p, e);
       if (p < e && s[p] == '"') {
         Str x;
-        p = scan_str(s, p + 1, e, x, wl);
+        p = scan_str<ESC>(s, p + 1, e, x, wl);
         if (!p) return 0;
         kind = CT_IS(x, "host") ? 0 : CT_IS(x, "gpu") ? 1 : CT_IS(x, "net") ? 2 : 0xFF;
       } else {
-        p = skip_value(s, p, e);
+        p = skip_value<ESC>(s, p, e);
         kind = 0xFF;
       }
     } else if (CT_IS(k, "idx")) {
       uint8_t wt = V_NONE;
       uint64_t wv = 0;
-      p = read_value(s, p, e, -1, wt, wv, wl);
+      p = read_value<ESC>(s, p, e, -1, wt, wv, wl);
       idx = wt == V_UINT && wv <= 0xFFFF ? (uint32_t)wv : 0xFFFFFFFFu;
     } else {
-      p = skip_value(s, p, e);
+      p = skip_value<ESC>(s, p, e);
     }
     if (!p) return 0;
     p = skip_ws(s, p, e);
@@ -527,20 +672,23 @@ struct LineOut {
 };
 
 __device__ __forceinline__ bool byte_blank(uint8_t c) { return c == ' ' || c == '\t' || c == 0x1f; }
-__device__ __forceinline__ bool byte_odd(uint8_t c) { return c >= 0x80 || c == '\\' || (c < 0x20 && c != '\t'); }
+// bytes the device does not read itself: raw control characters (invalid in JSON strings,
+// never JSON whitespace here).  Non-ASCII bytes and backslash escapes are decoded.
+__device__ __forceinline__ bool byte_odd(uint8_t c) { return c < 0x20 && c != '\t'; }
 
 // Line class before parsing: 0 blank (str.strip: the ASCII whitespace left inside a
 // line is space, tab, \x1f), 1 plain (no byte the device does not decode itself:
 // non-ASCII, backslash, control other than tab), 2 otherwise.  4 bytes at a time where
 // the text is word-aligned.
 __device__ __forceinline__ int line_class(const uint8_t* s, uint64_t b, uint64_t e, bool words) {
-  bool blank = true, plain = true;
+  bool blank = true, plain = true, bsl = false;
   uint64_t p = b;
   if (words) {
     for (; p < e && (p & 3); p++) {
       const uint8_t c = s[p];
       blank &= byte_blank(c);
       plain &= !byte_odd(c);
+      bsl |= c == '\\';
     }
     for (; p + 4 <= e; p += 4) {
       const uint32_t w = *reinterpret_cast<const uint32_t*>(s + p);
@@ -552,6 +700,7 @@ __device__ __forceinline__ int line_class(const uint8_t* s, uint64_t b, uint64_t
           const uint8_t c = (uint8_t)(w >> (8 * q));
           blank &= byte_blank(c);
           plain &= !byte_odd(c);
+          bsl |= c == '\\';
         }
       } else if (w != 0x20202020u) {
         blank = false;
@@ -562,20 +711,86 @@ __device__ __forceinline__ int line_class(const uint8_t* s, uint64_t b, uint64_t
     const uint8_t c = s[p];
     blank &= byte_blank(c);
     plain &= !byte_odd(c);
+    bsl |= c == '\\';
   }
-  return blank ? 0 : plain ? 1 : 2;
+  return blank ? 0 : !plain ? 2 : bsl ? 3 : 1;
+}
+
+// The canonical wire line -- write_trace's key order and compact separators
+// (events.py:251-291), which the reference, this package and the interposer all emit:
+//   {"seq":N,"ts":N,"kind":"K","comm":"S","nranks":N,"rank":N,"dev":N, then
+//   collective  "coll":"E","algo":"E","count":N,"dtype":"E"[,"root":N]}
+//   send / recv "peer":N,"count":N,"dtype":"E"}
+//   copies      "ckind":"E","src":{"kind":"E","idx":N},"dst":{...},"bytes":N}
+// matched literal by literal, values read by the generic readers.  true: every
+// consulted key was read into (types, fld) exactly as the generic loop would (the key
+// set is fixed, no duplicates, nothing else); false: any deviation -- the generic JSON
+// parser then reads the line from the start.  This skips the per-key name lookups,
+// which dominate the generic parse.
+template <int N>
+__device__ __forceinline__ bool lit_at(const uint8_t* s, uint64_t& p, uint64_t e, const char (&lit)[N]) {
+  if (p + (N - 1) > e) return false;
+  bool ok = true;
+#pragma unroll
+  for (int i = 0; i < N - 1; i++) ok &= s[p + i] == (uint8_t)lit[i];
+  p += N - 1;
+  return ok;
+}
+
+template <bool ESC>
+__device__ bool parse_canonical(const uint8_t* s, uint64_t b, uint64_t e, uint64_t wl, uint64_t* fld, int stride,
+                                uint64_t& types, const Side& side) {
+  uint64_t p = b;
+  auto val = [&](int key) -> bool {
+    uint8_t t = V_NONE;
+    uint64_t v = 0;
+    p = (key == K_SRC || key == K_DST) ? read_endpoint<ESC>(s, p, e, t, v, wl)
+                                       : read_value<ESC>(s, p, e, key, t, v, wl, &side);
+    types |= (uint64_t)t << (3 * key);
+    fld[key * stride] = v;
+    return p != 0;
+  };
+  types = 0;
+  if (!lit_at(s, p, e, "{\"seq\":") || !val(K_SEQ) || !lit_at(s, p, e, ",\"ts\":") || !val(K_TS) ||
+      !lit_at(s, p, e, ",\"kind\":") || !val(K_KIND) || !lit_at(s, p, e, ",\"comm\":") || !val(K_COMM) ||
+      !lit_at(s, p, e, ",\"nranks\":") || !val(K_NRANKS) || !lit_at(s, p, e, ",\"rank\":") || !val(K_RANK) ||
+      !lit_at(s, p, e, ",\"dev\":") || !val(K_DEV))
+    return false;
+  if (((types >> (3 * K_KIND)) & 7) != V_ENUM) return false;
+  const uint64_t kind = fld[K_KIND * stride];
+  if (kind == CT_KIND_COLLECTIVE) {
+    if (!lit_at(s, p, e, ",\"coll\":") || !val(K_COLL) || !lit_at(s, p, e, ",\"algo\":") || !val(K_ALGO) ||
+        !lit_at(s, p, e, ",\"count\":") || !val(K_COUNT) || !lit_at(s, p, e, ",\"dtype\":") || !val(K_DTYPE))
+      return false;
+    if (p < e && s[p] == ',' && (!lit_at(s, p, e, ",\"root\":") || !val(K_ROOT))) return false;
+  } else if (kind == CT_KIND_SEND || kind == CT_KIND_RECV) {
+    if (!lit_at(s, p, e, ",\"peer\":") || !val(K_PEER) || !lit_at(s, p, e, ",\"count\":") || !val(K_COUNT) ||
+        !lit_at(s, p, e, ",\"dtype\":") || !val(K_DTYPE))
+      return false;
+  } else {
+    if (!lit_at(s, p, e, ",\"ckind\":") || !val(K_CKIND) || !lit_at(s, p, e, ",\"src\":") || !val(K_SRC) ||
+        !lit_at(s, p, e, ",\"dst\":") || !val(K_DST) || !lit_at(s, p, e, ",\"bytes\":") || !val(K_BYTES))
+      return false;
+  }
+  if (!lit_at(s, p, e, "}")) return false;
+  return skip_ws(s, p, e) == e;  // "Extra data" otherwise (the generic path defers it)
 }
 
 // Parse line [b, e) of s; L_OK with `o` filled, L_BLANK, or L_DEFER.  ``fld`` is this
 // thread's field slots in shared memory (key k at fld[k * stride]).
+template <bool ESC>
 __device__ uint8_t parse_line(const uint8_t* s, uint64_t b, uint64_t e, bool words, uint64_t wl, uint64_t* fld,
-                              int stride, LineOut& o) {
+                              int stride, const Side& side, LineOut& o) {
   const int cls = line_class(s, b, e, words);
   if (cls == 0) return L_BLANK;
   if (cls == 2) return L_DEFER;
+  if (cls == 3 && !ESC) return L_ESC;
 
   // consulted fields: types 3 bits per key (register), payloads in shared memory
   uint64_t types = 0;
+  if (parse_canonical<ESC>(s, b, e, wl, fld, stride, types, side)) goto consulted;
+  types = 0;
+  {
   uint64_t p = skip_ws(s, b, e);
   if (p >= e || s[p] != '{') return L_DEFER;
   p = skip_ws(s, p + 1, e);
@@ -584,18 +799,19 @@ __device__ uint8_t parse_line(const uint8_t* s, uint64_t b, uint64_t e, bool wor
     p = skip_ws(s, p, e);
     if (p >= e || s[p] != '"') return L_DEFER;
     Str k;
-    p = scan_str(s, p + 1, e, k, wl);
+    p = scan_str<ESC>(s, p + 1, e, k, wl);
     if (!p) return L_DEFER;
     const int key = key_of(k);
     p = skip_ws(s, p, e);
     if (p >= e || s[p] != ':') return L_DEFER;
     p++;
     if (key < 0) {
-      p = skip_value(s, p, e);
+      p = skip_value<ESC>(s, p, e);
     } else {
       uint8_t t = V_NONE;
       uint64_t v = 0;
-      p = (key == K_SRC || key == K_DST) ? read_endpoint(s, p, e, t, v, wl) : read_value(s, p, e, key, t, v, wl);
+      p = (key == K_SRC || key == K_DST) ? read_endpoint<ESC>(s, p, e, t, v, wl)
+                                         : read_value<ESC>(s, p, e, key, t, v, wl, &side);
       types = (types & ~(7ull << (3 * key))) | ((uint64_t)t << (3 * key));
       fld[key * stride] = v;
     }
@@ -607,7 +823,9 @@ __device__ uint8_t parse_line(const uint8_t* s, uint64_t b, uint64_t e, bool wor
     return L_DEFER;
   }
   if (skip_ws(s, p, e) != e) return L_DEFER;  // "Extra data"
+  }
 
+consulted:
   // the reader's consulted keys and TraceEvent.validate, in effect (events.py:287-310)
   auto ty = [&](int key) -> uint32_t { return (uint32_t)(types >> (3 * key)) & 7; };
   auto fv = [&](int key) -> uint64_t { return ty(key) == V_NONE ? 0 : fld[key * stride]; };
@@ -677,8 +895,9 @@ __device__ uint8_t parse_line(const uint8_t* s, uint64_t b, uint64_t e, bool wor
   if ((f_comm >> 40) >= (1ull << 23)) return L_DEFER;  // name length field
   o.comm = f_comm;
   uint64_t h = 0xcbf29ce484222325ull;  // FNV-1a over the name bytes
-  const uint64_t coff = f_comm & ((1ull << 40) - 1), clen = f_comm >> 40;
-  for (uint64_t j = 0; j < clen; j++) h = (h ^ s[coff + j]) * 0x100000001b3ull;
+  const uint8_t* name = name_ptr(s, side.buf, f_comm);
+  const uint64_t clen = f_comm >> 40;
+  for (uint64_t j = 0; j < clen; j++) h = (h ^ name[j]) * 0x100000001b3ull;
   o.hash = h == kNoKey ? kNoKey - 1 : h;
   return L_OK;
 }
@@ -695,7 +914,7 @@ constexpr uint32_t kStageSlack = 32;  // readable bytes past the stage (word sca
 
 __global__ void __launch_bounds__(kParseThreads) k_parse(const uint8_t* s, uint64_t size, bool aligned,
                                                          const uint64_t* brk, uint64_t nb, uint64_t n_lines,
-                                                         uint8_t* status, LineOut* out) {
+                                                         uint8_t* status, LineOut* out, Side side) {
   extern __shared__ __align__(16) uint8_t stage[];
   const uint64_t k0 = blockIdx.x * (uint64_t)kParseThreads;
   const uint64_t k1 = min(k0 + kParseThreads, n_lines) - 1;  // last line of the block
@@ -728,12 +947,37 @@ __global__ void __launch_bounds__(kParseThreads) k_parse(const uint8_t* s, uint6
   // word reads may run up to 24 bytes past a string start: the stage has that slack,
   // the global text is read wordwise only away from its end
   const uint64_t wl = !aligned ? 0 : staged ? span_b + kStage + kStageSlack : (size > 32 ? size - 8 : 0);
-  const uint8_t st = parse_line(src, line_begin(k), line_end(k), aligned, wl, fields + threadIdx.x, kParseThreads, o);
+  const uint8_t st =
+      parse_line<false>(src, line_begin(k), line_end(k), aligned, wl, fields + threadIdx.x, kParseThreads, side, o);
   status[k] = st;
   if (st == L_OK) {
     out[k] = o;
   }
 }
+
+// Lines holding escapes (L_ESC after k_parse), one thread each, straight from the text:
+// the same parser with \\ / \\uXXXX decoding (comm names into the side buffer).
+__global__ void __launch_bounds__(kParseThreads) k_parse_esc(const uint8_t* s, uint64_t size, bool aligned,
+                                                             const uint64_t* brk, uint64_t nb, const uint64_t* lines,
+                                                             const uint64_t* n_esc, uint8_t* status, LineOut* out,
+                                                             Side side) {
+  __shared__ uint64_t fields[K_N * kParseThreads];
+  const uint64_t j = blockIdx.x * (uint64_t)kParseThreads + threadIdx.x;
+  if (j >= *n_esc) return;
+  const uint64_t k = lines[j];
+  const uint64_t b = k == 0 ? 0 : brk[k - 1] + break_len(s, size, brk[k - 1]);
+  const uint64_t e = k < nb ? brk[k] : size;
+  const uint64_t wl = aligned && size > 32 ? size - 8 : 0;
+  LineOut o;
+  const uint8_t st = parse_line<true>(s, b, e, aligned, wl, fields + threadIdx.x, kParseThreads, side, o);
+  status[k] = st;
+  if (st == L_OK) out[k] = o;
+}
+
+struct IsEsc {
+  const uint8_t* st;
+  __device__ __forceinline__ bool operator()(uint64_t k) const { return st[k] == L_ESC; }
+};
 
 struct NonBlank {
   const uint8_t* st;
@@ -794,15 +1038,16 @@ __global__ void k_iota(uint64_t n, uint64_t* out) {
 }
 
 __global__ void k_verify(uint64_t m, const uint64_t* keys, const uint64_t* vals, const uint32_t* seg,
-                         const uint64_t* seg_coff, const uint64_t* coff, const uint8_t* s, unsigned int* collide) {
+                         const uint64_t* seg_coff, const uint64_t* coff, const uint8_t* s, const uint8_t* side,
+                         unsigned int* collide) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
     if (keys[i] == kNoKey) continue;
     const uint64_t a = coff[vals[i]], h = seg_coff[seg[i] - 1];
     if (a == h) continue;
     const uint32_t la = (uint32_t)(a >> 40), lh = (uint32_t)(h >> 40);
     bool same = la == lh;
-    const uint64_t oa = a & ((1ull << 40) - 1), oh = h & ((1ull << 40) - 1);
-    for (uint32_t j = 0; same && j < la; j++) same = s[oa + j] == s[oh + j];
+    const uint8_t *na = name_ptr(s, side, a), *nh = name_ptr(s, side, h);
+    for (uint32_t j = 0; same && j < la; j++) same = na[j] == nh[j];
     if (!same) atomicOr(collide, 1u);
   }
 }
@@ -826,11 +1071,13 @@ struct NameLen {
 };
 
 __global__ void k_names(uint64_t u, const uint64_t* seg_order, const uint64_t* seg_first, const uint64_t* seg_coff,
-                        const uint64_t* name_off, const uint8_t* s, uint8_t* names, uint64_t* rows) {
+                        const uint64_t* name_off, const uint8_t* s, const uint8_t* side, uint8_t* names,
+                        uint64_t* rows) {
   for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < u; r += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t g = seg_order[r], c = seg_coff[g];
-    const uint64_t len = c >> 40, off = c & ((1ull << 40) - 1);
-    for (uint64_t j = 0; j < len; j++) names[name_off[r] + j] = s[off + j];
+    const uint64_t len = c >> 40;
+    const uint8_t* nm = name_ptr(s, side, c);
+    for (uint64_t j = 0; j < len; j++) names[name_off[r] + j] = nm[j];
     rows[3 * r] = seg_first[g];
     rows[3 * r + 1] = name_off[r];
     rows[3 * r + 2] = len;
@@ -962,12 +1209,35 @@ int run(ct_jsonl* j, const uint8_t* text, uint64_t size, int on_device) {
   uint64_t* ridx = pool.alloc<uint64_t>(n_lines + 1);
   JL_NN(status); JL_NN(lo); JL_NN(ridx);
   JL_TRY(cudaMemsetAsync(status + n_lines, L_BLANK, 1, j->st));
+  // decoded (escaped) comm names: up to 16 MB, the rest of such lines are read on the host
+  const uint64_t side_cap = std::min<uint64_t>(16ull << 20, std::max<uint64_t>(size, 1024));
+  uint8_t* side = pool.alloc<uint8_t>(side_cap);
+  JL_NN(side);
   if (n_lines) {
     JL_TRY(cudaFuncSetAttribute(k_parse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kStage + kStageSlack)));
     k_parse<<<(unsigned)((n_lines + kParseThreads - 1) / kParseThreads), kParseThreads, kStage + kStageSlack, j->st>>>(
-        s, size, aligned, brk, nb, n_lines, status, lo);
+        s, size, aligned, brk, nb, n_lines, status, lo, Side{side, reinterpret_cast<unsigned long long*>(scal + 4),
+                                                             side_cap});
   }
   JL_TRY(cudaGetLastError());
+  if (n_lines) {  // lines with escapes: compacted, parsed by the escape-decoding instantiation
+    uint64_t* elines = pool.alloc<uint64_t>(n_lines);
+    JL_NN(elines);
+    tb = 0;
+    IsEsc ise{status};
+    JL_TRY(cub::DeviceSelect::If(nullptr, tb, idx, elines, scal + 3, (int64_t)n_lines, ise, j->st));
+    t = pool.temp(tb);
+    JL_NN(t);
+    JL_TRY(cub::DeviceSelect::If(t, tb, idx, elines, scal + 3, (int64_t)n_lines, ise, j->st));
+    uint64_t ne = 0;
+    JL_TRY(cudaMemcpyAsync(&ne, scal + 3, sizeof(uint64_t), cudaMemcpyDeviceToHost, j->st));
+    JL_TRY(cudaStreamSynchronize(j->st));
+    if (ne)
+      k_parse_esc<<<(unsigned)((ne + kParseThreads - 1) / kParseThreads), kParseThreads, 0, j->st>>>(
+          s, size, aligned, brk, nb, elines, scal + 3, status, lo,
+          Side{side, reinterpret_cast<unsigned long long*>(scal + 4), side_cap});
+    JL_TRY(cudaGetLastError());
+  }
   auto nb_it = thrust::make_transform_iterator(idx, NonBlank{status});
   tb = 0;
   JL_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tb, nb_it, ridx, (int64_t)n_lines + 1, j->st));
@@ -1047,7 +1317,7 @@ int run(ct_jsonl* j, const uint8_t* text, uint64_t size, int on_device) {
   if (u) {
     const int g = grid_for(n_rec);
     k_heads<<<g, 256, 0, j->st>>>(n_rec, keys2, vals2, seg, seg_first, seg_coff, coff);
-    k_verify<<<g, 256, 0, j->st>>>(n_rec, keys2, vals2, seg, seg_coff, coff, s, flags);
+    k_verify<<<g, 256, 0, j->st>>>(n_rec, keys2, vals2, seg, seg_coff, coff, s, side, flags);
     JL_TRY(cudaGetLastError());
     k_iota<<<grid_for(u), 256, 0, j->st>>>(u, seg_ids);
     tb = 0;
@@ -1072,7 +1342,8 @@ int run(ct_jsonl* j, const uint8_t* text, uint64_t size, int on_device) {
     name_bytes = lastoff + (lastc >> 40);
     j->names = pool.alloc<uint8_t>(name_bytes);
     JL_NN(j->names);
-    k_names<<<grid_for(u), 256, 0, j->st>>>(u, seg_order, seg_first, seg_coff, name_off, s, j->names, j->comm_rows);
+    k_names<<<grid_for(u), 256, 0, j->st>>>(u, seg_order, seg_first, seg_coff, name_off, s, side, j->names,
+                                            j->comm_rows);
     JL_TRY(cudaGetLastError());
   }
   j->info.comm_bytes = name_bytes;
@@ -1104,7 +1375,7 @@ int ct_jsonl_parse(int device, const char* text, uint64_t size, int on_device, c
   *out = j;
   j->device = device;
   if (!text && size) { j->err = "null text"; return CT_ERR_ARGUMENT; }
-  if (size >= (1ull << 40)) { j->err = "text larger than 2^40 bytes"; return CT_ERR_ARGUMENT; }
+  if (size >= (1ull << 39)) { j->err = "text larger than 2^39 bytes"; return CT_ERR_ARGUMENT; }
   cudaError_t e = cudaSetDevice(device);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&j->st, cudaStreamNonBlocking);
   if (e != cudaSuccess) { j->err = cudaGetErrorString(e); return CT_ERR_CUDA; }

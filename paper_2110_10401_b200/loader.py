@@ -7,9 +7,11 @@ offending line) as ``pack_events(parse_trace(text))``.
 
 The sm_100a library splits lines (``str.splitlines`` terminators), parses, checks and
 packs every line it can prove the reference accepts unchanged, and interns comm names
-(``csrc/ct_jsonl.cu``).  The remaining "deferred" lines (non-ASCII text, escapes,
-floats / bools / huge integers in consulted keys, and every malformed or invalid
-line) are read here with the reference-mirroring line reader
+(``csrc/ct_jsonl.cu``), non-ASCII text and ``\\`` / ``\\uXXXX`` escapes included (names
+decoded on the device).  The remaining "deferred" lines (raw control characters,
+floats / bools / huge integers in consulted keys, escaped comm names longer than 256
+bytes, and every malformed or invalid line) are read here with the reference-mirroring
+line reader
 (``events._parse_line``): for a well-formed trace that is normally none of them; for
 a broken one it is where the reference's exception is raised.  Device-accepted lines
 can never raise, so the first exception is the reference's.  There is no CPU path for
@@ -95,7 +97,8 @@ def load_trace(source, device: int | None = None) -> PackedTrace:
     comm_first = {}
     for cid in range(nc):
         first, off, ln = (int(x) for x in crows[cid])
-        comm_first[name_bytes[off:off + ln].decode("ascii")] = (first, cid)
+        # raw UTF-8 or decoded escapes (lone surrogates as in "surrogatepass")
+        comm_first[name_bytes[off:off + ln].decode("utf-8", "surrogatepass")] = (first, cid)
     load_info = {"lines": int(info.n_lines), "deferred": nd, "device_comms": nc,
                  "ms_device": float(info.ms_device)}
     if nd == 0:

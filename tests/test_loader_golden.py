@@ -115,3 +115,32 @@ def test_device_resident_text_matches_reference(fuzz_golden):
             if data:
                 buf[off:] = torch.frombuffer(bytearray(data), dtype=torch.uint8).cuda()
             check(load_trace, buf[off:], expect(row, "bytes"))
+
+
+@pytest.mark.gpu
+def test_escapes_and_non_ascii_parse_on_device():
+    """Raw UTF-8 names and \\uXXXX / \\" escapes (the reference's own write_trace escapes
+    every non-ASCII name) are decoded on the device: nothing is left to the host reader,
+    and one name written both ways is one communicator."""
+    import json
+
+    from paper_2110_10401_b200.events import parse_trace
+    from paper_2110_10401_b200.loader import load_trace
+    from paper_2110_10401_b200.packed import pack_events
+
+    names = ["café", "日本", "\U0001f600", 'q"uote', "back\\slash", "tab\tname", "\ud83d"]
+    lines = []
+    for k in range(400):
+        nm = names[k % len(names)]
+        o = {"seq": k // 2, "ts": k, "kind": "collective", "comm": nm, "nranks": 2, "rank": k % 2, "dev": k % 2,
+             "coll": "allreduce", "algo": "ring", "count": 100 + k // 2, "dtype": "float32"}
+        ascii_form = k % 3 != 0 or "\ud83d" in nm  # write_trace style (\\u escapes) or raw UTF-8
+        lines.append(json.dumps(o, separators=(",", ":"), ensure_ascii=ascii_form))
+    lines.append(json.dumps({"seq": 0, "ts": 0, "kind": "coll\\u0065ctive"}))  # escaped enum: rejected exactly
+    text = "\n".join(lines[:-1]) + "\n"
+    data = text.encode("utf-8", "surrogatepass")
+    got = load_trace(data)
+    ref = pack_events(parse_trace(data.decode("utf-8", "surrogatepass")))
+    assert got.load_info["deferred"] == 0
+    assert got.records.cpu().numpy().tobytes() == ref.records.tobytes()
+    assert got.comms == ref.comms and len(got.comms) == len(names)
