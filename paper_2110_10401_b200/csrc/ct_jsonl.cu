@@ -60,13 +60,36 @@ __device__ __forceinline__ uint32_t break_mask16(const uint8_t* s, uint64_t n, u
   uint8_t b[16];
   if (aligned && i0 + 16 <= n) {
     const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-    // candidates are bytes < 0x20 or >= 0x80: most 16-byte chunks have none
-    uint32_t any = 0;
+    // candidates are bytes < 0x20 or >= 0x80 (a superset: borrow artefacts above a true
+    // candidate are re-checked): most 16-byte chunks have none, a line end has one
+    uint32_t cand = 0;
 #pragma unroll
-    for (int q = 0; q < 4; q++) any |= ((w[q] - 0x20202020u) & ~w[q]) | w[q];
-    if (!(any & 0x80808080u)) return 0;
-#pragma unroll
-    for (int j = 0; j < 16; j++) b[j] = (uint8_t)(w[j >> 2] >> (8 * (j & 3)));
+    for (int q = 0; q < 4; q++) {
+      const uint32_t t = (((w[q] - 0x20202020u) & ~w[q]) | w[q]) & 0x80808080u;
+      cand |= (((t >> 7) & 1u) | ((t >> 14) & 2u) | ((t >> 21) & 4u) | ((t >> 28) & 8u)) << (4 * q);
+    }
+    if (!cand) return 0;
+    uint32_t m = 0;
+    bool hi = false;
+    while (cand) {
+      const int j = __ffs(cand) - 1;
+      cand &= cand - 1;
+      const uint32_t c = (w[j >> 2] >> (8 * (j & 3))) & 0xFF;
+      auto at = [&](int k) -> uint32_t {  // byte k of the chunk, or of the text beyond it
+        return k < 16 ? (w[k >> 2] >> (8 * (k & 3))) & 0xFF : (i0 + k < n ? s[i0 + k] : 0u);
+      };
+      const uint64_t i = i0 + j;
+      hi |= c >= 0x80;
+      bool brk;
+      if (c == '\n') brk = j > 0 ? at(j - 1) != '\r' : (i == 0 || s[i - 1] != '\r');
+      else if (c == '\r' || c == 0x0b || c == 0x0c || c == 0x1c || c == 0x1d || c == 0x1e) brk = true;
+      else if (c == 0xC2) brk = at(j + 1) == 0x85;
+      else if (c == 0xE2) brk = at(j + 1) == 0x80 && (at(j + 2) == 0xA8 || at(j + 2) == 0xA9);
+      else brk = false;
+      if (brk) m |= 1u << j;
+    }
+    non_ascii = hi;
+    return m;
   } else {
 #pragma unroll
     for (int j = 0; j < 16; j++) b[j] = i0 + j < n ? s[i0 + j] : (uint8_t)'x';
