@@ -64,16 +64,24 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objs = []
     obj_dir = os.path.join(OUT or PKG, "_obj")
     os.makedirs(obj_dir, exist_ok=True)
+    cmds = []
     for src in SOURCES:
         path = os.path.join(CSRC, src)
         if not os.path.exists(path):
             continue
         obj = os.path.join(obj_dir, src.replace(".cu", ".o"))
-        cmd = [NVCC, *FLAGS, "-c", path, "-o", obj]
+        cmds.append([NVCC, *FLAGS, "-c", path, "-o", obj])
+        objs.append(obj)
+    # translation units compile independently: one nvcc per source, in parallel
+    from concurrent.futures import ThreadPoolExecutor
+
+    def _cc(cmd):
         if verbose:
             print(" ".join(cmd))
         subprocess.run(cmd, check=True)
-        objs.append(obj)
+
+    with ThreadPoolExecutor(max_workers=max(1, min(len(cmds), os.cpu_count() or 1))) as ex:
+        list(ex.map(_cc, cmds))
     cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB, *objs,
            "-lcudart"]
     subprocess.run(cmd, check=True)
