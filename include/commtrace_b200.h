@@ -245,6 +245,8 @@ typedef struct ct_jsonl_info {
   uint64_t comm_bytes;  /* total bytes of those names                               */
   uint32_t non_ascii;   /* 1: the text holds bytes >= 0x80 (UTF-8 check is the caller's) */
   float ms_device;      /* device time of the parse (CUDA events)                   */
+  uint32_t fused;       /* 1: the single-pass loader took the text, 0: the multi-pass one */
+  uint64_t n_slow;      /* single pass: lines read by the generic parser (not the template) */
 } ct_jsonl_info;
 /* Parse ``size`` bytes (host or device memory).  *out is always set (free it with
  * ct_jsonl_free, also on error; message via ct_jsonl_error). */

@@ -127,6 +127,8 @@ class CtJsonlInfo(C.Structure):
         ("comm_bytes", C.c_uint64),
         ("non_ascii", C.c_uint32),
         ("ms_device", C.c_float),
+        ("fused", C.c_uint32),
+        ("n_slow", C.c_uint64),
     ]
 
 

@@ -22,7 +22,12 @@
 #include <thrust/iterator/counting_iterator.h>
 #include <thrust/iterator/transform_iterator.h>
 
+#include <algorithm>
+#include <array>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
 #include <string>
 #include <vector>
 
@@ -1120,6 +1125,795 @@ __global__ void k_deferred_rows(uint64_t nd, const uint64_t* lines, const uint64
   }
 }
 
+
+// ---------------------------------------------------------------- fused single pass
+// The common case in one pass over the text.  One CTA per 32 KB tile,
+// claimed in text order through a ticket.  A line belongs to the tile holding its
+// terminator (the final unterminated line: the last tile); its start lies in the tile
+// or in the kFM bytes before it, which are staged with the tile.  Per tile: terminator
+// masks over the staged bytes -> ordered line ends; a blank test per line -> record
+// slots; a decoupled look-back over earlier tiles -> the tile's first line number and
+// record slot; then every line goes through the canonical-template parser (thread per
+// line, from shared memory) or onto the slow list, which the generic parser (escapes
+// included) reads in the next kernel.  Comm names are interned through a per-CTA cache
+// into a global open-addressing table of 64-bit name keys; records carry the table slot
+// until the final remap into first-seen order.  Outside these bounds (a line longer than
+// the look-behind, > kFMaxLines lines in a tile, > kFMaxNames names, lists or record
+// slots beyond their capacity) the fallback flag is raised and the caller reruns the
+// multi-pass pipeline, which has no such bounds.
+constexpr int kFThreads = 256;
+constexpr uint32_t kFT = 32 * 1024;   // terminator bytes per tile
+constexpr uint32_t kFM = 4 * 1024;    // look-behind: a line may start this far before its tile
+constexpr uint32_t kFStage = kFM + kFT + 128;  // + zero padding (template reads overrun)
+static_assert(kFM + kFT < 65536, "line ends are 16-bit stage offsets");
+constexpr int kFMaxLines = 2048;
+constexpr int kFMaxRecs = 512;        // records per tile (non-blank lines averaging >= 64 bytes)
+constexpr int kFCache = 64;           // per-CTA name cache entries
+constexpr uint32_t kFNameMax = 32;    // longest name the cache holds (longer: slow list)
+constexpr uint32_t kFTable = 1u << 14;
+constexpr uint32_t kFMaxNames = 2048;  // distinct names (k_ffinal ranks them in one CTA)
+constexpr uint64_t kFNameCap = 1ull << 20;
+constexpr uint64_t kFListCap = 1ull << 22;
+
+enum : uint32_t { FB_FALLBACK = 1, FB_NONASCII = 2, FB_COLLIDE = 4 };
+
+struct FCtl {
+  unsigned long long ticket;
+  unsigned long long n_lines, n_recs;
+  unsigned long long n_slow, n_defer, n_verify;
+  unsigned long long name_bytes;
+  unsigned int flags, n_names, n_used;
+  unsigned int pad;
+};
+
+struct FArgs {
+  const uint8_t* s;
+  uint64_t size, ntiles, cap;
+  FCtl* ctl;
+  uint32_t* tcnt;             // per tile: lines, records
+  unsigned long long* toff;    // per tile: first line, first record (k_fscan)
+  ct_record* trec;             // per tile: kFMaxRecs temporary record slots
+  int64_t* tts;
+  ct_record* recs;             // final records / timestamps (k_fcompact)
+  int64_t* ts;
+  unsigned long long *gkey, *gname, *gfirst;  // name table: key, name ref, first record slot
+  uint32_t* gid;                               // table slot -> comm id
+  uint64_t *slow, *defer, *verify;             // 4, 4, 2 words per entry
+  uint64_t* comm_rows;
+  uint8_t* names;
+  uint64_t lcap;  // entries of each list
+  Side side;
+};
+
+__device__ __forceinline__ void fb(const FArgs& A, uint32_t f) { atomicOr(&A.ctl->flags, f); }
+
+// 64-bit name key: little-endian 8-byte words (zero-padded), then the length; never 0
+__device__ __forceinline__ uint64_t nk_mix(uint64_t h, uint64_t w) {
+  h = (h ^ w) * 0x9E3779B97F4A7C15ull;
+  return h ^ (h >> 29);
+}
+__device__ __forceinline__ uint64_t nk_final(uint64_t h, uint32_t len) {
+  h = nk_mix(h, len);
+  return h ? h : 1;
+}
+__device__ uint64_t name_key_bytes(const uint8_t* p, uint32_t len) {
+  uint64_t h = 0x243F6A8885A308D3ull;
+  for (uint32_t i = 0; i < len; i += 8) {
+    uint64_t w = 0;
+    for (uint32_t k = 0; k < 8 && i + k < len; k++) w |= (uint64_t)p[i + k] << (8 * k);
+    h = nk_mix(h, w);
+  }
+  return nk_final(h, len);
+}
+
+// global name table slot of ``key`` (inserted with its name reference when new), -1: full
+__device__ int table_slot(const FArgs& A, uint64_t key, uint64_t ref) {
+  uint32_t i = (uint32_t)(key ^ (key >> 32)) & (kFTable - 1);
+  for (uint32_t probe = 0; probe < kFTable / 2; probe++) {
+    const unsigned long long old = atomicCAS(&A.gkey[i], 0ull, (unsigned long long)key);
+    if (old == 0) {
+      A.gname[i] = ref;
+      if (atomicAdd(&A.ctl->n_names, 1u) >= kFMaxNames) fb(A, FB_FALLBACK);
+      return (int)i;
+    }
+    if (old == key) return (int)i;
+    i = (i + 1) & (kFTable - 1);
+  }
+  fb(A, FB_FALLBACK);
+  return -1;
+}
+
+__device__ __forceinline__ bool list_put(const FArgs& A, unsigned long long* cnt, uint64_t* list, int words,
+                                         uint64_t a, uint64_t b, uint64_t c, uint64_t d) {
+  const unsigned long long i = atomicAdd(cnt, 1ull);
+  if (i >= A.lcap) { fb(A, FB_FALLBACK); return false; }
+  list[words * i] = a;
+  list[words * i + 1] = b;
+  if (words == 4) { list[4 * i + 2] = c; list[4 * i + 3] = d; }
+  return true;
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// unaligned 8 bytes of the (16-byte aligned) stage at p
+__device__ __forceinline__ uint64_t st8(const uint8_t* st, uint32_t p) {
+  const uint32_t* W = reinterpret_cast<const uint32_t*>(st);
+  const uint32_t i = p >> 2, sh = (p & 3) * 8;
+  const uint32_t w0 = W[i], w1 = W[i + 1], w2 = W[i + 2];
+  return (uint64_t)__funnelshift_r(w0, w1, sh) | ((uint64_t)__funnelshift_r(w1, w2, sh) << 32);
+}
+
+// terminator starts in stage bytes [q, q + 16) (absolute position st0 + q): the same
+// rules as break_mask16; bytes at or past ``size`` are never terminators
+__device__ uint32_t brk16s(const uint8_t* st, uint32_t q, uint64_t st0, const uint8_t* s, uint64_t size,
+                           bool& non_ascii) {
+  non_ascii = false;
+  const uint4 v = *reinterpret_cast<const uint4*>(st + q);
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+  uint32_t cand = 0;
+#pragma unroll
+  for (int k = 0; k < 4; k++) {
+    const uint32_t t = (((w[k] - 0x20202020u) & ~w[k]) | w[k]) & 0x80808080u;
+    cand |= (((t >> 7) & 1u) | ((t >> 14) & 2u) | ((t >> 21) & 4u) | ((t >> 28) & 8u)) << (4 * k);
+  }
+  if (!cand) return 0;
+  uint32_t m = 0;
+  bool hi = false;
+  while (cand) {
+    const int j = __ffs(cand) - 1;
+    cand &= cand - 1;
+    const uint64_t i = st0 + q + j;
+    if (i >= size) break;
+    const uint32_t c = st[q + j];
+    hi |= c >= 0x80;
+    bool brk;
+    if (c == '\n') brk = q + j > 0 ? st[q + j - 1] != '\r' : (i == 0 || s[i - 1] != '\r');
+    else if (c == '\r' || c == 0x0b || c == 0x0c || c == 0x1c || c == 0x1d || c == 0x1e) brk = true;
+    else if (c == 0xC2) brk = i + 1 < size && st[q + j + 1] == 0x85;
+    else if (c == 0xE2) brk = i + 2 < size && st[q + j + 1] == 0x80 && (st[q + j + 2] == 0xA8 || st[q + j + 2] == 0xA9);
+    else brk = false;
+    if (brk) m |= 1u << j;
+  }
+  non_ascii = hi;
+  return m;
+}
+
+__device__ __forceinline__ uint32_t blen_s(const uint8_t* st, uint32_t p, uint32_t nst) {
+  const uint8_t b = st[p];
+  if (b == '\r') return p + 1 < nst && st[p + 1] == '\n' ? 2 : 1;
+  if (b == 0xC2) return 2;
+  if (b == 0xE2) return 3;
+  return 1;
+}
+
+// ---- canonical-template parser over the stage (write_trace's key order, compact
+// separators; see parse_canonical).  Every byte of [b, e) is consumed by a literal, a
+// number, an enum value or the comm name, so acceptance implies a plain line.
+struct FLine {
+  ct_record r;
+  int64_t ts;
+  uint64_t key;       // name key
+  uint32_t nb, nlen;  // name: stage offset, length
+};
+
+template <int N>
+__device__ __forceinline__ bool flit(const uint8_t* st, uint32_t& p, const char (&lit)[N]) {
+  constexpr int L = N - 1;
+  uint64_t v0 = 0, v1 = 0;
+#pragma unroll
+  for (int i = 0; i < L && i < 8; i++) v0 |= (uint64_t)(uint8_t)lit[i] << (8 * i);
+#pragma unroll
+  for (int i = 8; i < L && i < 16; i++) v1 |= (uint64_t)(uint8_t)lit[i] << (8 * (i - 8));
+  const uint64_t m0 = L >= 8 ? ~0ull : (1ull << (8 * L)) - 1;
+  const uint64_t m1 = L <= 8 ? 0ull : (L >= 16 ? ~0ull : (1ull << (8 * (L - 8))) - 1);
+  bool ok = (st8(st, p) & m0) == v0;
+  if (L > 8) ok = ok && (st8(st, p + 8) & m1) == v1;
+  if (L > 16) ok = ok && st[p + 16] == (uint8_t)lit[16];
+  p += L;
+  return ok;
+}
+
+__constant__ uint64_t kPow10[9] = {1ull, 10ull, 100ull, 1000ull, 10000ull, 100000ull, 1000000ull, 10000000ull,
+                                   100000000ull};
+
+// up to 8 digit values (first digit in the lowest byte) -> integer
+__device__ __forceinline__ uint64_t swar8(uint64_t d, uint32_t k) {
+  d <<= 8 * (8 - k);
+  d = (d * 10 + (d >> 8)) & 0x00FF00FF00FF00FFull;
+  d = (d * 100 + (d >> 16)) & 0x0000FFFF0000FFFFull;
+  return (d * 10000 + (d >> 32)) & 0xFFFFFFFFull;
+}
+
+// JSON integer (no sign) of <= 19 digits at p: false for anything else (leading zeros,
+// 20+ digits; fractions / exponents fail on the literal that follows)
+__device__ __forceinline__ bool fnum(const uint8_t* st, uint32_t& p, uint64_t& v) {
+  uint64_t x = st8(st, p) ^ 0x3030303030303030ull;
+  uint64_t nd = ((x + 0x7676767676767676ull) | x) & 0x8080808080808080ull;
+  uint32_t k = nd ? (uint32_t)(__ffsll((long long)nd) - 1) >> 3 : 8u;
+  if (k == 0 || ((x & 0xFF) == 0 && k > 1)) return false;
+  v = swar8(x, k);
+  uint32_t tot = k;
+  while (k == 8) {
+    x = st8(st, p + tot) ^ 0x3030303030303030ull;
+    nd = ((x + 0x7676767676767676ull) | x) & 0x8080808080808080ull;
+    k = nd ? (uint32_t)(__ffsll((long long)nd) - 1) >> 3 : 8u;
+    if (tot + k > 19) return false;
+    if (k) v = v * kPow10[k] + swar8(x, k);
+    tot += k;
+  }
+  p += tot;
+  return true;
+}
+
+// string body at p (after the quote) up to 16 bytes without escapes: packed value for
+// enum_of; p moves past the closing quote
+__device__ __forceinline__ bool fstr16(const uint8_t* st, uint32_t& p, Str& out) {
+  const uint64_t x = st8(st, p), y = st8(st, p + 8);
+  const uint64_t qx = x ^ 0x2222222222222222ull, qy = y ^ 0x2222222222222222ull;
+  const uint64_t zx = (qx - 0x0101010101010101ull) & ~qx & 0x8080808080808080ull;
+  const uint64_t zy = (qy - 0x0101010101010101ull) & ~qy & 0x8080808080808080ull;
+  uint32_t len;
+  if (zx) len = (uint32_t)(__ffsll((long long)zx) - 1) >> 3;
+  else if (zy) len = 8 + ((uint32_t)(__ffsll((long long)zy) - 1) >> 3);
+  else return false;
+  out.len = len;
+  out.w0 = len >= 8 ? x : (x & ((1ull << (8 * len)) - 1));
+  out.w1 = len <= 8 ? 0ull : (y & ((1ull << (8 * (len - 8))) - 1));
+  p += len + 1;
+  return true;
+}
+
+// the comm name at p (after the quote): plain printable ASCII without '"' / '\\', at most
+// kFNameMax bytes; key accumulated over 8-byte words
+__device__ __forceinline__ bool fname(const uint8_t* st, uint32_t& p, uint32_t& len, uint64_t& key) {
+  uint64_t h = 0x243F6A8885A308D3ull;
+  for (uint32_t i = 0; i <= kFNameMax; i += 8) {
+    const uint64_t x = st8(st, p + i);
+    const uint64_t qx = x ^ 0x2222222222222222ull, bx = x ^ 0x5C5C5C5C5C5C5C5Cull;
+    const uint64_t q = (qx - 0x0101010101010101ull) & ~qx & 0x8080808080808080ull;
+    const uint64_t bad = (((bx - 0x0101010101010101ull) & ~bx) | (x - 0x2020202020202020ull) | x) &
+                         0x8080808080808080ull;  // backslash, control, non-ASCII (a superset past the quote)
+    if (q) {
+      const uint32_t j = (uint32_t)(__ffsll((long long)q) - 1) >> 3;
+      if (bad & ((1ull << (8 * j)) - 1)) return false;
+      len = i + j;
+      if (len > kFNameMax) return false;
+      if (j) h = nk_mix(h, x & ((1ull << (8 * j)) - 1));
+      key = nk_final(h, len);
+      p += len + 1;
+      return true;
+    }
+    if (bad) return false;
+    h = nk_mix(h, x);
+  }
+  return false;
+}
+
+// the common head {"seq":N,"ts":N,"kind":"K","comm":"S","nranks":N,"rank":N,"dev":N: p
+// moves to the kind-specific part
+__device__ bool fast_prefix(const uint8_t* st, uint32_t& p, FLine& o, int& kind) {
+  uint64_t seq, tsm, n, rank, dev;
+  bool neg = false;
+  Str kv;
+  if (!flit(st, p, "{\"seq\":") || !fnum(st, p, seq) || !flit(st, p, ",\"ts\":")) return false;
+  if (st[p] == '-') { neg = true; p++; }
+  if (!fnum(st, p, tsm) || !flit(st, p, ",\"kind\":\"") || !fstr16(st, p, kv)) return false;
+  kind = enum_of(K_KIND, kv);
+  if (kind < 0 || !flit(st, p, ",\"comm\":\"") || !fname(st, p, o.nlen, o.key)) return false;
+  o.nb = p - o.nlen - 1;
+  if (!flit(st, p, ",\"nranks\":") || !fnum(st, p, n) || !flit(st, p, ",\"rank\":") || !fnum(st, p, rank) ||
+      !flit(st, p, ",\"dev\":") || !fnum(st, p, dev))
+    return false;
+  if (neg ? tsm > (1ull << 63) : tsm >= (1ull << 63)) return false;
+  if (n < 1 || n > 0xFFFF || rank >= n || dev > 0xFFFF) return false;
+  o.r.seq = seq;
+  o.r.nranks = (uint16_t)n;
+  o.r.rank = (uint16_t)rank;
+  o.r.dev = (uint16_t)dev;
+  o.ts = neg ? (int64_t)(0ull - tsm) : (int64_t)tsm;
+  return true;
+}
+
+// the kind-specific tail from p to the end of the line e: count, aux, aux2, kc, ad
+__device__ bool fast_suffix(const uint8_t* st, uint32_t p, uint32_t e, int kind, uint32_t n, uint32_t rank,
+                            ct_record& r) {
+  uint64_t cnt, x;
+  r.aux = 0;
+  r.aux2 = 0;
+  if (kind == CT_KIND_COLLECTIVE) {
+    Str cv, av, dv;
+    if (!flit(st, p, ",\"coll\":\"") || !fstr16(st, p, cv) || !flit(st, p, ",\"algo\":\"") || !fstr16(st, p, av) ||
+        !flit(st, p, ",\"count\":") || !fnum(st, p, cnt) || !flit(st, p, ",\"dtype\":\"") || !fstr16(st, p, dv))
+      return false;
+    const int coll = enum_of(K_COLL, cv), algo = enum_of(K_ALGO, av), dt = enum_of(K_DTYPE, dv);
+    if (coll < 0 || algo < 0 || dt < 0) return false;
+    const bool rooted = coll == CT_COLL_BROADCAST || coll == CT_COLL_REDUCE;
+    if (st[p] == ',') {
+      if (!flit(st, p, ",\"root\":") || !fnum(st, p, x) || !rooted || x >= n) return false;
+      r.aux = (uint16_t)x;
+    } else if (rooted) {
+      return false;
+    }
+    if ((algo == CT_ALGO_TREE || algo == CT_ALGO_COLLNET) && coll != CT_COLL_ALLREDUCE) return false;
+    r.count = cnt;
+    r.kc = (uint8_t)(kind | (coll << 3) | (rooted ? 1 << 6 : 0));
+    r.ad = (uint8_t)(algo | (dt << 2));
+  } else if (kind == CT_KIND_SEND || kind == CT_KIND_RECV) {
+    Str dv;
+    if (!flit(st, p, ",\"peer\":") || !fnum(st, p, x) || !flit(st, p, ",\"count\":") || !fnum(st, p, cnt) ||
+        !flit(st, p, ",\"dtype\":\"") || !fstr16(st, p, dv))
+      return false;
+    const int dt = enum_of(K_DTYPE, dv);
+    if (dt < 0 || x == rank || x >= n) return false;
+    r.aux = (uint16_t)x;
+    r.count = cnt;
+    r.kc = (uint8_t)kind;
+    r.ad = (uint8_t)(dt << 2);
+  } else {
+    Str ckv, sk, dk;
+    uint64_t si, di;
+    if (!flit(st, p, ",\"ckind\":\"") || !fstr16(st, p, ckv) || !flit(st, p, ",\"src\":{\"kind\":\"") ||
+        !fstr16(st, p, sk) || !flit(st, p, ",\"idx\":") || !fnum(st, p, si) ||
+        !flit(st, p, "},\"dst\":{\"kind\":\"") || !fstr16(st, p, dk) || !flit(st, p, ",\"idx\":") ||
+        !fnum(st, p, di) || !flit(st, p, "},\"bytes\":") || !fnum(st, p, cnt))
+      return false;
+    const int ck = enum_of(K_CKIND, ckv);
+    if (ck < 0) return false;
+    const uint32_t s_k = CT_IS(sk, "host") ? 0u : CT_IS(sk, "gpu") ? 1u : 0xFFu;
+    const uint32_t d_k = CT_IS(dk, "host") ? 0u : CT_IS(dk, "gpu") ? 1u : 0xFFu;
+    const uint32_t want_s = ck == CT_CKIND_H2D ? 0 : 1, want_d = ck == CT_CKIND_D2H ? 0 : 1;
+    if (s_k != want_s || d_k != want_d || si > 0xFFFF || di > 0xFFFF) return false;
+    if ((want_s == 0 && si != 0) || (want_d == 0 && di != 0)) return false;
+    if (ck == CT_CKIND_D2D && si == di) return false;
+    r.aux = (uint16_t)si;
+    r.aux2 = (uint16_t)di;
+    r.count = cnt;
+    r.kc = (uint8_t)kind;
+    r.ad = (uint8_t)(ck << 6);
+  }
+  if (!flit(st, p, "}")) return false;
+  return p == e;
+}
+
+__global__ void __launch_bounds__(kFThreads) k_fused(FArgs A) {
+  extern __shared__ __align__(16) uint8_t st[];  // the stage: [st0, t1) and 32 zero-padded bytes
+  __shared__ uint16_t msk[(kFM + kFT) / 16];
+  __shared__ uint16_t tp[kFMaxLines + 1];          // line ends (stage offsets < 2^16)
+  __shared__ uint16_t rl[kFMaxLines];              // record index within the tile (0xFFFF: blank)
+  __shared__ unsigned long long ckey[kFCache];
+  __shared__ unsigned long long cref[kFCache];
+  __shared__ int cslot[kFCache];
+  __shared__ uint32_t cfirst[kFCache];
+  __shared__ uint32_t clen[kFCache];
+  __shared__ __align__(16) uint8_t cname[kFCache][kFNameMax];
+  __shared__ unsigned long long s_t;
+  __shared__ uint32_t s_prev, s_nl, s_abort;
+  using BS = cub::BlockScan<uint32_t, kFThreads>;
+  using BR = cub::BlockReduce<int, kFThreads>;
+  __shared__ union {
+    typename BS::TempStorage scan;
+    typename BR::TempStorage red;
+  } tmp;
+  const int tid = threadIdx.x;
+
+  __shared__ __align__(8) unsigned long long sbar;
+  if (tid == 0) {
+    s_t = atomicAdd(&A.ctl->ticket, 1ull);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&sbar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (tid < kFCache) { ckey[tid] = 0; cslot[tid] = -1; cfirst[tid] = 0xFFFFFFFFu; }
+  __syncthreads();
+  const uint64_t t = s_t;
+  const uint64_t t0 = t * kFT, t1 = min(t0 + kFT, A.size);
+  const uint64_t st0 = t0 > kFM ? t0 - kFM : 0;
+  const uint32_t nst = (uint32_t)(t1 - st0);
+  // the stage: one TMA bulk copy of the 16-byte multiple, the rest (and the zero padding
+  // past the text) by the threads
+#ifndef CT_FSTAGE_TMA
+#define CT_FSTAGE_TMA 1
+#endif
+  const uint32_t nbk = CT_FSTAGE_TMA ? (uint32_t)(min(A.size, st0 + nst + 128) - st0) & ~15u : 0u;
+  if (!CT_FSTAGE_TMA) {
+    for (uint32_t v = tid; v < (nst + 128 + 15) / 16; v += kFThreads) {
+      const uint64_t a = st0 + 16ull * v;
+      if (a + 16 <= A.size) *reinterpret_cast<uint4*>(st + 16 * v) = *reinterpret_cast<const uint4*>(A.s + a);
+      else for (int q = 0; q < 16; q++) st[16 * v + q] = a + q < A.size ? A.s[a + q] : 0;
+    }
+  }
+  if (tid == 0 && nbk) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&sbar)), "r"(nbk)
+                 : "memory");
+    for (uint32_t o = 0; o < nbk; o += 16384)
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              smem_u32(st + o)),
+          "l"(A.s + st0 + o), "r"(min(16384u, nbk - o)), "r"(smem_u32(&sbar))
+          : "memory");
+  }
+  if (CT_FSTAGE_TMA)
+    for (uint32_t q = nbk + tid; q < nst + 128; q += kFThreads) st[q] = st0 + q < A.size ? A.s[st0 + q] : 0;
+  __syncthreads();
+  if (nbk) {
+    uint32_t done = 0;
+    while (!done)
+      asm volatile(
+          "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+          : "=r"(done)
+          : "r"(smem_u32(&sbar))
+          : "memory");
+  }
+
+  // ---- terminator masks (look-behind and owned groups)
+  const uint32_t gb = (uint32_t)(t0 - st0) / 16, ng = (nst + 15) / 16;
+  bool hi = false;
+  for (uint32_t g = tid; g < ng; g += kFThreads) {
+    bool h;
+    msk[g] = (uint16_t)brk16s(st, 16 * g, st0, A.s, A.size, h);
+    hi |= h && g >= gb;
+  }
+  if (__syncthreads_or(hi) && tid == 0) fb(A, FB_NONASCII);
+  // the last terminator before the tile: the first owned line starts after it
+  int last = -1;
+  for (uint32_t g = tid; g < gb; g += kFThreads)
+    if (msk[g]) last = max(last, (int)(16 * g + 31 - __clz((uint32_t)msk[g])));
+  last = BR(tmp.red).Reduce(last, cub::Max());
+  if (tid == 0) {
+    s_abort = 0;
+    if (last >= 0) s_prev = (uint32_t)last + blen_s(st, (uint32_t)last, nst);
+    else if (st0 == 0) s_prev = 0;
+    else { s_prev = 0; s_abort = 1; }  // a line longer than the look-behind
+  }
+  __syncthreads();
+  // ---- owned terminators in text order: 8 contiguous groups per thread
+  uint32_t cnt = 0;
+  const uint32_t g0 = gb + 8 * tid;
+#pragma unroll
+  for (int k = 0; k < 8; k++) cnt += g0 + k < ng ? __popc((uint32_t)msk[g0 + k]) : 0u;
+  uint32_t off, tot;
+  BS(tmp.scan).ExclusiveSum(cnt, off, tot);
+  if (tot > (uint32_t)kFMaxLines) {
+    if (tid == 0) { fb(A, FB_FALLBACK); s_abort = 1; }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      if (g0 + k >= ng) break;
+      uint32_t m = msk[g0 + k];
+      while (m) {
+        const int j = __ffs(m) - 1;
+        m &= m - 1;
+        tp[off++] = (uint16_t)(16 * (g0 + k) + j);
+      }
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    uint32_t L = min(tot, (uint32_t)kFMaxLines);
+    if (t1 == A.size && !s_abort) {  // the final line when the text does not end with a terminator
+      const uint32_t le = L ? tp[L - 1] + blen_s(st, tp[L - 1], nst) : s_prev;
+      if (le < nst && L < (uint32_t)kFMaxLines) tp[L++] = (uint16_t)nst;
+      else if (le < nst) s_abort = 1;
+    }
+    s_nl = L;
+    if (s_abort) fb(A, FB_FALLBACK);
+  }
+  __syncthreads();
+  const uint32_t L = s_nl;
+  const bool abort_ = s_abort != 0;
+  auto lbeg = [&](uint32_t k) -> uint32_t { return k == 0 ? s_prev : tp[k - 1] + blen_s(st, tp[k - 1], nst); };
+
+  // ---- blank test, record index within the tile (rounds of kFThreads lines, text order)
+  uint32_t rbase = 0;
+  for (uint32_t r0 = 0; r0 < L; r0 += kFThreads) {
+    const uint32_t k = r0 + tid;
+    uint32_t nb = 0;
+    if (k < L && !abort_) {
+      const uint32_t b = lbeg(k), e = tp[k];
+      nb = b < e && !byte_blank(st[b]) ? 1u : (line_class(st, b, e, true) != 0 ? 1u : 0u);
+    }
+    uint32_t o, rt;
+    BS(tmp.scan).ExclusiveSum(nb, o, rt);
+    if (k < L) rl[k] = nb ? (uint16_t)(rbase + o) : (uint16_t)0xFFFF;
+    rbase += rt;
+    __syncthreads();
+  }
+  const uint32_t R = rbase;
+  // per-tile counts; the tile's records go to its own block of kFMaxRecs temporary slots
+  // (k_fscan / k_fcompact place them), so no tile waits for another
+  if (tid == 0) {
+    A.tcnt[2 * t] = L;
+    A.tcnt[2 * t + 1] = R;
+    if (R > (uint32_t)kFMaxRecs) { fb(A, FB_FALLBACK); s_abort = 1; }
+  }
+  __syncthreads();
+  if (s_abort) return;
+
+  // ---- parse: canonical lines here, the rest onto the slow list.  Per round of
+  // kFThreads lines: the common head (thread = line), the name through the cache, then
+  // the kind-specific tail with the lines regrouped by kind so that warps stay uniform.
+  // The mask array is free now: per-line state between the two halves lives there.
+  uint16_t* s_p = reinterpret_cast<uint16_t*>(msk);   // tail start
+  uint16_t* s_n = s_p + kFThreads;                     // nranks, rank, dev, comm slot
+  uint16_t* s_rank = s_n + kFThreads;
+  uint16_t* s_dev = s_rank + kFThreads;
+  uint16_t* s_cs = s_dev + kFThreads;
+  uint8_t* s_kind = reinterpret_cast<uint8_t*>(s_cs + kFThreads);
+  uint8_t* s_ce = s_kind + kFThreads;
+  uint8_t* s_ord = s_ce + kFThreads;                   // regrouped position -> line of the round
+  static_assert(kFThreads * 13 <= (int)sizeof(msk), "per-line state must fit the mask array");
+  __shared__ uint32_t s_wcnt[3][kFThreads / 32];
+  const int warp = tid >> 5, lane = tid & 31;
+  for (uint32_t r0 = 0; r0 < L; r0 += kFThreads) {
+    const uint32_t k = r0 + tid;
+    FLine o;
+    int kind = -1;
+    bool ok = false;
+    int ce = -1;       // cache entry
+    bool mine = false; // this thread inserted the entry
+    uint32_t p = 0;
+    const bool line_here = k < L && rl[k] != 0xFFFF;
+    if (line_here) {
+      p = lbeg(k);
+      ok = fast_prefix(st, p, o, kind);
+      if (ok) {  // cache entry of the name (inserted by the first thread to see it)
+        uint32_t i = (uint32_t)o.key & (kFCache - 1);
+        for (int probe = 0; probe < kFCache; probe++, i = (i + 1) & (kFCache - 1)) {
+          const unsigned long long old = atomicCAS(&ckey[i], 0ull, (unsigned long long)o.key);
+          if (old == 0) { ce = (int)i; mine = true; break; }
+          if (old == o.key) { ce = (int)i; break; }
+        }
+        if (ce < 0) ok = false;  // cache full: the slow list interns it
+      }
+    }
+    __syncthreads();
+    if (mine) {
+      clen[ce] = o.nlen;
+#pragma unroll
+      for (int w = 0; w < (int)kFNameMax / 8; w++) {
+        const uint32_t q = 8 * w;
+        const uint64_t x = q < o.nlen ? st8(st, o.nb + q) : 0ull;
+        const uint64_t mk = q + 8 <= o.nlen ? ~0ull : (q < o.nlen ? (1ull << (8 * (o.nlen - q))) - 1 : 0ull);
+        *reinterpret_cast<uint64_t*>(&cname[ce][q]) = x & mk;
+      }
+      const uint64_t ref = (st0 + o.nb) | ((uint64_t)o.nlen << 40);
+      cref[ce] = ref;
+      cslot[ce] = table_slot(A, o.key, ref);
+    }
+    __syncthreads();
+    if (ok) {  // the name must equal the entry's (a 64-bit key collision fails the load)
+      bool same = clen[ce] == o.nlen && cslot[ce] >= 0;
+#pragma unroll
+      for (int w = 0; w < (int)kFNameMax / 8; w++) {
+        const uint32_t q = 8 * w;
+        const uint64_t x = q < o.nlen ? st8(st, o.nb + q) : 0ull;
+        const uint64_t mk = q + 8 <= o.nlen ? ~0ull : (q < o.nlen ? (1ull << (8 * (o.nlen - q))) - 1 : 0ull);
+        same = same && *reinterpret_cast<const uint64_t*>(&cname[ce][q]) == (x & mk);
+      }
+      if (!same) {
+        if (cslot[ce] >= 0) fb(A, FB_COLLIDE);
+        ok = false;
+      }
+    }
+    if (line_here) {
+      if (ok) {  // the head's fields; the tail comes below
+        const uint64_t slot = t * kFMaxRecs + rl[k];
+        reinterpret_cast<unsigned long long*>(A.trec + slot)[1] = o.r.seq;
+        A.tts[slot] = o.ts;
+        s_p[tid] = (uint16_t)p;
+        s_n[tid] = o.r.nranks;
+        s_rank[tid] = o.r.rank;
+        s_dev[tid] = o.r.dev;
+        s_cs[tid] = (uint16_t)cslot[ce];
+        s_kind[tid] = (uint8_t)kind;
+        s_ce[tid] = (uint8_t)ce;
+      } else {  // (tile, line in tile, record in tile), byte range
+        list_put(A, &A.ctl->n_slow, A.slow, 4, t << 32 | (uint64_t)k << 16 | rl[k], 0, st0 + lbeg(k), st0 + tp[k]);
+      }
+    }
+    // regroup the lines with a valid head by kind class (collective, send/recv, copy)
+    const int cls = ok ? (kind == CT_KIND_COLLECTIVE ? 0 : (kind <= CT_KIND_RECV ? 1 : 2)) : 3;
+    unsigned bm[3];
+#pragma unroll
+    for (int c = 0; c < 3; c++) {
+      bm[c] = __ballot_sync(0xFFFFFFFFu, cls == c);
+      if (lane == 0) s_wcnt[c][warp] = __popc(bm[c]);
+    }
+    __syncthreads();
+    uint32_t nsorted = 0, pos = 0;
+#pragma unroll
+    for (int c = 0; c < 3; c++)
+      for (int w = 0; w < kFThreads / 32; w++) {
+        const uint32_t v = s_wcnt[c][w];
+        if (c < cls || (c == cls && w < warp)) pos += v;
+        nsorted += v;
+      }
+    if (cls < 3) s_ord[pos + __popc(bm[cls] & ((1u << lane) - 1))] = (uint8_t)tid;
+    __syncthreads();
+    if ((uint32_t)tid < nsorted) {
+      const uint32_t i = s_ord[tid], kk = r0 + i;
+      ct_record rec;
+      const int kd = s_kind[i];
+      if (fast_suffix(st, s_p[i], tp[kk], kd, s_n[i], s_rank[i], rec)) {
+        const uint64_t slot = t * kFMaxRecs + rl[kk];
+        atomicMin(&cfirst[s_ce[i]], (uint32_t)rl[kk]);
+        reinterpret_cast<unsigned long long*>(A.trec + slot)[0] = rec.count;
+        uint4 w;
+        w.x = s_cs[i];
+        w.y = (uint32_t)s_n[i] | ((uint32_t)s_rank[i] << 16);
+        w.z = (uint32_t)s_dev[i] | ((uint32_t)rec.aux << 16);
+        w.w = (uint32_t)rec.aux2 | ((uint32_t)rec.kc << 16) | ((uint32_t)rec.ad << 24);
+        reinterpret_cast<uint4*>(A.trec + slot)[1] = w;
+      } else {
+        list_put(A, &A.ctl->n_slow, A.slow, 4, t << 32 | (uint64_t)kk << 16 | rl[kk], 0, st0 + lbeg(kk), st0 + tp[kk]);
+      }
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  if (tid < kFCache && ckey[tid] && cslot[tid] >= 0 && cfirst[tid] != 0xFFFFFFFFu) {
+    atomicMin(&A.gfirst[cslot[tid]], t << 16 | cfirst[tid]);  // (tile, record in tile): text order
+    list_put(A, &A.ctl->n_verify, A.verify, 2, (uint64_t)cslot[tid], cref[tid], 0, 0);
+  }
+}
+
+// tiles in text order: first line number and first record slot of every tile
+constexpr int kScanThreads = 512;
+__global__ void __launch_bounds__(kScanThreads) k_fscan(FArgs A) {
+  constexpr int kI = 8;
+  using Scan = cub::BlockScan<unsigned long long, kScanThreads>;
+  __shared__ typename Scan::TempStorage tmp;
+  if (A.ctl->flags & FB_FALLBACK) return;
+  unsigned long long bl = 0, br = 0;
+  for (uint64_t c0 = 0; c0 < A.ntiles; c0 += kScanThreads * kI) {
+    const uint64_t t0 = c0 + (uint64_t)threadIdx.x * kI;
+    unsigned long long l[kI], r[kI], ol[kI], orr[kI], sl, sr;
+#pragma unroll
+    for (int q = 0; q < kI; q++) {
+      const bool in = t0 + q < A.ntiles;
+      const uint2 c = in ? reinterpret_cast<const uint2*>(A.tcnt)[t0 + q] : make_uint2(0, 0);
+      l[q] = c.x;
+      r[q] = c.y;
+    }
+    Scan(tmp).ExclusiveSum(l, ol, sl);
+    __syncthreads();
+    Scan(tmp).ExclusiveSum(r, orr, sr);
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < kI; q++)
+      if (t0 + q < A.ntiles) reinterpret_cast<ulonglong2*>(A.toff)[t0 + q] = make_ulonglong2(bl + ol[q], br + orr[q]);
+    bl += sl;
+    br += sr;
+  }
+  if (threadIdx.x == 0) {
+    A.ctl->n_lines = bl;
+    A.ctl->n_recs = br;
+    if (br > A.cap) fb(A, FB_FALLBACK);
+  }
+}
+
+// slow list: the generic parser (escapes decoded) straight from the text, into the
+// tile's temporary slot
+__global__ void __launch_bounds__(kParseThreads) k_fslow(FArgs A, bool aligned) {
+  __shared__ uint64_t fields[K_N * kParseThreads];
+  if (A.ctl->flags & FB_FALLBACK) return;
+  const uint64_t n = min(*reinterpret_cast<volatile unsigned long long*>(&A.ctl->n_slow), (unsigned long long)A.lcap);
+  const uint64_t wl = aligned && A.size > 32 ? A.size - 8 : 0;
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t w0 = A.slow[4 * j], b = A.slow[4 * j + 2], e = A.slow[4 * j + 3];
+    const uint64_t tt = w0 >> 32, k = (w0 >> 16) & 0xFFFF, lr = w0 & 0xFFFF;
+    const uint64_t tmp_slot = tt * kFMaxRecs + lr;
+    LineOut o;
+    const uint8_t st = parse_line<true>(A.s, b, e, aligned, wl, fields + threadIdx.x, kParseThreads, A.side, o);
+    if (st == L_OK) {
+      const uint32_t len = (uint32_t)(o.comm >> 40);
+      const uint64_t key = name_key_bytes(name_ptr(A.s, A.side.buf, o.comm), len);
+      const int gs = table_slot(A, key, o.comm);
+      if (gs >= 0) {
+        atomicMin(&A.gfirst[gs], (unsigned long long)(tt << 16 | lr));
+        list_put(A, &A.ctl->n_verify, A.verify, 2, (uint64_t)gs, o.comm, 0, 0);
+      }
+      o.r.comm = gs >= 0 ? (uint32_t)gs : 0u;
+      A.trec[tmp_slot] = o.r;
+      A.tts[tmp_slot] = o.ts;
+    } else {  // the caller reads it (a blank one is dropped there)
+      A.trec[tmp_slot] = ct_record{};
+      A.tts[tmp_slot] = 0;
+      list_put(A, &A.ctl->n_defer, A.defer, 4, A.toff[2 * tt] + k + 1, A.toff[2 * tt + 1] + lr, b, e - b);
+    }
+  }
+}
+
+// every (table slot, name) pair seen: byte-equal to the slot's name
+__global__ void k_fverify(FArgs A) {
+  const uint64_t n = min(*reinterpret_cast<volatile unsigned long long*>(&A.ctl->n_verify), (unsigned long long)A.lcap);
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t gs = A.verify[2 * j], a = A.verify[2 * j + 1], h = A.gname[gs];
+    if (a == h) continue;
+    const uint32_t la = (uint32_t)(a >> 40), lh = (uint32_t)(h >> 40);
+    bool same = la == lh;
+    const uint8_t *na = name_ptr(A.s, A.side.buf, a), *nh = name_ptr(A.s, A.side.buf, h);
+    for (uint32_t q = 0; same && q < la; q++) same = na[q] == nh[q];
+    if (!same) fb(A, FB_COLLIDE);
+  }
+}
+
+// one CTA: table slots in first-seen order -> comm ids, comm rows and names
+constexpr int kFinThreads = 1024;
+__global__ void __launch_bounds__(kFinThreads) k_ffinal(FArgs A) {
+  using Scan = cub::BlockScan<unsigned long long, kFinThreads>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ unsigned long long ufirst[kFMaxNames];
+  __shared__ uint32_t uslot[kFMaxNames];
+  __shared__ uint32_t uorder[kFMaxNames];  // rank -> entry
+  __shared__ unsigned int n_used;
+  const int tid = threadIdx.x;
+  if (tid == 0) n_used = 0;
+  __syncthreads();
+  if (A.ctl->flags & FB_FALLBACK) return;
+  for (uint32_t i = tid; i < kFTable; i += kFinThreads) {
+    // a name whose lines all left the template path and were deferred has no first record
+    if (A.gkey[i] == 0 || A.gfirst[i] == ~0ull) continue;
+    const unsigned int u = atomicAdd(&n_used, 1u);
+    if (u < kFMaxNames) { ufirst[u] = A.gfirst[i]; uslot[u] = i; }
+  }
+  __syncthreads();
+  const uint32_t nu = n_used;
+  if (nu > kFMaxNames) {
+    if (tid == 0) fb(A, FB_FALLBACK);
+    return;
+  }
+  // first-seen order: the rank of each (tile, record in tile) key among the (distinct) keys
+  for (uint32_t i = tid; i < nu; i += kFinThreads) {
+    const unsigned long long k = ufirst[i];
+    uint32_t r = 0;
+    for (uint32_t q = 0; q < nu; q++) r += ufirst[q] < k ? 1u : 0u;
+    uorder[r] = i;
+  }
+  __syncthreads();
+  constexpr int kI = kFMaxNames / kFinThreads;
+  unsigned long long len[kI], off[kI];
+#pragma unroll
+  for (int q = 0; q < kI; q++) {
+    const uint32_t r = kI * tid + q;
+    len[q] = r < nu ? (A.gname[uslot[uorder[r]]] >> 40) : 0ull;
+  }
+  unsigned long long tot;
+  Scan(tmp).ExclusiveSum(len, off, tot);
+  if (tid == 0) { A.ctl->name_bytes = tot; A.ctl->n_used = nu; }
+  if (tot > kFNameCap) {
+    if (tid == 0) fb(A, FB_FALLBACK);
+    return;
+  }
+#pragma unroll
+  for (int q = 0; q < kI; q++) {
+    const uint32_t r = kI * tid + q;
+    if (r >= nu) continue;
+    const uint32_t e = uorder[r], gs = uslot[e];
+    const unsigned long long k = ufirst[e];
+    A.gid[gs] = r;
+    A.comm_rows[3 * r] = A.toff[2 * (k >> 16) + 1] + (k & 0xFFFF);
+    A.comm_rows[3 * r + 1] = off[q];
+    A.comm_rows[3 * r + 2] = len[q];
+    const uint8_t* nm = name_ptr(A.s, A.side.buf, A.gname[gs]);
+    for (uint64_t b = 0; b < len[q]; b++) A.names[off[q] + b] = nm[b];
+  }
+}
+
+// tiles' temporary records -> final positions, comm field: table slot -> comm id
+__global__ void __launch_bounds__(256) k_fcompact(FArgs A) {
+  if (A.ctl->flags & FB_FALLBACK) return;
+  for (uint64_t tt = blockIdx.x; tt < A.ntiles; tt += gridDim.x) {
+    const uint32_t R = A.tcnt[2 * tt + 1];
+    const uint64_t dst = A.toff[2 * tt + 1], src = tt * kFMaxRecs;
+    for (uint32_t i = threadIdx.x; i < R; i += blockDim.x) {
+      ct_record r = A.trec[src + i];
+      r.comm = A.gid[r.comm & (kFTable - 1)];
+      A.recs[dst + i] = r;
+      A.ts[dst + i] = A.tts[src + i];
+    }
+  }
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------- handle + C ABI
@@ -1169,6 +1963,110 @@ int grid_for(uint64_t n, int threads = 256) {
   return (int)(g < 1 ? 1 : g > 148 * 32 ? 148 * 32 : g);
 }
 
+// The fused single pass (k_fused + slow list + name table finalisation): 0 done, 1 the
+// text needs the multi-pass pipeline, else an error status.
+int run_fused(ct_jsonl* j, const uint8_t* s, uint64_t size, Pool& pool, cudaEvent_t done) {
+  const uint64_t ntiles = (size + kFT - 1) / kFT;
+  // record slots: a valid trace line is > 90 bytes; texts whose non-blank lines average
+  // fewer than 64 bytes overflow and take the multi-pass pipeline
+  const uint64_t cap = size / 64 + 64;
+  if (cap >= (1ull << 32)) return 1;
+  FArgs A{};
+  A.s = s;
+  A.size = size;
+  A.ntiles = ntiles;
+  A.cap = cap;
+  A.lcap = std::min<uint64_t>(cap, kFListCap);
+  A.ctl = pool.alloc<FCtl>(1);
+  A.tcnt = pool.alloc<uint32_t>(2 * ntiles);
+  A.toff = pool.alloc<unsigned long long>(2 * ntiles);
+  A.trec = pool.alloc<ct_record>(ntiles * kFMaxRecs);
+  A.tts = pool.alloc<int64_t>(ntiles * kFMaxRecs);
+  A.recs = pool.alloc<ct_record>(cap);
+  A.ts = pool.alloc<int64_t>(cap);
+  A.gkey = pool.alloc<unsigned long long>(kFTable);
+  A.gname = pool.alloc<unsigned long long>(kFTable);
+  A.gfirst = pool.alloc<unsigned long long>(kFTable);
+  A.gid = pool.alloc<uint32_t>(kFTable);
+  A.slow = pool.alloc<uint64_t>(4 * A.lcap);
+  A.defer = pool.alloc<uint64_t>(4 * A.lcap);
+  A.verify = pool.alloc<uint64_t>(2 * A.lcap);
+  A.comm_rows = pool.alloc<uint64_t>(3 * kFMaxNames);
+  A.names = pool.alloc<uint8_t>(kFNameCap);
+  const uint64_t side_cap = std::min<uint64_t>(16ull << 20, std::max<uint64_t>(size, 1024));
+  uint8_t* side = pool.alloc<uint8_t>(side_cap);
+  unsigned long long* side_used = pool.alloc<unsigned long long>(1);
+  JL_NN(A.ctl); JL_NN(A.tcnt); JL_NN(A.toff); JL_NN(A.trec); JL_NN(A.tts); JL_NN(A.recs); JL_NN(A.ts); JL_NN(A.gkey); JL_NN(A.gname);
+  JL_NN(A.gfirst); JL_NN(A.gid); JL_NN(A.slow); JL_NN(A.defer); JL_NN(A.verify); JL_NN(A.comm_rows);
+  JL_NN(A.names); JL_NN(side); JL_NN(side_used);
+  A.side = Side{side, side_used, side_cap};
+  JL_TRY(cudaMemsetAsync(A.ctl, 0, sizeof(FCtl), j->st));
+  JL_TRY(cudaMemsetAsync(A.gkey, 0, kFTable * sizeof(unsigned long long), j->st));
+  JL_TRY(cudaMemsetAsync(A.gfirst, 0xFF, kFTable * sizeof(unsigned long long), j->st));
+  JL_TRY(cudaMemsetAsync(side_used, 0, sizeof(unsigned long long), j->st));
+  static bool attr_set = false;
+  if (!attr_set) {
+    JL_TRY(cudaFuncSetAttribute(k_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFStage));
+    attr_set = true;
+  }
+  const bool dbg = getenv("CT_JSONL_DEBUG") != nullptr;
+  cudaEvent_t ev[6];
+  if (dbg)
+    for (auto& x : ev) cudaEventCreate(&x);
+  if (dbg) cudaEventRecord(ev[0], j->st);
+  k_fused<<<(unsigned)ntiles, kFThreads, kFStage, j->st>>>(A);
+  k_fscan<<<1, kScanThreads, 0, j->st>>>(A);
+  if (dbg) cudaEventRecord(ev[1], j->st);
+  k_fslow<<<148 * 4, kParseThreads, 0, j->st>>>(A, true);
+  if (dbg) cudaEventRecord(ev[2], j->st);
+  k_fverify<<<148, 256, 0, j->st>>>(A);
+  if (dbg) cudaEventRecord(ev[3], j->st);
+  k_ffinal<<<1, kFinThreads, 0, j->st>>>(A);
+  if (dbg) cudaEventRecord(ev[4], j->st);
+  k_fcompact<<<(unsigned)std::min<uint64_t>(ntiles, 148 * 16), 256, 0, j->st>>>(A);
+  if (dbg) cudaEventRecord(ev[5], j->st);
+  JL_TRY(cudaGetLastError());
+  JL_TRY(cudaEventRecord(done, j->st));  // end of the device work (the status read below is host I/O)
+  if (dbg) {
+    cudaEventSynchronize(ev[5]);
+    float f[5];
+    for (int q = 0; q < 5; q++) cudaEventElapsedTime(&f[q], ev[q], ev[q + 1]);
+    fprintf(stderr, "ct_jsonl fused ms: fused+scan %.3f slow %.3f verify %.3f final %.3f compact %.3f\n", f[0], f[1], f[2],
+            f[3], f[4]);
+    for (auto& x : ev) cudaEventDestroy(x);
+  }
+  FCtl c{};
+  JL_TRY(cudaMemcpyAsync(&c, A.ctl, sizeof(FCtl), cudaMemcpyDeviceToHost, j->st));
+  JL_TRY(cudaStreamSynchronize(j->st));
+  if (c.flags & FB_FALLBACK) return 1;
+  if (c.flags & FB_COLLIDE) {
+    j->err = "comm name hash collision (64-bit name key): two different names share a key";
+    return CT_ERR_CAPACITY;
+  }
+  if (c.n_recs >= (1ull << 32)) { j->err = "more than 2^32 - 1 records in one text"; return CT_ERR_CAPACITY; }
+  j->info.n_lines = c.n_lines;
+  j->info.n_records = c.n_recs;
+  j->info.n_deferred = c.n_defer;
+  j->info.n_comms = c.n_used;
+  j->info.comm_bytes = c.name_bytes;
+  j->info.non_ascii = (c.flags & FB_NONASCII) ? 1 : 0;
+  j->info.n_slow = c.n_slow;
+  if (getenv("CT_JSONL_DEBUG") && c.n_slow) {  // the first slow lines (1-based numbers) on stderr
+    uint64_t rows[4 * 8];
+    const uint64_t k = std::min<uint64_t>(c.n_slow, 8);
+    JL_TRY(cudaMemcpy(rows, A.slow, 4 * k * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    for (uint64_t i = 0; i < k; i++)
+      fprintf(stderr, "ct_jsonl slow line %llu (bytes %llu..%llu)\n", (unsigned long long)rows[4 * i],
+              (unsigned long long)rows[4 * i + 2], (unsigned long long)rows[4 * i + 3]);
+  }
+  j->recs = A.recs;
+  j->ts = A.ts;
+  j->deferred_rows = A.defer;
+  j->comm_rows = A.comm_rows;
+  j->names = A.names;
+  return 0;
+}
+
 int run(ct_jsonl* j, const uint8_t* text, uint64_t size, int on_device) {
   Pool pool{j};
   cudaEvent_t e0, e1;
@@ -1182,6 +2080,25 @@ int run(ct_jsonl* j, const uint8_t* text, uint64_t size, int on_device) {
     s = d;
   }
   JL_TRY(cudaEventRecord(e0, j->st));
+  if (getenv("CT_JSONL_DEBUG")) {
+    cudaEventSynchronize(e0);
+    fprintf(stderr, "ct_jsonl: text on the device\n");
+  }
+  const bool multipass = getenv("CT_JSONL_MULTIPASS") != nullptr;  // A/B and tests
+  if (size > 0 && (reinterpret_cast<uintptr_t>(s) & 15) == 0 && !multipass) {
+    const int rc = run_fused(j, s, size, pool, e1);
+    if (rc != 1) {
+      JL_TRY(cudaEventSynchronize(e1));
+      float ms = 0;
+      JL_TRY(cudaEventElapsedTime(&ms, e0, e1));
+      j->info.ms_device = ms;
+      j->info.fused = 1;
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+      return rc;
+    }
+    j->info = ct_jsonl_info{};  // the multi-pass pipeline from the start
+  }
   uint64_t* scal = pool.alloc<uint64_t>(8);  // device scalars
   JL_NN(scal);
   JL_TRY(cudaMemsetAsync(scal, 0, 8 * sizeof(uint64_t), j->st));
@@ -1400,6 +2317,13 @@ int ct_jsonl_parse(int device, const char* text, uint64_t size, int on_device, c
   if (!text && size) { j->err = "null text"; return CT_ERR_ARGUMENT; }
   if (size >= (1ull << 39)) { j->err = "text larger than 2^39 bytes"; return CT_ERR_ARGUMENT; }
   cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) {  // keep freed blocks in the stream-ordered pool between calls
+    cudaMemPool_t mp;
+    if (cudaDeviceGetDefaultMemPool(&mp, device) == cudaSuccess) {
+      uint64_t keep = ~0ull;
+      cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  }
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&j->st, cudaStreamNonBlocking);
   if (e != cudaSuccess) { j->err = cudaGetErrorString(e); return CT_ERR_CUDA; }
   const int rc = run(j, reinterpret_cast<const uint8_t*>(text), size, on_device);
@@ -1426,6 +2350,12 @@ int ct_jsonl_deferred(ct_jsonl* j, uint64_t* rows) {
   if (n) e = cudaMemcpyAsync(rows, j->deferred_rows, 4 * n * sizeof(uint64_t), cudaMemcpyDeviceToHost, j->st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(j->st);
   if (e != cudaSuccess) { j->err = cudaGetErrorString(e); return CT_ERR_CUDA; }
+  if (j->info.fused && n > 1) {  // appended in completion order: line order for the caller
+    std::vector<std::array<uint64_t, 4>> v(n);
+    memcpy(v.data(), rows, 4 * n * sizeof(uint64_t));
+    std::sort(v.begin(), v.end(), [](const auto& a, const auto& b) { return a[0] < b[0]; });
+    memcpy(rows, v.data(), 4 * n * sizeof(uint64_t));
+  }
   return CT_OK;
 }
 

@@ -100,7 +100,8 @@ def load_trace(source, device: int | None = None) -> PackedTrace:
         # raw UTF-8 or decoded escapes (lone surrogates as in "surrogatepass")
         comm_first[name_bytes[off:off + ln].decode("utf-8", "surrogatepass")] = (first, cid)
     load_info = {"lines": int(info.n_lines), "deferred": nd, "device_comms": nc,
-                 "ms_device": float(info.ms_device)}
+                 "ms_device": float(info.ms_device), "fused": bool(info.fused),
+                 "slow": int(info.n_slow)}
     if nd == 0:
         names_out = [None] * nc
         for name, (_, cid) in comm_first.items():

@@ -48,3 +48,14 @@ def has_gpu():
         return torch.cuda.is_available()
     except Exception:
         return False
+
+
+@pytest.fixture(params=["fused", "multipass"])
+def loader_pipeline(request, monkeypatch):
+    """Run a loader test through the single-pass loader and through the multi-pass one
+    (CT_JSONL_MULTIPASS, read by ct_jsonl_parse on every call)."""
+    if request.param == "multipass":
+        monkeypatch.setenv("CT_JSONL_MULTIPASS", "1")
+    else:
+        monkeypatch.delenv("CT_JSONL_MULTIPASS", raising=False)
+    return request.param

@@ -21,7 +21,7 @@ from paper_2110_10401_b200.matrix import analyze_events, analyze_packed
 from paper_2110_10401_b200.packed import PackedTrace, RECORD_DTYPE, pack_events, unpack
 from paper_2110_10401_b200.events import write_trace
 
-pytestmark = pytest.mark.gpu
+pytestmark = [pytest.mark.gpu, pytest.mark.usefixtures("loader_pipeline")]
 
 
 def reference(text):

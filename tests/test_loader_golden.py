@@ -86,7 +86,7 @@ def test_host_mirror_matches_reference(fuzz_golden):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("group", ["multi", "single", "device", "escape"])
-def test_device_loader_matches_reference(fuzz_golden, group):
+def test_device_loader_matches_reference(fuzz_golden, group, loader_pipeline):
     from paper_2110_10401_b200.loader import load_trace
 
     seen = {"ok": 0, "err": 0}
@@ -100,7 +100,7 @@ def test_device_loader_matches_reference(fuzz_golden, group):
 
 
 @pytest.mark.gpu
-def test_device_resident_text_matches_reference(fuzz_golden):
+def test_device_resident_text_matches_reference(fuzz_golden, loader_pipeline):
     """Text already in HBM (on_device=1), aligned and at odd offsets (unstaged path)."""
     import torch
 
@@ -118,7 +118,7 @@ def test_device_resident_text_matches_reference(fuzz_golden):
 
 
 @pytest.mark.gpu
-def test_escapes_and_non_ascii_parse_on_device():
+def test_escapes_and_non_ascii_parse_on_device(loader_pipeline):
     """Raw UTF-8 names and \\uXXXX / \\" escapes (the reference's own write_trace escapes
     every non-ASCII name) are decoded on the device: nothing is left to the host reader,
     and one name written both ways is one communicator."""

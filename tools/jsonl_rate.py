@@ -37,6 +37,7 @@ ms = tr.load_info["ms_device"]
 assert len(tr) == n and tr.load_info["deferred"] == 0
 assert tr.records[:blk].cpu().numpy().tobytes() == ref.records.tobytes()
 print(f"text {len(text) / 1e9:.3f} GB, {n / 1e6:.1f} M records ({len(text) / n:.0f} B/record)")
+print("load_info", {k: v for k, v in tr.load_info.items()})
 print(f"device parse {ms:.2f} ms -> {n / ms / 1e6:.2f} G rec/s, {len(text) / ms / 1e6:.1f} GB/s of JSONL")
 print(f"load_trace end to end (host bytes -> HBM records) {t_e2e * 1e3:.1f} ms -> {n / t_e2e / 1e6:.1f} M rec/s")
 print(f"host reader parse_trace+pack_events on {blk} records: {blk / t_host / 1e3:.1f} K rec/s (1 core)")
