@@ -29,6 +29,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/commtrace_b200.h"
@@ -1166,6 +1167,8 @@ struct FCtl {
   unsigned int pad;
 };
 
+static_assert(sizeof(FCtl) % 8 == 0, "k_finit clears FCtl as 64-bit words");
+
 struct FArgs {
   const uint8_t* s;
   uint64_t size, ntiles, cap;
@@ -1275,6 +1278,23 @@ __device__ uint32_t brk16s(const uint8_t* st, uint32_t q, uint64_t st0, const ui
     if (brk) m |= 1u << j;
   }
   non_ascii = hi;
+  return m;
+}
+
+// brk16s for the common group: its only byte below 0x20 is '\n' (not after a '\r') and
+// none is >= 0x80 -- branch-free; ``rare`` asks for brk16s otherwise
+__device__ __forceinline__ uint32_t brk16f(const uint8_t* st, uint32_t q, uint64_t st0, uint64_t size, bool& rare) {
+  const uint4 v = *reinterpret_cast<const uint4*>(st + q);
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+  uint32_t m = 0, odd = 0;
+#pragma unroll
+  for (int k = 0; k < 4; k++) {
+    const uint32_t x = w[k] ^ 0x0A0A0A0Au;
+    const uint32_t z = ~(((x & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | x | 0x7F7F7F7Fu);  // exact: byte == '\n'
+    odd |= ((((w[k] - 0x20202020u) & ~w[k]) | w[k]) & 0x80808080u) & ~z;      // other control / non-ASCII
+    m |= (((z >> 7) * 0x01020408u) >> 24) << (4 * k);
+  }
+  rare = odd != 0 || st0 + q + 16 > size || ((m & 1u) && (q == 0 || st[q - 1] == '\r'));
   return m;
 }
 
@@ -1547,24 +1567,36 @@ __global__ void __launch_bounds__(kFThreads) k_fused(FArgs A) {
   // ---- terminator masks (look-behind and owned groups)
   const uint32_t gb = (uint32_t)(t0 - st0) / 16, ng = (nst + 15) / 16;
   bool hi = false;
-  for (uint32_t g = tid; g < ng; g += kFThreads) {
-    bool h;
-    msk[g] = (uint16_t)brk16s(st, 16 * g, st0, A.s, A.size, h);
-    hi |= h && g >= gb;
+  for (uint32_t g = gb + tid; g < ng; g += kFThreads) {  // owned groups
+    bool rare, h = false;
+    uint32_t m = brk16f(st, 16 * g, st0, A.size, rare);
+    if (rare) m = brk16s(st, 16 * g, st0, A.s, A.size, h);
+    msk[g] = (uint16_t)m;
+    hi |= h;
+  }
+  // the last terminator before the tile (the first owned line starts after it): warp 0
+  // walks the look-behind back from the tile, 32 groups per step
+  if (tid < 32) {
+    int last = -1;
+    for (int top = (int)gb - 1; top >= 0 && last < 0; top -= 32) {
+      const int g = top - tid;
+      uint32_t m = 0;
+      if (g >= 0) {
+        bool rare, h;
+        m = brk16f(st, 16 * g, st0, A.size, rare);
+        if (rare) m = brk16s(st, 16 * g, st0, A.s, A.size, h);
+      }
+      const int cand = m ? 16 * g + 31 - __clz(m) : -1;
+      last = __reduce_max_sync(0xFFFFFFFFu, cand);
+    }
+    if (tid == 0) {
+      s_abort = 0;
+      if (last >= 0) s_prev = (uint32_t)last + blen_s(st, (uint32_t)last, nst);
+      else if (st0 == 0) s_prev = 0;
+      else { s_prev = 0; s_abort = 1; }  // a line longer than the look-behind
+    }
   }
   if (__syncthreads_or(hi) && tid == 0) fb(A, FB_NONASCII);
-  // the last terminator before the tile: the first owned line starts after it
-  int last = -1;
-  for (uint32_t g = tid; g < gb; g += kFThreads)
-    if (msk[g]) last = max(last, (int)(16 * g + 31 - __clz((uint32_t)msk[g])));
-  last = BR(tmp.red).Reduce(last, cub::Max());
-  if (tid == 0) {
-    s_abort = 0;
-    if (last >= 0) s_prev = (uint32_t)last + blen_s(st, (uint32_t)last, nst);
-    else if (st0 == 0) s_prev = 0;
-    else { s_prev = 0; s_abort = 1; }  // a line longer than the look-behind
-  }
-  __syncthreads();
   // ---- owned terminators in text order: 8 contiguous groups per thread
   uint32_t cnt = 0;
   const uint32_t g0 = gb + 8 * tid;
@@ -1791,6 +1823,17 @@ __global__ void __launch_bounds__(kScanThreads) k_fscan(FArgs A) {
   }
 }
 
+// per-call state: control block, name table (keys 0, first records ~0), side buffer use
+__global__ void k_finit(FArgs A) {
+  const uint32_t i0 = blockIdx.x * blockDim.x + threadIdx.x;
+  for (uint32_t i = i0; i < kFTable; i += gridDim.x * blockDim.x) {
+    A.gkey[i] = 0;
+    A.gfirst[i] = ~0ull;
+  }
+  if (i0 < sizeof(FCtl) / sizeof(unsigned long long)) reinterpret_cast<unsigned long long*>(A.ctl)[i0] = 0;
+  if (i0 == 0) *A.side.used = 0;
+}
+
 // slow list: the generic parser (escapes decoded) straight from the text, into the
 // tile's temporary slot
 __global__ void __launch_bounds__(kParseThreads) k_fslow(FArgs A, bool aligned) {
@@ -1977,33 +2020,44 @@ int run_fused(ct_jsonl* j, const uint8_t* s, uint64_t size, Pool& pool, cudaEven
   A.ntiles = ntiles;
   A.cap = cap;
   A.lcap = std::min<uint64_t>(cap, kFListCap);
-  A.ctl = pool.alloc<FCtl>(1);
-  A.tcnt = pool.alloc<uint32_t>(2 * ntiles);
-  A.toff = pool.alloc<unsigned long long>(2 * ntiles);
-  A.trec = pool.alloc<ct_record>(ntiles * kFMaxRecs);
-  A.tts = pool.alloc<int64_t>(ntiles * kFMaxRecs);
-  A.recs = pool.alloc<ct_record>(cap);
-  A.ts = pool.alloc<int64_t>(cap);
-  A.gkey = pool.alloc<unsigned long long>(kFTable);
-  A.gname = pool.alloc<unsigned long long>(kFTable);
-  A.gfirst = pool.alloc<unsigned long long>(kFTable);
-  A.gid = pool.alloc<uint32_t>(kFTable);
-  A.slow = pool.alloc<uint64_t>(4 * A.lcap);
-  A.defer = pool.alloc<uint64_t>(4 * A.lcap);
-  A.verify = pool.alloc<uint64_t>(2 * A.lcap);
-  A.comm_rows = pool.alloc<uint64_t>(3 * kFMaxNames);
-  A.names = pool.alloc<uint8_t>(kFNameCap);
+  // one stream-ordered allocation carved into every array (a single pool call per text)
   const uint64_t side_cap = std::min<uint64_t>(16ull << 20, std::max<uint64_t>(size, 1024));
-  uint8_t* side = pool.alloc<uint8_t>(side_cap);
-  unsigned long long* side_used = pool.alloc<unsigned long long>(1);
-  JL_NN(A.ctl); JL_NN(A.tcnt); JL_NN(A.toff); JL_NN(A.trec); JL_NN(A.tts); JL_NN(A.recs); JL_NN(A.ts); JL_NN(A.gkey); JL_NN(A.gname);
-  JL_NN(A.gfirst); JL_NN(A.gid); JL_NN(A.slow); JL_NN(A.defer); JL_NN(A.verify); JL_NN(A.comm_rows);
-  JL_NN(A.names); JL_NN(side); JL_NN(side_used);
+  uint8_t* side = nullptr;
+  unsigned long long* side_used = nullptr;
+  uint8_t* base = nullptr;
+  uint64_t used = 0;
+  auto carve = [&](auto*& ptr, uint64_t n) {
+    used = (used + 255) & ~255ull;
+    ptr = reinterpret_cast<std::remove_reference_t<decltype(ptr)>>(base + used);
+    used += n * sizeof(*ptr);
+  };
+  for (int pass = 0; pass < 2; pass++) {
+    used = 0;
+    carve(A.ctl, 1);
+    carve(A.tcnt, 2 * ntiles);
+    carve(A.toff, 2 * ntiles);
+    carve(A.trec, ntiles * kFMaxRecs);
+    carve(A.tts, ntiles * kFMaxRecs);
+    carve(A.recs, cap);
+    carve(A.ts, cap);
+    carve(A.gkey, kFTable);
+    carve(A.gname, kFTable);
+    carve(A.gfirst, kFTable);
+    carve(A.gid, kFTable);
+    carve(A.slow, 4 * A.lcap);
+    carve(A.defer, 4 * A.lcap);
+    carve(A.verify, 2 * A.lcap);
+    carve(A.comm_rows, 3 * kFMaxNames);
+    carve(A.names, kFNameCap);
+    carve(side, side_cap);
+    carve(side_used, 1);
+    if (pass == 0) {
+      base = pool.alloc<uint8_t>(used);
+      JL_NN(base);
+    }
+  }
   A.side = Side{side, side_used, side_cap};
-  JL_TRY(cudaMemsetAsync(A.ctl, 0, sizeof(FCtl), j->st));
-  JL_TRY(cudaMemsetAsync(A.gkey, 0, kFTable * sizeof(unsigned long long), j->st));
-  JL_TRY(cudaMemsetAsync(A.gfirst, 0xFF, kFTable * sizeof(unsigned long long), j->st));
-  JL_TRY(cudaMemsetAsync(side_used, 0, sizeof(unsigned long long), j->st));
+  k_finit<<<16, 256, 0, j->st>>>(A);
   static bool attr_set = false;
   if (!attr_set) {
     JL_TRY(cudaFuncSetAttribute(k_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFStage));
