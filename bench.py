@@ -445,7 +445,7 @@ def main():
         dist.destroy_process_group()
 
 
-def loader_measure(ctx, blk=20_000, reps=50):
+def loader_measure(ctx, blk=20_000, reps=200):
     """Device JSONL loader (``load_trace``) on a generated C3 text: ``blk``
     records written with the reference wire format (write_trace), repeated ``reps``
     times, passed as host bytes.  Reported beside the headline, not part of it."""
@@ -479,6 +479,8 @@ def loader_measure(ctx, blk=20_000, reps=50):
         assert tr.records[:blk].cpu().numpy().tobytes() == want.records.tobytes() and tr.comms == want.comms
         ms, dt = statistics.median(dev_ms), statistics.median(e2e_s)
         return {"records_per_s_device": n / (ms / 1e3), "jsonl_gb_per_s_device": len(text) / (ms / 1e3) / 1e9,
+                "hbm_frac_device": len(text) / (ms / 1e3) / 1e9 / peaks()[0],
+                "pipeline": "single-pass" if tr.load_info.get("fused") else "multi-pass",
                 "ms_device": ms, "e2e_records_per_s": n / dt, "e2e_ms": dt * 1e3, "lines": n, "bytes": len(text),
                 "sample": f"C3 {blk} records x {reps} as JSONL, host bytes; median of 3",
                 "api": "load_trace (JSONL -> records in HBM; device time = CUDA events around ct_jsonl_parse)"}

@@ -1142,13 +1142,16 @@ __global__ void k_deferred_rows(uint64_t nd, const uint64_t* lines, const uint64
 // the look-behind, > kFMaxLines lines in a tile, > kFMaxNames names, lists or record
 // slots beyond their capacity) the fallback flag is raised and the caller reruns the
 // multi-pass pipeline, which has no such bounds.
-constexpr int kFThreads = 256;
-constexpr uint32_t kFT = 32 * 1024;   // terminator bytes per tile
+#ifndef CT_FTHREADS
+#define CT_FTHREADS 256
+#endif
+constexpr int kFThreads = CT_FTHREADS;
+constexpr uint32_t kFT = kFThreads * 128;  // terminator bytes per tile: 8 groups of 16 per thread
 constexpr uint32_t kFM = 4 * 1024;    // look-behind: a line may start this far before its tile
 constexpr uint32_t kFStage = kFM + kFT + 128;  // + zero padding (template reads overrun)
 static_assert(kFM + kFT < 65536, "line ends are 16-bit stage offsets");
-constexpr int kFMaxLines = 2048;
-constexpr int kFMaxRecs = 512;        // records per tile (non-blank lines averaging >= 64 bytes)
+constexpr int kFMaxLines = (int)kFT / 16;
+constexpr int kFMaxRecs = (int)kFT / 64;  // records per tile (non-blank lines averaging >= 64 bytes)
 constexpr int kFCache = 64;           // per-CTA name cache entries
 constexpr uint32_t kFNameMax = 32;    // longest name the cache holds (longer: slow list)
 constexpr uint32_t kFTable = 1u << 14;
@@ -1181,6 +1184,7 @@ struct FArgs {
   int64_t* ts;
   unsigned long long *gkey, *gname, *gfirst;  // name table: key, name ref, first record slot
   uint32_t* gid;                               // table slot -> comm id
+  uint32_t* gused;                             // inserted table slots, in insertion order
   uint64_t *slow, *defer, *verify;             // 4, 4, 2 words per entry
   uint64_t* comm_rows;
   uint8_t* names;
@@ -1216,7 +1220,9 @@ __device__ int table_slot(const FArgs& A, uint64_t key, uint64_t ref) {
     const unsigned long long old = atomicCAS(&A.gkey[i], 0ull, (unsigned long long)key);
     if (old == 0) {
       A.gname[i] = ref;
-      if (atomicAdd(&A.ctl->n_names, 1u) >= kFMaxNames) fb(A, FB_FALLBACK);
+      const unsigned int u = atomicAdd(&A.ctl->n_names, 1u);
+      if (u < kFMaxNames) A.gused[u] = i;
+      else fb(A, FB_FALLBACK);
       return (int)i;
     }
     if (old == key) return (int)i;
@@ -1893,9 +1899,11 @@ __global__ void __launch_bounds__(kFinThreads) k_ffinal(FArgs A) {
   if (tid == 0) n_used = 0;
   __syncthreads();
   if (A.ctl->flags & FB_FALLBACK) return;
-  for (uint32_t i = tid; i < kFTable; i += kFinThreads) {
+  const uint32_t nins = min(A.ctl->n_names, kFMaxNames);
+  for (uint32_t q = tid; q < nins; q += kFinThreads) {
+    const uint32_t i = A.gused[q];
     // a name whose lines all left the template path and were deferred has no first record
-    if (A.gkey[i] == 0 || A.gfirst[i] == ~0ull) continue;
+    if (A.gfirst[i] == ~0ull) continue;
     const unsigned int u = atomicAdd(&n_used, 1u);
     if (u < kFMaxNames) { ufirst[u] = A.gfirst[i]; uslot[u] = i; }
   }
@@ -2044,6 +2052,7 @@ int run_fused(ct_jsonl* j, const uint8_t* s, uint64_t size, Pool& pool, cudaEven
     carve(A.gname, kFTable);
     carve(A.gfirst, kFTable);
     carve(A.gid, kFTable);
+    carve(A.gused, kFMaxNames);
     carve(A.slow, 4 * A.lcap);
     carve(A.defer, 4 * A.lcap);
     carve(A.verify, 2 * A.lcap);
