@@ -98,6 +98,26 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
       : "memory");
 }
 
+// the same on shared-window addresses computed once per warp (no generic->shared
+// conversion in the ring loop)
+__device__ __forceinline__ void bulk_load_a(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait_a(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  }
+}
+
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t parity) {
   uint32_t done = 0;
   while (!done) {
@@ -812,6 +832,8 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
     auto chunk_bytes = [&](uint32_t c) -> uint32_t { return c < nfull ? 32u * (uint32_t)sizeof(ct_record) : tail; };
     for (uint32_t q = 0; q < (uint32_t)kRing && q < lastc; q++)
       if (lane == 0) bulk_load(W.ring[q], gsrc + (size_t)q * 32, chunk_bytes(q), &W.bar[q]);
+    const uint32_t bar_a = smem_addr(&W.bar[0]), ring_a = smem_addr(&W.ring[0][0]);
+    static_assert(sizeof(W.ring[0]) == 1024 && sizeof(W.bar[0]) == 8, "ring slot / barrier strides");
     uint32_t freed = 0;             // chunks released (slot re-issued)
     uint32_t qh = 0, qt = 0;        // element queue head / tail
     int cover = 0;                  // element lengths + copies (must equal the range's records)
@@ -824,8 +846,8 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
     uint32_t ns = 1;              // chunks scanned this step (two when both are in the ring)
     for (; q < lastc && !bail; q += ns) {
       ns = q + 1 < min(freed + (uint32_t)kRing, lastc) ? 2u : 1u;
-      mbar_wait(&W.bar[q % kRing], (q / kRing) & 1);
-      if (ns == 2) mbar_wait(&W.bar[(q + 1) % kRing], ((q + 1) / kRing) & 1);
+      mbar_wait_a(bar_a + 8 * (q % kRing), (q / kRing) & 1);
+      if (ns == 2) mbar_wait_a(bar_a + 8 * ((q + 1) % kRing), ((q + 1) / kRing) & 1);
       waited = q + ns;
       const uint32_t ql = q + ns - 1;  // last chunk of this step
       if (stream_only) {  // diagnostic: stream only (roofline experiments)
@@ -1087,12 +1109,12 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
       if (keep > freed) {
         __syncwarp();
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        do {
-          const uint32_t nq = freed + kRing;
-          if (nq < lastc && lane == 0)
-            bulk_load(W.ring[freed % kRing], gsrc + (size_t)nq * 32, chunk_bytes(nq), &W.bar[freed % kRing]);
-          freed++;
-        } while (freed < keep);
+        {  // lane j refills the slot of released chunk freed + j (keep - freed <= kRing)
+          const uint32_t c = freed + (uint32_t)lane, nq = c + kRing;
+          if (c < keep && nq < lastc)
+            bulk_load_a(ring_a + 1024 * (c % kRing), gsrc + (size_t)nq * 32, chunk_bytes(nq), bar_a + 8 * (c % kRing));
+          freed = keep;
+        }
       }
     }
     if (!bail && !(P.dbg & 4)) {  // element lengths must tile the range exactly
