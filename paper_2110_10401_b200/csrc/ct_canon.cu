@@ -137,6 +137,87 @@ __global__ void __launch_bounds__(32 * kCanonWarps) k_count(const ct_record* rec
   }
 }
 
+// k_meta and k_count in one read: the key histograms use a guessed key stride ``nmax``
+// (the largest nranks of a sample); a record with more ranks sets meta->bad bit 1 and
+// the host reruns k_count with the true stride.  Per-comm nranks / first-seen minima
+// live in shared memory and are flushed once per CTA.
+__global__ void __launch_bounds__(32 * kCanonWarps) k_count_meta(const ct_record* recs, uint64_t n, uint64_t chunk,
+                                                                uint64_t T, uint32_t K, uint32_t nmax, uint32_t kc,
+                                                                uint32_t kh, uint32_t* counts, uint32_t n_comms,
+                                                                Meta* meta, unsigned int* nr_min, unsigned int* nr_max,
+                                                                unsigned long long* cfirst) {
+  extern __shared__ unsigned long long smem_cm[];
+  unsigned long long* s_first = smem_cm;                                  // [n_comms]
+  unsigned int* s_min = reinterpret_cast<unsigned int*>(s_first + n_comms);  // [n_comms]
+  unsigned int* s_max = s_min + n_comms;                                  // [n_comms]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned int* cnt = s_max + n_comms + (size_t)warp * K;
+  for (uint32_t c = threadIdx.x; c < n_comms; c += blockDim.x) {
+    s_min[c] = 0xFFFFFFFFu; s_max[c] = 0; s_first[c] = ~0ull;
+  }
+  __syncthreads();
+  unsigned int nm = 0, bad = 0;
+  int max_dev = -1;
+  uint32_t last_comm = 0xFFFFFFFFu, last_nr = 0;
+  const uint64_t W = (uint64_t)gridDim.x * kCanonWarps;
+  for (uint64_t t = (uint64_t)blockIdx.x * kCanonWarps + warp; t < T; t += W) {
+    for (uint32_t k = lane; k < K; k += 32) cnt[k] = 0;
+    __syncwarp();
+    const uint64_t lo = t * chunk, hi = min(n, lo + chunk);
+    for (uint64_t i = lo + lane; i < hi; i += 32) {
+      const uint4 b = __ldg(reinterpret_cast<const uint4*>(recs + i) + 1);
+      const uint32_t kind = (b.w >> 16) & 7u, comm = b.x, nr = b.y & 0xFFFFu, rank = b.y >> 16;
+      const uint32_t dev = b.z & 0xFFFFu, aux = b.z >> 16, aux2 = b.w & 0xFFFFu;
+      max_dev = max(max_dev, (int)dev);
+      bool ok = true;
+      if (kind <= CT_KIND_RECV) {
+        if (comm >= n_comms || nr == 0 || rank >= nr || (kind != CT_KIND_COLLECTIVE && (aux >= nr || aux == rank))) {
+          bad |= 1u;
+          ok = false;
+        }
+        nm = max(nm, nr);
+        if (nr > nmax) { bad |= 2u; ok = false; }  // the guessed key stride is too small
+        if (kind == CT_KIND_COLLECTIVE && comm < n_comms) {
+          if (comm != last_comm || nr != last_nr) {
+            atomicMin(&s_min[comm], nr);
+            atomicMax(&s_max[comm], nr);
+            last_comm = comm;
+            last_nr = nr;
+          }
+          if (i < s_first[comm]) atomicMin(&s_first[comm], (unsigned long long)i);
+        }
+      } else if (kind <= CT_KIND_ZEROCOPY) {
+        const uint32_t ck = b.w >> 30;
+        if (ck != CT_CKIND_H2D) max_dev = max(max_dev, (int)aux);
+        if (ck != CT_CKIND_D2H) max_dev = max(max_dev, (int)aux2);
+      } else {
+        bad |= 1u;
+        ok = false;
+      }
+      if (ok) atomicAdd(&cnt[key_of(b, nmax, kc, kh)], 1u);
+    }
+    __syncwarp();
+    for (uint32_t k = lane; k < K; k += 32) counts[(uint64_t)k * T + t] = cnt[k];
+    __syncwarp();
+  }
+  __syncthreads();
+  for (uint32_t c = threadIdx.x; c < n_comms; c += blockDim.x) {
+    if (s_max[c]) {
+      atomicMin(&nr_min[c], s_min[c]);
+      atomicMax(&nr_max[c], s_max[c]);
+    }
+    if (s_first[c] != ~0ull) atomicMin(&cfirst[c], s_first[c]);
+  }
+  nm = __reduce_max_sync(0xFFFFFFFFu, nm);
+  bad = __reduce_or_sync(0xFFFFFFFFu, bad);
+  for (int o = 16; o; o >>= 1) max_dev = max(max_dev, __shfl_xor_sync(0xFFFFFFFFu, max_dev, o));
+  if (lane == 0) {
+    if (nm) atomicMax(&meta->nmax, nm);
+    if (bad) atomicOr(&meta->bad, bad);
+    atomicMax(&meta->max_dev, max_dev);
+  }
+}
+
 __global__ void k_key_totals(const uint32_t* counts, const uint64_t* offs, uint64_t T, uint32_t K, uint64_t* base,
                              uint64_t* total) {
   for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < K; k += gridDim.x * blockDim.x) {
@@ -269,7 +350,8 @@ int count_canonicalize(const ct_record* recs, uint64_t n, uint32_t n_comms, int 
   auto cleanup = [&]() {
     for (void* p : scratch) cudaFreeAsync(p, st);
   };
-  // ---- pass 1: meta
+  // ---- pass 1: meta and per-tile key counts in one read (key stride guessed from the
+  // first records; a larger nranks later reruns the count with the true stride)
   Meta* meta = dalloc<Meta>(1, st);
   unsigned int* nr_min = dalloc<unsigned int>(n_comms, st);
   unsigned int* nr_max = dalloc<unsigned int>(n_comms, st);
@@ -281,10 +363,48 @@ int count_canonicalize(const ct_record* recs, uint64_t n, uint32_t n_comms, int 
   cudaMemsetAsync(nr_min, 0xFF, n_comms * 4, st);
   cudaMemsetAsync(nr_max, 0, n_comms * 4, st);
   cudaMemsetAsync(cfirst, 0xFF, n_comms * 8, st);
-  const uint64_t blocks = std::min<uint64_t>((uint64_t)num_sms * 8, (n + 4095) / 4096);
-  const uint64_t span = (n + blocks - 1) / blocks;
-  k_meta<<<(unsigned)blocks, kMetaThreads, 0, st>>>(recs, n, span, n_comms, meta, nr_min, nr_max, cfirst);
-  L++;
+  uint32_t nguess = 1;
+  {
+    const uint64_t ns = std::min<uint64_t>(n, 1024);
+    std::vector<ct_record> sample(ns);
+    cudaMemcpyAsync(sample.data(), recs, ns * sizeof(ct_record), cudaMemcpyDeviceToHost, st);
+    if (cudaError_t e = cudaStreamSynchronize(st)) { cleanup(); return (int)e; }
+    for (const ct_record& r : sample)
+      if ((r.kc & 7) <= CT_KIND_RECV) nguess = std::max<uint32_t>(nguess, r.nranks);
+  }
+  uint32_t nmax = nguess, K = 0;
+  uint64_t kc = 0, kh = 0, chunk = 1024, T = 0;
+  uint32_t* counts = nullptr;
+  uint64_t* offs = nullptr;
+  auto keyspace = [&](uint32_t nm) -> bool {  // key stride nm -> K, tiles, count buffers
+    nmax = nm;
+    kc = (uint64_t)n_comms * nmax;
+    kh = (uint64_t)n_comms * nmax * nmax;
+    const uint64_t K64 = kc + 2 * kh + 1;
+    if (K64 > kMaxKeys) return false;
+    K = (uint32_t)K64;
+    chunk = 1024;
+    while ((n + chunk - 1) / chunk * (uint64_t)K > (64ull << 20)) chunk *= 2;  // <= 64M counters
+    T = (n + chunk - 1) / chunk;
+    counts = dalloc<uint32_t>(T * K, st);
+    offs = dalloc<uint64_t>(T * K, st);
+    scratch.insert(scratch.end(), {counts, offs});
+    return counts && offs;
+  };
+  if (!keyspace(nguess)) { cleanup(); return kCanonUnsupported; }
+  uint64_t* kbase = dalloc<uint64_t>(kMaxKeys, st);
+  uint64_t* ktot = dalloc<uint64_t>(kMaxKeys, st);
+  scratch.insert(scratch.end(), {kbase, ktot});
+  if (!kbase || !ktot) { cleanup(); return (int)cudaErrorMemoryAllocation; }
+  uint64_t ctas = std::min<uint64_t>((uint64_t)num_sms * 8, (T + kCanonWarps - 1) / kCanonWarps);
+  {
+    const size_t smem_cm = (size_t)n_comms * 16 + (size_t)kCanonWarps * K * 4;
+    cudaFuncSetAttribute(k_count_meta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_cm);
+    k_count_meta<<<(unsigned)ctas, 32 * kCanonWarps, smem_cm, st>>>(recs, n, chunk, T, K, nmax, (uint32_t)kc,
+                                                                     (uint32_t)kh, counts, n_comms, meta, nr_min,
+                                                                     nr_max, cfirst);
+    L++;
+  }
   Meta hm;
   std::vector<unsigned int> h_min(n_comms), h_max(n_comms);
   std::vector<unsigned long long> h_first(n_comms);
@@ -293,31 +413,20 @@ int count_canonicalize(const ct_record* recs, uint64_t n, uint32_t n_comms, int 
   cudaMemcpyAsync(h_max.data(), nr_max, n_comms * 4, cudaMemcpyDeviceToHost, st);
   cudaMemcpyAsync(h_first.data(), cfirst, n_comms * 8, cudaMemcpyDeviceToHost, st);
   if (cudaError_t e = cudaStreamSynchronize(st)) { cleanup(); return (int)e; }
-  if (hm.bad) { cleanup(); return kCanonUnsupported; }
+  if (hm.bad & 1u) { cleanup(); return kCanonUnsupported; }
   for (uint32_t c = 0; c < n_comms; c++)
     if (h_max[c] && h_min[c] != h_max[c]) { cleanup(); return kCanonUnsupported; }  // nranks disagreement
-  const uint32_t nmax = std::max(hm.nmax, 1u);
-  const uint64_t kc = (uint64_t)n_comms * nmax, kh = (uint64_t)n_comms * nmax * nmax;
-  const uint64_t K64 = kc + 2 * kh + 1;
-  if (K64 > kMaxKeys) { cleanup(); return kCanonUnsupported; }
-  const uint32_t K = (uint32_t)K64;
-  // ---- pass 2: per-tile key counts, one exclusive scan over [key][tile]
-  uint64_t chunk = 1024;
-  while ((n + chunk - 1) / chunk * (uint64_t)K > (64ull << 20)) chunk *= 2;  // <= 64M counters
-  const uint64_t T = (n + chunk - 1) / chunk;
-  uint32_t* counts = dalloc<uint32_t>(T * K, st);
-  uint64_t* offs = dalloc<uint64_t>(T * K, st);
-  uint64_t* kbase = dalloc<uint64_t>(K, st);
-  uint64_t* ktot = dalloc<uint64_t>(K, st);
-  scratch.insert(scratch.end(), {counts, offs, kbase, ktot});
-  if (!counts || !offs || !kbase || !ktot) { cleanup(); return (int)cudaErrorMemoryAllocation; }
+  if (hm.bad & 2u) {  // the sample under-estimated nranks: count again with the true stride
+    if (!keyspace(std::max(hm.nmax, 1u))) { cleanup(); return kCanonUnsupported; }
+    ctas = std::min<uint64_t>((uint64_t)num_sms * 8, (T + kCanonWarps - 1) / kCanonWarps);
+    const size_t smem_c = (size_t)kCanonWarps * K * 4;
+    cudaFuncSetAttribute(k_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_c);
+    k_count<<<(unsigned)ctas, 32 * kCanonWarps, smem_c, st>>>(recs, n, chunk, T, K, nmax, (uint32_t)kc, (uint32_t)kh,
+                                                              counts);
+    L++;
+  }
   const size_t smem = (size_t)kCanonWarps * K * 4;
-  const uint64_t ctas = std::min<uint64_t>((uint64_t)num_sms * 8, (T + kCanonWarps - 1) / kCanonWarps);
-  cudaFuncSetAttribute(k_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaFuncSetAttribute(k_scatter<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * smem));
-  k_count<<<(unsigned)ctas, 32 * kCanonWarps, smem, st>>>(recs, n, chunk, T, K, nmax, (uint32_t)kc, (uint32_t)kh,
-                                                          counts);
-  L++;
   {
     size_t tmp = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, tmp, counts, offs, (int64_t)(T * K), st);

@@ -155,3 +155,24 @@ def test_seq_inversion_takes_exact_path():
     assert np.array_equal(cells.astype(object), np.array(want["cells"], dtype=object))
     rc3, *_ = _analyze(buf, n, 1, force=3)
     assert rc3 == 22  # outside the counting path's scope: refused, not misanalysed
+
+
+def test_key_stride_guess_too_small_recounts():
+    """The fused meta + count pass guesses the key stride from the first 1024 records;
+    a trace whose early records all come from 2-rank communicators and whose later ones
+    reach 8 ranks is counted again with the true stride -- and equals the exact path."""
+    import torch
+    from paper_2110_10401_b200 import _lib
+    from paper_2110_10401_b200.packed import RECORD_DTYPE
+    lib = _lib.load()
+    n = lib.ct_generate_boundary(5, 200_000)
+    recs = _gen(5, n, seed=13).cpu().numpy().view(RECORD_DTYPE)
+    small = recs[recs["nranks"] == 2]
+    rest = recs[recs["nranks"] != 2]
+    assert len(small) > 2048
+    merged = np.concatenate([_process_merge(small, seed=1), _process_merge(rest, seed=2)])
+    buf = torch.from_numpy(merged.view(np.uint8).reshape(-1).copy()).cuda()
+    cap = _analyze(buf, n, 7)
+    exact = _analyze(buf, n, 7, force=2)
+    assert cap[1].path == 3 and exact[1].path == 2
+    _same(cap, exact)
