@@ -8,6 +8,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstddef>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -64,6 +65,8 @@ struct ct_context {
   bool last_explicit = false;
   uint64_t canon_n = 0;
   ShardState shard;  // multi-GPU canonicalise-then-shard state (ct_shard_*)
+  unsigned char* exp_tab = nullptr;  // ct_partial_export: global comm / channel hash tables
+  size_t exp_tab_cap = 0;
 };
 
 namespace {
@@ -203,7 +206,8 @@ int host_dev_of(ct_context* c, const ct_record* recs, uint64_t i, cudaStream_t s
 // status precedence (decomposition errors before accumulation errors).
 int summarize_state(ct_context* c, const GlobalState& gs, int gcap, int64_t d, int path,
                     const uint64_t extra_diag[3], const ct_record* arr, uint32_t n_comms,
-                    cudaStream_t st, ct_summary* out) {
+                    cudaStream_t st, ct_summary* out, const unsigned long long* pre_tcf = nullptr,
+                    const unsigned long long* pre_cells = nullptr) {
   const int g2 = gcap + 2;
   const size_t ncell = (size_t)kTypes * g2 * g2;
   c->last_state = gs;
@@ -225,9 +229,14 @@ int summarize_state(ct_context* c, const GlobalState& gs, int gcap, int64_t d, i
   // first valid instance), then sendrecv, then copies by first event
   {
     std::vector<unsigned long long> tcf(6 * (size_t)n_comms);
-    CTX_TRY(c, cudaMemcpyAsync(tcf.data(), c->tcf, tcf.size() * 8, cudaMemcpyDeviceToHost, st));
-    CTX_TRY(c, cudaMemcpyAsync(h.data(), c->cells, 2 * ncell * 8, cudaMemcpyDeviceToHost, st));  // one sync for both
-    CTX_TRY(c, cudaStreamSynchronize(st));
+    if (pre_tcf && pre_cells) {  // already on the host (one sync with the caller's own reads)
+      std::copy(pre_tcf, pre_tcf + tcf.size(), tcf.begin());
+      std::copy(pre_cells, pre_cells + h.size(), h.begin());
+    } else {
+      CTX_TRY(c, cudaMemcpyAsync(tcf.data(), c->tcf, tcf.size() * 8, cudaMemcpyDeviceToHost, st));
+      CTX_TRY(c, cudaMemcpyAsync(h.data(), c->cells, 2 * ncell * 8, cudaMemcpyDeviceToHost, st));  // one sync for both
+      CTX_TRY(c, cudaStreamSynchronize(st));
+    }
     const unsigned long long* cf = tcf.data() + 5 * (size_t)n_comms;
     std::vector<std::pair<std::pair<uint64_t, uint64_t>, int>> order;
     for (int t = 0; t < 5; t++) {
@@ -359,6 +368,7 @@ int ct_context_destroy(ct_context* c) {
   cudaFree(c->tcf);
   cudaFree(c->slots);
   cudaFree(c->chans);
+  cudaFree(c->exp_tab);
   cudaFree(c->ring);
   if (c->canon_keep) cudaFree(c->canon_keep);
   for (int k = 0; k < 4; k++) cudaEventDestroy(c->ev[k]);
@@ -758,70 +768,94 @@ uint64_t partial_words(int g2, uint32_t n_comms) {
   return kHdr + kStats + 6ull * n_comms + 2ull * kTypes * g2 * g2 + kExport * kExpWords + kExportCh * kChWords + 1;
 }
 
-// comm / channel lists of a shard in first-seen order (single thread, once per export)
-// One CTA: the unique communicators (<= kExport) and p2p channels (<= kExportCh) of this
-// shard's warp ranges, each with its first and last occurrence (lowest / highest warp
-// range), found with shared-memory hash sets; then the boundary summaries the merge
-// checks across shards (first / last block records, first / last channel seqs).
-__global__ void __launch_bounds__(1024) k_shard_export(const WarpSlot* slots, const Chans chans,
-                                                       uint32_t total_warps, const ct_record* recs, uint64_t* exp,
-                                                       uint64_t* chx, uint64_t* overflow) {
-  constexpr int TC = 2 * kExport, TH = 2 * kExportCh;
-  __shared__ unsigned long long ckey[TC], hkey[TH];
-  __shared__ uint32_t cmin[TC], cmax[TC], hmin[TH], hmax[TH];
-  __shared__ int nc, nh, ovf;
+// The unique communicators (<= kExport) and p2p channels (<= kExportCh) of a shard's warp
+// ranges, each with its first and last occurrence (lowest / highest warp range), then
+// the boundary summaries the merge checks across shards (first / last block records,
+// first / last channel seqs).  k_export_scan: every CTA hashes its slice of the warp
+// summaries into shared-memory sets and merges them into global ones (a few atomics per
+// CTA); k_export_write (one CTA) compacts the global sets into the partial.
+constexpr int kTC = 2 * kExport, kTH = 2 * kExportCh;
+struct ExpTab {
+  unsigned long long ckey[kTC], hkey[kTH];  // ~0: empty
+  uint32_t cmin[kTC], hmin[kTH];            // ~0 initially
+  uint32_t cmax[kTC], hmax[kTH];            // 0 initially
+  uint32_t overflow;
+};
+constexpr size_t kExpTabFF = offsetof(ExpTab, cmax);  // bytes set to 0xFF, the rest to 0
+
+__device__ int exp_insert(unsigned long long* tab, int cap, unsigned long long key) {
+  uint32_t h = (uint32_t)((key * 0x9E3779B97F4A7C15ull) >> 40) % (uint32_t)cap;
+  for (int probe = 0; probe < cap; probe++, h = (h + 1) % (uint32_t)cap) {
+    const unsigned long long old = atomicCAS(&tab[h], ~0ull, key);
+    if (old == ~0ull || old == key) return (int)h;
+  }
+  return -1;
+}
+
+__global__ void __launch_bounds__(256) k_export_scan(const WarpSlot* slots, const Chans chans, uint32_t total_warps,
+                                                     ExpTab* g) {
+  __shared__ unsigned long long ckey[kTC], hkey[kTH];
+  __shared__ uint32_t cmin[kTC], cmax[kTC], hmin[kTH], hmax[kTH];
+  __shared__ int ovf;
   const int tid = threadIdx.x;
-  for (int i = tid; i < TC; i += blockDim.x) { ckey[i] = ~0ull; cmin[i] = ~0u; cmax[i] = 0; }
-  for (int i = tid; i < TH; i += blockDim.x) { hkey[i] = ~0ull; hmin[i] = ~0u; hmax[i] = 0; }
-  if (tid == 0) { nc = 0; nh = 0; ovf = 0; }
+  for (int i = tid; i < kTC; i += blockDim.x) { ckey[i] = ~0ull; cmin[i] = ~0u; cmax[i] = 0; }
+  for (int i = tid; i < kTH; i += blockDim.x) { hkey[i] = ~0ull; hmin[i] = ~0u; hmax[i] = 0; }
+  if (tid == 0) ovf = 0;
   __syncthreads();
-  auto insert = [&](unsigned long long* tab, int cap, unsigned long long key) -> int {
-    uint32_t h = (uint32_t)((key * 0x9E3779B97F4A7C15ull) >> 40) % (uint32_t)cap;
-    for (int probe = 0; probe < cap; probe++, h = (h + 1) % (uint32_t)cap) {
-      const unsigned long long old = atomicCAS(&tab[h], ~0ull, key);
-      if (old == ~0ull || old == key) return (int)h;
-    }
-    return -1;
-  };
-  const uint32_t ns = total_warps * kCS, nq = total_warps * kPC;
-  for (uint32_t i = tid; i < ns; i += blockDim.x) {
+  const uint64_t ns = (uint64_t)total_warps * kCS, nq = (uint64_t)total_warps * kPC;
+  const uint64_t s0 = ns * blockIdx.x / gridDim.x, s1 = ns * (blockIdx.x + 1) / gridDim.x;
+  for (uint64_t i = s0 + tid; i < s1; i += blockDim.x) {
     const WarpSlot& x = slots[i];
     if (x.comm == 0xFFFFFFFFu || x.n == 0) continue;
-    const int h = insert(ckey, TC, x.comm);
+    const int h = exp_insert(ckey, kTC, x.comm);
     if (h < 0) { ovf = 1; continue; }
-    atomicMin(&cmin[h], i);
-    atomicMax(&cmax[h], i);
+    atomicMin(&cmin[h], (uint32_t)i);
+    atomicMax(&cmax[h], (uint32_t)i);
   }
-  // channel keys are contiguous: each thread takes 4 adjacent keys per step (two 16-byte
-  // loads in flight) so the scan is not one dependent load per iteration
-  for (uint32_t i0 = 4 * tid; i0 < nq; i0 += 4 * blockDim.x) {
-    unsigned long long k4[4];
-    if (i0 + 4 <= nq) {
-      const ulonglong2 a = *reinterpret_cast<const ulonglong2*>(&chans.key(i0));
-      const ulonglong2 b = *reinterpret_cast<const ulonglong2*>(&chans.key(i0 + 2));
-      k4[0] = a.x; k4[1] = a.y; k4[2] = b.x; k4[3] = b.y;
-    } else {
-      for (int k = 0; k < 4; k++) k4[k] = i0 + k < nq ? chans.key(i0 + k) : ~0ull;
-    }
-#pragma unroll
-    for (int k = 0; k < 4; k++) {
-      if (k4[k] == ~0ull) continue;
-      const int h = insert(hkey, TH, k4[k]);
-      if (h < 0) { ovf = 1; continue; }
-      atomicMin(&hmin[h], i0 + k);
-      atomicMax(&hmax[h], i0 + k);
-    }
+  const uint64_t q0 = nq * blockIdx.x / gridDim.x, q1 = nq * (blockIdx.x + 1) / gridDim.x;
+  for (uint64_t i = q0 + tid; i < q1; i += blockDim.x) {
+    const unsigned long long k = chans.key(i);
+    if (k == ~0ull) continue;
+    const int h = exp_insert(hkey, kTH, k);
+    if (h < 0) { ovf = 1; continue; }
+    atomicMin(&hmin[h], (uint32_t)i);
+    atomicMax(&hmax[h], (uint32_t)i);
   }
   __syncthreads();
-  // compact into the export lists (any order: the merge matches entries by key)
-  for (int i = tid; i < TC; i += blockDim.x)
+  for (int i = tid; i < kTC; i += blockDim.x)
     if (ckey[i] != ~0ull) {
+      const int h = exp_insert(g->ckey, kTC, ckey[i]);
+      if (h < 0) { ovf = 1; continue; }
+      atomicMin(&g->cmin[h], cmin[i]);
+      atomicMax(&g->cmax[h], cmax[i]);
+    }
+  for (int i = tid; i < kTH; i += blockDim.x)
+    if (hkey[i] != ~0ull) {
+      const int h = exp_insert(g->hkey, kTH, hkey[i]);
+      if (h < 0) { ovf = 1; continue; }
+      atomicMin(&g->hmin[h], hmin[i]);
+      atomicMax(&g->hmax[h], hmax[i]);
+    }
+  __syncthreads();
+  if (tid == 0 && ovf) g->overflow = 1;
+}
+
+__global__ void __launch_bounds__(256) k_export_write(const ExpTab* g, const WarpSlot* slots, const Chans chans,
+                                                      const ct_record* recs, uint64_t* exp, uint64_t* chx,
+                                                      uint64_t* overflow) {
+  __shared__ int nc, nh, ovf;
+  const int tid = threadIdx.x;
+  if (tid == 0) { nc = 0; nh = 0; ovf = g->overflow ? 1 : 0; }
+  __syncthreads();
+  // compact into the export lists (any order: the merge matches entries by key)
+  for (int i = tid; i < kTC; i += blockDim.x)
+    if (g->ckey[i] != ~0ull) {
       const int e = atomicAdd(&nc, 1);
       if (e >= kExport) { ovf = 1; continue; }
-      const WarpSlot& f = slots[cmin[i]];
-      const WarpSlot& l = slots[cmax[i]];
+      const WarpSlot& f = slots[g->cmin[i]];
+      const WarpSlot& l = slots[g->cmax[i]];
       uint64_t* o = exp + e * kExpWords;
-      o[0] = ckey[i];
+      o[0] = g->ckey[i];
       o[1] = f.n;
       o[2] = f.coll_first;
       o[3] = l.coll_last;
@@ -831,23 +865,24 @@ __global__ void __launch_bounds__(1024) k_shard_export(const WarpSlot* slots, co
         for (uint32_t r = 0; r < f.n; r++) { fr[r] = recs[f.coll_first + r]; lr[r] = recs[l.coll_last + r]; }
       }
     }
-  for (int i = tid; i < TH; i += blockDim.x)
-    if (hkey[i] != ~0ull) {
+  for (int i = tid; i < kTH; i += blockDim.x)
+    if (g->hkey[i] != ~0ull) {
       const int e = atomicAdd(&nh, 1);
       if (e >= kExportCh) { ovf = 1; continue; }
       uint64_t* o = chx + e * kChWords;
-      o[0] = hkey[i];
-      o[1] = chans.first_s(hmin[i]);
-      o[2] = chans.first_r(hmin[i]);
-      o[3] = chans.last_s(hmax[i]);
-      o[4] = chans.last_r(hmax[i]);
+      o[0] = g->hkey[i];
+      o[1] = chans.first_s(g->hmin[i]);
+      o[2] = chans.first_r(g->hmin[i]);
+      o[3] = chans.last_s(g->hmax[i]);
+      o[4] = chans.last_r(g->hmax[i]);
     }
   __syncthreads();
   if (tid == 0 && ovf) *overflow = 1;
 }
 
 __global__ void k_merge_partials(const uint64_t* parts, int world, uint64_t words, int g2, uint32_t n_comms,
-                                 unsigned long long* cells, unsigned long long* tcf, GlobalState* gs) {
+                                 unsigned long long* cells, unsigned long long* tcf, GlobalState* gs,
+                                 unsigned long long* info) {
   const uint64_t ncell = (uint64_t)kTypes * g2 * g2;
   const uint64_t o_tcf = kHdr + kStats, o_cells = o_tcf + 6ull * n_comms;
   const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, stride = (uint64_t)gridDim.x * blockDim.x;
@@ -861,6 +896,17 @@ __global__ void k_merge_partials(const uint64_t* parts, int world, uint64_t word
     tcf[j] = best;
   }
   if (tid == 0) {
+    // every partial: a ct partial of this layout (info[1]: 1 not a partial, 2 layouts
+    // differ); info[0]: records over all shards
+    unsigned long long n_all = 0, bad = 0;
+    for (int w = 0; w < world; w++) {
+      const uint64_t* p = parts + w * words;
+      if (p[0] != kPartialMagic) bad |= 1;
+      else if (p[1] != (uint64_t)g2 || p[2] != n_comms) bad |= 2;
+      n_all += p[3];
+    }
+    info[0] = n_all;
+    info[1] = bad;
     GlobalState g{};
     g.max_dev = -1;
     g.oor_key = ~0ull;
@@ -992,9 +1038,14 @@ int ct_partial_export(ct_context* c, uint64_t* dev_out, uint64_t words, void* st
   CTX_TRY(c, cudaMemsetAsync(dev_out + words - 1, 0, 8, st));
   if (c->last.path == 1 && c->last_total_warps) {
     uint64_t* chx = dev_out + o_exp + kExport * kExpWords;
-    k_shard_export<<<1, 1024, 0, st>>>(c->slots, Chans{c->chans, (uint64_t)c->last_total_warps * kPC},
-                                       c->last_total_warps, c->last_input, dev_out + o_exp, chx,
-                                       dev_out + words - 1);
+    if (ensure(c, c->exp_tab, c->exp_tab_cap, sizeof(ExpTab))) return CT_ERR_CUDA;
+    ExpTab* g = reinterpret_cast<ExpTab*>(c->exp_tab);
+    CTX_TRY(c, cudaMemsetAsync(c->exp_tab, 0xFF, kExpTabFF, st));
+    CTX_TRY(c, cudaMemsetAsync(c->exp_tab + kExpTabFF, 0, sizeof(ExpTab) - kExpTabFF, st));
+    const Chans ch{c->chans, (uint64_t)c->last_total_warps * kPC};
+    const unsigned grid = (unsigned)std::min<uint64_t>((uint64_t)c->num_sms, std::max<uint64_t>(1, c->last_total_warps / 8));
+    k_export_scan<<<grid, 256, 0, st>>>(c->slots, ch, c->last_total_warps, g);
+    k_export_write<<<1, 256, 0, st>>>(g, c->slots, ch, c->last_input, dev_out + o_exp, chx, dev_out + words - 1);
     CTX_TRY(c, cudaGetLastError());
   }
   return CT_OK;
@@ -1005,20 +1056,12 @@ int ct_partial_merge(ct_context* c, const uint64_t* dev_in, int world, uint64_t 
   if (!c || !dev_in || !out || world < 1) return fail(c, CT_ERR_ARGUMENT, "bad argument");
   CTX_TRY(c, cudaSetDevice(c->device));
   cudaStream_t st = stream ? (cudaStream_t)stream : c->stream;
-  std::vector<uint64_t> h0(4 * (size_t)world);
-  for (int w = 0; w < world; w++)
-    CTX_TRY(c, cudaMemcpyAsync(&h0[4 * w], dev_in + w * words, 32, cudaMemcpyDeviceToHost, st));
-  CTX_TRY(c, cudaStreamSynchronize(st));
-  if (h0[0] != kPartialMagic) return fail(c, CT_ERR_ARGUMENT, "not a ct partial");
-  const int g2 = (int)h0[1];
-  const uint32_t nc = (uint32_t)h0[2];
-  if (words != partial_words(g2, nc)) return fail(c, CT_ERR_ARGUMENT, "partial size mismatch");
-  uint64_t n = 0;
-  for (int w = 0; w < world; w++) {
-    if (h0[4 * w] != kPartialMagic || h0[4 * w + 1] != h0[1] || h0[4 * w + 2] != h0[2])
-      return fail(c, CT_ERR_ARGUMENT, "partials disagree on layout (use the same d / dev_hint on every rank)");
-    n += h0[4 * w + 3];
-  }
+  // the layout is this rank's own (every rank analysed with the same d / dev_hint and
+  // comm count); the merge kernel checks every partial against it on the device, so the
+  // whole merge costs one host round trip
+  const int g2 = c->last_g2;
+  const uint32_t nc = c->last_comms;
+  if (g2 < 3 || words != partial_words(g2, nc)) return fail(c, CT_ERR_ARGUMENT, "partial size mismatch");
   const uint64_t ncell = (uint64_t)kTypes * g2 * g2;
   size_t cap = c->cells_cap;
   if (ensure(c, c->cells, cap, 2 * ncell)) return CT_ERR_CUDA;
@@ -1026,26 +1069,35 @@ int ct_partial_merge(ct_context* c, const uint64_t* dev_in, int world, uint64_t 
   cap = c->tcf_cap;
   if (ensure(c, c->tcf, cap, 6ull * nc)) return CT_ERR_CUDA;
   c->tcf_cap = cap;
+  if (ensure(c, c->exp_tab, c->exp_tab_cap, sizeof(ExpTab) + 16)) return CT_ERR_CUDA;
+  unsigned long long* info = reinterpret_cast<unsigned long long*>(c->exp_tab + ((sizeof(ExpTab) + 7) & ~7ull));
   memset(out, 0, sizeof *out);
   CTX_TRY(c, cudaEventRecord(c->ev[2], st));
   CTX_TRY(c, cudaMemsetAsync(c->st, 0, sizeof(GlobalState), st));
   const uint64_t o_exp = kHdr + kStats + 6ull * nc + 2 * ncell;
   k_merge_order<<<(world * (kExport + kExportCh) + 255) / 256, 256, 0, st>>>(dev_in, world, words, o_exp, c->st);
-  k_merge_partials<<<1, 256, 0, st>>>(dev_in, world, words, g2, nc, c->cells, c->tcf, c->st);
+  k_merge_partials<<<1, 256, 0, st>>>(dev_in, world, words, g2, nc, c->cells, c->tcf, c->st, info);
   k_merge_cells<<<64, 256, 0, st>>>(dev_in, world, words, g2, nc, c->cells, c->st);
   CTX_TRY(c, cudaGetLastError());
   GlobalState gs;
+  unsigned long long hinfo[2];
+  std::vector<unsigned long long> h_tcf(6 * (size_t)nc), h_cells(2 * ncell);
   CTX_TRY(c, cudaMemcpyAsync(&gs, c->st, sizeof gs, cudaMemcpyDeviceToHost, st));
+  CTX_TRY(c, cudaMemcpyAsync(hinfo, info, sizeof hinfo, cudaMemcpyDeviceToHost, st));
+  CTX_TRY(c, cudaMemcpyAsync(h_tcf.data(), c->tcf, h_tcf.size() * 8, cudaMemcpyDeviceToHost, st));
+  CTX_TRY(c, cudaMemcpyAsync(h_cells.data(), c->cells, h_cells.size() * 8, cudaMemcpyDeviceToHost, st));
+  CTX_TRY(c, cudaEventRecord(c->ev[3], st));
   CTX_TRY(c, cudaStreamSynchronize(st));
+  if (hinfo[1] & 1) return fail(c, CT_ERR_ARGUMENT, "not a ct partial");
+  if (hinfo[1] & 2)
+    return fail(c, CT_ERR_ARGUMENT, "partials disagree on layout (use the same d / dev_hint on every rank)");
   if (gs.flags & F_NONCANON)
     return fail(c, CT_ERR_NOT_CANONICAL, "sharded analysis needs the canonical layout in every shard and across shard boundaries");
   const int gcap = g2 - 2;
   const int64_t d = c->last_explicit ? c->last.d : (int64_t)gs.max_dev + 1;
   const uint64_t extra[3] = {0, 0, 0};
-  if (int e = summarize_state(c, gs, gcap, d, 1, extra, nullptr, nc, st, out)) return e;
-  out->n_records = n;
-  CTX_TRY(c, cudaEventRecord(c->ev[3], st));
-  CTX_TRY(c, cudaEventSynchronize(c->ev[3]));
+  if (int e = summarize_state(c, gs, gcap, d, 1, extra, nullptr, nc, st, out, h_tcf.data(), h_cells.data())) return e;
+  out->n_records = hinfo[0];
   CTX_TRY(c, cudaEventElapsedTime(&out->ms_total, c->ev[2], c->ev[3]));
   out->n_launches = 3;
   c->last = *out;
