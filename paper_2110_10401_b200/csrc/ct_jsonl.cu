@@ -1352,7 +1352,7 @@ __device__ __forceinline__ uint64_t swar8(uint64_t d, uint32_t k) {
 
 // JSON integer (no sign) of <= 19 digits at p: false for anything else (leading zeros,
 // 20+ digits; fractions / exponents fail on the literal that follows)
-__device__ __forceinline__ bool fnum(const uint8_t* st, uint32_t& p, uint64_t& v) {
+__device__ __forceinline__ bool fnum_i(const uint8_t* st, uint32_t& p, uint64_t& v) {
   uint64_t x = st8(st, p) ^ 0x3030303030303030ull;
   uint64_t nd = ((x + 0x7676767676767676ull) | x) & 0x8080808080808080ull;
   uint32_t k = nd ? (uint32_t)(__ffsll((long long)nd) - 1) >> 3 : 8u;
@@ -1373,7 +1373,7 @@ __device__ __forceinline__ bool fnum(const uint8_t* st, uint32_t& p, uint64_t& v
 
 // string body at p (after the quote) up to 16 bytes without escapes: packed value for
 // enum_of; p moves past the closing quote
-__device__ __forceinline__ bool fstr16(const uint8_t* st, uint32_t& p, Str& out) {
+__device__ __forceinline__ bool fstr16_i(const uint8_t* st, uint32_t& p, Str& out) {
   const uint64_t x = st8(st, p), y = st8(st, p + 8);
   const uint64_t qx = x ^ 0x2222222222222222ull, qy = y ^ 0x2222222222222222ull;
   const uint64_t zx = (qx - 0x0101010101010101ull) & ~qx & 0x8080808080808080ull;
@@ -1387,6 +1387,54 @@ __device__ __forceinline__ bool fstr16(const uint8_t* st, uint32_t& p, Str& out)
   out.w1 = len <= 8 ? 0ull : (y & ((1ull << (8 * (len - 8))) - 1));
   p += len + 1;
   return true;
+}
+
+// One out-of-line copy of each value reader (CT_FNOINLINE, default on): the template
+// parser calls them ~20 times per line, and inlining every call site made the kernel's
+// code larger than the instruction cache; results come back by value (registers).
+#ifndef CT_FNOINLINE
+#define CT_FNOINLINE 1
+#endif
+struct NumOut {
+  uint64_t v;
+  uint32_t p;
+  uint32_t ok;
+};
+__device__ __noinline__ NumOut fnum_o(const uint8_t* st, uint32_t p) {
+  NumOut r;
+  r.ok = fnum_i(st, p, r.v) ? 1u : 0u;
+  r.p = p;
+  return r;
+}
+struct StrOut {
+  uint64_t w0, w1;
+  uint32_t len, p, ok;
+};
+__device__ __noinline__ StrOut fstr16_o(const uint8_t* st, uint32_t p) {
+  Str s;
+  StrOut r;
+  r.ok = fstr16_i(st, p, s) ? 1u : 0u;
+  r.p = p;
+  r.w0 = s.w0;
+  r.w1 = s.w1;
+  r.len = s.len;
+  return r;
+}
+__device__ __forceinline__ bool fnum(const uint8_t* st, uint32_t& p, uint64_t& v) {
+  if (!CT_FNOINLINE) return fnum_i(st, p, v);
+  const NumOut r = fnum_o(st, p);
+  p = r.p;
+  v = r.v;
+  return r.ok != 0;
+}
+__device__ __forceinline__ bool fstr16(const uint8_t* st, uint32_t& p, Str& out) {
+  if (!CT_FNOINLINE) return fstr16_i(st, p, out);
+  const StrOut r = fstr16_o(st, p);
+  p = r.p;
+  out.w0 = r.w0;
+  out.w1 = r.w1;
+  out.len = r.len;
+  return r.ok != 0;
 }
 
 // the comm name at p (after the quote): plain printable ASCII without '"' / '\\', at most
