@@ -160,3 +160,29 @@ def test_number_edges():
 def test_empty_and_blank_texts():
     for text in (b"", b"\n", b"  \n\t\n", b"\r\n\r\n"):
         check_same(text)
+
+
+def test_random_bytes_multi_tile():
+    """Garbage over several tiles (JSON punctuation, digits, terminators, invalid UTF-8,
+    fragments of canonical lines): the same records or the same first exception as the
+    reference-mirroring reader, through both pipelines."""
+    rnd = random.Random(17)
+    alphabet = b'{}[]":,0123456789-.eE abcdefghijklmnopqrstuvwxyz\t\n\r\x0b\x0c\x1c\\\xc2\x85\xe2\x80\xa8\xff'
+    canon = [line(k).encode() for k in range(50)]
+    for trial in range(12):
+        parts = []
+        while sum(map(len, parts)) < 70_000:
+            r = rnd.random()
+            if r < 0.6:
+                parts.append(rnd.choice(canon) + b"\n")
+            elif r < 0.8:  # a canonical line with a few bytes flipped
+                b = bytearray(rnd.choice(canon))
+                for _ in range(rnd.randint(1, 3)):
+                    b[rnd.randrange(len(b))] = rnd.choice(alphabet)
+                parts.append(bytes(b) + b"\n")
+            else:
+                parts.append(bytes(rnd.choice(alphabet) for _ in range(rnd.randint(1, 300))))
+        text = b"".join(parts)
+        if trial % 3 == 0:  # valid prefix, garbage only after the first tiles
+            text = b"".join(c + b"\n" for c in canon * 20) + text
+        check_same(text)
