@@ -979,6 +979,7 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
           uint64_t rseq = 0;
           uint32_t rdev = 0;
           const uint32_t j0 = n == 0 ? 0u : ((n & (n - 1)) == 0 ? (uint32_t)lane & (n - 1) : (uint32_t)lane % n);
+          const bool all8 = __all_sync(kFull, !isC || bad || h.nranks == 8);  // warp-uniform choice
           if (isC && !bad) {
             // compare raw words against the head: w4 comm, w5 nranks | rank << 16, w6 dev |
             // aux << 16 (aux = root when rooted), w7 aux2 | kc << 16 | ad << 24
@@ -1001,15 +1002,23 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
               m32 |= 1u << (dv & 31);
               devs |= (dv & 15u) << (4 * (j & 7));
             };
-            uint32_t j = j0;
-            uint32_t i = 0;
-            for (; i + 1 < n; i += 2) {
-              const uint32_t j1 = j + 1 == n ? 0 : j + 1;
-              vrec(j);
-              vrec(j1);
-              j = j1 + 1 == n ? 0 : j1 + 1;
+#ifndef CT_N8
+#define CT_N8 1
+#endif
+            if (CT_N8 && all8) {  // every block of the batch has 8 ranks: fully unrolled
+#pragma unroll
+              for (uint32_t k = 0; k < 8; k++) vrec((j0 + k) & 7u);
+            } else {
+              uint32_t j = j0;
+              uint32_t i = 0;
+              for (; i + 1 < n; i += 2) {
+                const uint32_t j1 = j + 1 == n ? 0 : j + 1;
+                vrec(j);
+                vrec(j1);
+                j = j1 + 1 == n ? 0 : j1 + 1;
+              }
+              if (i < n) vrec(j);
             }
-            if (i < n) vrec(j);
             if (badw) bad = true;
             uniform = useqw == 0;
             if (CT_LIKELY(!big)) {  // devices < 32: the mask holds them all
