@@ -397,6 +397,7 @@ __device__ __noinline__ uint32_t copy_edge_slow(const FastParams& P, unsigned lo
   Sink<SH> sk(P);
   sk.rec_key = (2ull << 62) | (min(gidx, (1ull << 41) - 1) << 21);
   sk.edge(type, src, dst, (unsigned __int128)cnt);
+  if (max(src, dst) >= 0) atomicMax(&cta_mem().max_dev, max(src, dst));  // GPU endpoints for d
   return sk.flags;
 }
 
@@ -864,8 +865,12 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
             const unsigned long long cnt = reinterpret_cast<const unsigned long long*>(R + (rel & kRM))[0];
             const int ck = (int)(b.w >> 30);
             const uint32_t aux = b.z >> 16, aux2 = b.w & 0xFFFF;
-            if (ck != CT_CKIND_H2D) my_max_dev = max(my_max_dev, (int)aux);
-            if (ck != CT_CKIND_D2H) my_max_dev = max(my_max_dev, (int)aux2);
+            // d over copy GPU endpoints: with the CTA histogram, every in-table copy leaves a
+            // cell with a frequency (read in the epilogue) and copy_edge_slow notes the rest
+            if (!SH) {
+              if (ck != CT_CKIND_H2D) my_max_dev = max(my_max_dev, (int)aux);
+              if (ck != CT_CKIND_D2H) my_max_dev = max(my_max_dev, (int)aux2);
+            }
             const int t = kind - CT_KIND_MEMCPY;  // statistics: the host sums the type's cells
             if (!no_expand) {
               const int src = ck == CT_CKIND_H2D ? -1 : (int)aux, dst = ck == CT_CKIND_D2H ? -1 : (int)aux2;
@@ -1162,15 +1167,19 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
   GlobalState* G = P.st;
   if (SH) {
     uint32_t of = 0;
+    int cmx = -1;  // copy GPU endpoints (d inference): the copy planes' touched cells
+    const int copy0 = CT_T_EXPLICIT * P.g2 * P.g2;
     for (int c = tid; c < ncell; c += kThreads) {
       const unsigned int f = shl[2 * ncell + c];
       if (!f) continue;
+      if (c >= copy0) cmx = max(cmx, max((c / P.g2) % P.g2, c % P.g2) - 2);
       const unsigned long long bb = shl[c] | ((unsigned long long)shl[ncell + c] << 32);
       const unsigned long long old = atomicAdd(P.cells + c, bb);
       if (old + bb < old) { of |= F_OVERFLOW; atomicMin(&G->of_cell, (unsigned long long)c); }
       atomicAdd(P.freq + c, (unsigned long long)f);
     }
     if (of) atomicOr(&C.flags, of);
+    if (cmx >= 0) atomicMax(&C.max_dev, cmx);
   }
   if (tid < kTypes) {
     const uint32_t* L = C.st[tid];
