@@ -22,8 +22,11 @@
 #include <thrust/iterator/counting_iterator.h>
 #include <thrust/iterator/transform_iterator.h>
 
+#include <omp.h>
+
 #include <algorithm>
 #include <array>
+#include <mutex>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -2178,6 +2181,52 @@ int run_fused(ct_jsonl* j, const uint8_t* s, uint64_t size, Pool& pool, cudaEven
   return 0;
 }
 
+// Host text -> device.  A pageable cudaMemcpy goes through the driver's bounce buffers at
+// a fraction of the link rate; large texts instead stream through two pinned 16 MB
+// staging slots: host threads copy chunk k + 1 into one slot while the DMA engine moves
+// chunk k out of the other.
+constexpr uint64_t kStageChunk = 16ull << 20;
+
+int upload_text(ct_jsonl* j, uint8_t* d, const uint8_t* text, uint64_t size) {
+  static uint8_t* pinned = nullptr;  // per process, reused across calls
+  static cudaEvent_t ev[2];
+  static std::mutex mu;
+  if (size < 4 * kStageChunk || getenv("CT_JSONL_PAGEABLE")) {
+    JL_TRY(cudaMemcpyAsync(d, text, size, cudaMemcpyHostToDevice, j->st));
+    return 0;
+  }
+  std::lock_guard<std::mutex> lock(mu);
+  if (!pinned) {
+    if (cudaHostAlloc(&pinned, 2 * kStageChunk, cudaHostAllocPortable) != cudaSuccess) {
+      pinned = nullptr;
+      JL_TRY(cudaMemcpyAsync(d, text, size, cudaMemcpyHostToDevice, j->st));
+      return 0;
+    }
+    JL_TRY(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+    JL_TRY(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+  }
+  static const int nthr_env = getenv("CT_JSONL_UPLOAD_THREADS") ? atoi(getenv("CT_JSONL_UPLOAD_THREADS")) : 4;
+  const int nthr = std::max(1, std::min(nthr_env, omp_get_max_threads()));
+  uint64_t k = 0;
+  for (uint64_t off = 0; off < size; off += kStageChunk, k++) {
+    const int slot = (int)(k & 1);
+    if (k >= 2) JL_TRY(cudaEventSynchronize(ev[slot]));  // the slot's previous DMA is done
+    const uint64_t len = std::min(kStageChunk, size - off);
+    uint8_t* dst = pinned + slot * kStageChunk;
+    const uint64_t part = (len + nthr - 1) / nthr;
+#pragma omp parallel for num_threads(nthr) schedule(static)
+    for (int q = 0; q < nthr; q++) {
+      const uint64_t a = (uint64_t)q * part;
+      if (a < len) memcpy(dst + a, text + off + a, std::min(part, len - a));
+    }
+    JL_TRY(cudaMemcpyAsync(d + off, dst, len, cudaMemcpyHostToDevice, j->st));
+    JL_TRY(cudaEventRecord(ev[slot], j->st));
+  }
+  // the staging slots are reused by the next call: their last DMAs must finish first
+  JL_TRY(cudaEventSynchronize(ev[(k - 1) & 1]));
+  return 0;
+}
+
 int run(ct_jsonl* j, const uint8_t* text, uint64_t size, int on_device) {
   Pool pool{j};
   cudaEvent_t e0, e1;
@@ -2187,7 +2236,7 @@ int run(ct_jsonl* j, const uint8_t* text, uint64_t size, int on_device) {
   if (!on_device) {
     uint8_t* d = pool.alloc<uint8_t>(size + 1);
     JL_NN(d);
-    JL_TRY(cudaMemcpyAsync(d, text, size, cudaMemcpyHostToDevice, j->st));
+    if (int e = upload_text(j, d, text, size)) return e;
     s = d;
   }
   JL_TRY(cudaEventRecord(e0, j->st));
