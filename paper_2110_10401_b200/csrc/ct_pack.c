@@ -3,7 +3,7 @@
  * (include/commtrace_b200.h), the front end of analyze_events(list[TraceEvent])
  * (reference pkg/src/commtrace/matrix.py:316-347).
  *
- *   pack(events, comm_ids, codes) -> (records: bytes, ts: bytes(int64) | None, bad: int)
+ *   pack(events, comm_ids, codes) -> (records: bytearray, ts: bytearray(int64) | None, bad: int)
  *
  * ``comm_ids`` (dict name -> id) is extended in first-seen order.  ``codes`` is a tuple
  * of dicts mapping enum ``_value_`` strings to the record codes: (kind, coll, algo,
@@ -21,6 +21,7 @@
  */
 #define PY_SSIZE_T_CLEAN
 #include <Python.h>
+#include <structmember.h>
 #include <stdint.h>
 #include <string.h>
 
@@ -38,8 +39,39 @@ typedef struct {
   uint8_t kc, ad;
 } Rec;
 
+/* Slotted classes (this package's TraceEvent / Endpoint are dataclass(slots=True)): the
+ * byte offset of every field's member descriptor, resolved once per type; a field is then
+ * one load from the object.  Other classes (the reference's TraceEvent) use getattr. */
+#define NTYPES_CACHED 4
+typedef struct { PyTypeObject* type; Py_ssize_t off[NF]; } SlotCache;
+static SlotCache g_slots[NTYPES_CACHED];
+
+static const SlotCache* slots_of(PyTypeObject* tp) {
+  for (int k = 0; k < NTYPES_CACHED; k++)
+    if (g_slots[k].type == tp) return g_slots[k].off[0] == -2 ? NULL : &g_slots[k];
+  int k = 0;
+  while (k < NTYPES_CACHED && g_slots[k].type) k++;
+  if (k == NTYPES_CACHED) return NULL;  /* cache full: getattr */
+  SlotCache* c = &g_slots[k];
+  c->type = tp;
+  Py_INCREF(tp);
+  int any = 0;
+  for (int f = 0; f < NF; f++) {
+    c->off[f] = -1;
+    PyObject* d = _PyType_Lookup(tp, g_names[f]);  /* borrowed */
+    if (d && Py_TYPE(d) == &PyMemberDescr_Type) {
+      PyMemberDef* m = ((PyMemberDescrObject*)d)->d_member;
+      if (m->type == Py_T_OBJECT_EX) { c->off[f] = m->offset; any = 1; }
+    }
+  }
+  if (!any) { c->off[0] = -2; return NULL; }
+  return c;
+}
+
 /* borrowed reference to attribute ``f`` of ``o`` (through its __dict__ when it has one) */
 static PyObject* field(PyObject* o, PyObject* dict, int f) {
+  const SlotCache* sc = slots_of(Py_TYPE(o));
+  if (sc && sc->off[f] >= 0) return *(PyObject**)((char*)o + sc->off[f]);  /* NULL: unset slot */
   if (dict) {
     PyObject* v = PyDict_GetItemWithError(dict, g_names[f]);
     if (v || PyErr_Occurred()) return v;
@@ -116,11 +148,12 @@ static PyObject* pack(PyObject* self, PyObject* args) {
            *dmap = PyTuple_GET_ITEM(codes, 3), *ckmap = PyTuple_GET_ITEM(codes, 4), *epmap = PyTuple_GET_ITEM(codes, 5);
   const Py_ssize_t n = PySequence_Fast_GET_SIZE(seqf);
   PyObject** items = PySequence_Fast_ITEMS(seqf);
-  PyObject* recs = PyBytes_FromStringAndSize(NULL, n * (Py_ssize_t)sizeof(Rec));
-  PyObject* tsb = PyBytes_FromStringAndSize(NULL, n * (Py_ssize_t)sizeof(int64_t));
+  /* bytearrays: numpy views them writable without a copy */
+  PyObject* recs = PyByteArray_FromStringAndSize(NULL, n * (Py_ssize_t)sizeof(Rec));
+  PyObject* tsb = PyByteArray_FromStringAndSize(NULL, n * (Py_ssize_t)sizeof(int64_t));
   if (!recs || !tsb) { Py_XDECREF(recs); Py_XDECREF(tsb); Py_DECREF(seqf); return NULL; }
-  Rec* out = (Rec*)PyBytes_AS_STRING(recs);
-  int64_t* ts = (int64_t*)PyBytes_AS_STRING(tsb);
+  Rec* out = (Rec*)PyByteArray_AS_STRING(recs);
+  int64_t* ts = (int64_t*)PyByteArray_AS_STRING(tsb);
   int ts_ok = 1;
   Py_ssize_t bad = -1;
   PyObject* last_comm = NULL;  /* consecutive events usually share a communicator */

@@ -169,8 +169,9 @@ def pack_events(events, comms: dict | None = None) -> PackedTrace:
         comm_ids: dict[str, int] = {} if comms is None else dict(comms)
         raw, ts, bad = native.pack(events, comm_ids, _NATIVE_CODES)
         if bad < 0:
-            rec = np.frombuffer(raw, dtype=RECORD_DTYPE).copy() if events else np.zeros(0, RECORD_DTYPE)
-            ts_out = np.frombuffer(ts, dtype=np.int64).copy() if ts is not None else [e.ts_ns for e in events]
+            # the packer's bytearrays: writable numpy views, no copy
+            rec = np.frombuffer(raw, dtype=RECORD_DTYPE) if events else np.zeros(0, RECORD_DTYPE)
+            ts_out = np.frombuffer(ts, dtype=np.int64) if ts is not None else [e.ts_ns for e in events]
             names = [None] * len(comm_ids)
             for name, cid in comm_ids.items():
                 names[cid] = name
