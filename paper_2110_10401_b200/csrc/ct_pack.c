@@ -42,7 +42,7 @@ typedef struct {
 /* Slotted classes (this package's TraceEvent / Endpoint are dataclass(slots=True)): the
  * byte offset of every field's member descriptor, resolved once per type; a field is then
  * one load from the object.  Other classes (the reference's TraceEvent) use getattr. */
-#define NTYPES_CACHED 4
+#define NTYPES_CACHED 32
 typedef struct { PyTypeObject* type; Py_ssize_t off[NF]; } SlotCache;
 static SlotCache g_slots[NTYPES_CACHED];
 
@@ -260,8 +260,142 @@ static PyObject* pack(PyObject* self, PyObject* args) {
   return Py_BuildValue("(NNn)", recs, tsb, bad);
 }
 
+/*
+ * unpack(records, ts, comms, tables) -> list[TraceEvent]: the inverse, for slotted event
+ * classes (instances are allocated and their slots filled directly; the records come
+ * from this package's packers or the device loader, so they are valid by construction).
+ *   records  buffer of n * 32 bytes
+ *   ts       buffer of n int64, or a list of n ints (timestamps beyond int64)
+ *   comms    list of comm names by id
+ *   tables   (TraceEvent type, Endpoint type, kinds[6], colls[5], algos[4], dtypes[10],
+ *             ckinds[3], HOST endpoint, GPU endpoint kind)
+ */
+static int set_slot(PyObject* o, const SlotCache* sc, int f, PyObject* v) { /* steals v */
+  if (!v) return -1;
+  PyObject** slot = (PyObject**)((char*)o + sc->off[f]);
+  Py_XSETREF(*slot, v);
+  return 0;
+}
+
+static PyObject* unpack(PyObject* self, PyObject* args) {
+  Py_buffer rb, tb;
+  PyObject *tsobj, *comms, *tables;
+  if (!PyArg_ParseTuple(args, "y*OO!O!", &rb, &tsobj, &PyList_Type, &comms, &PyTuple_Type, &tables)) return NULL;
+  PyObject* out = NULL;
+  int ts_list = PyList_Check(tsobj), have_tb = 0;
+  if (!ts_list) {
+    if (PyObject_GetBuffer(tsobj, &tb, PyBUF_SIMPLE) < 0) goto done;
+    have_tb = 1;
+  }
+  if (PyTuple_GET_SIZE(tables) != 9) { PyErr_SetString(PyExc_ValueError, "tables must hold 9 entries"); goto done; }
+  PyTypeObject* evt = (PyTypeObject*)PyTuple_GET_ITEM(tables, 0);
+  PyTypeObject* ept = (PyTypeObject*)PyTuple_GET_ITEM(tables, 1);
+  PyObject *kinds = PyTuple_GET_ITEM(tables, 2), *colls = PyTuple_GET_ITEM(tables, 3), *algos = PyTuple_GET_ITEM(tables, 4),
+           *dtypes = PyTuple_GET_ITEM(tables, 5), *ckinds = PyTuple_GET_ITEM(tables, 6);
+  PyObject *host = PyTuple_GET_ITEM(tables, 7), *gpu_kind = PyTuple_GET_ITEM(tables, 8);
+  if (!PyType_Check(evt) || !PyType_Check(ept)) { PyErr_SetString(PyExc_TypeError, "event / endpoint types"); goto done; }
+  const SlotCache* se = slots_of(evt);
+  const SlotCache* sp = slots_of(ept);
+  if (!se || !sp || sp->off[F_KIND] < 0 || sp->off[F_INDEX] < 0) {
+    PyErr_SetString(PyExc_TypeError, "unpack needs slotted event and endpoint classes");
+    goto done;
+  }
+  for (int f = 0; f < F_INDEX; f++)
+    if (se->off[f] < 0) { PyErr_SetString(PyExc_TypeError, "event class lacks a field slot"); goto done; }
+  const Py_ssize_t n = rb.len / 32;
+  if (ts_list ? PyList_GET_SIZE(tsobj) != n : tb.len / 8 != n) {
+    PyErr_SetString(PyExc_ValueError, "records and timestamps differ in length");
+    goto done;
+  }
+  out = PyList_New(n);
+  if (!out) goto done;
+  PyObject* gpu_ep[256] = {0};  /* endpoints of GPUs 0..255, shared (frozen, hashable) */
+  const Py_ssize_t ncomms = PyList_GET_SIZE(comms);
+  const uint8_t* base = (const uint8_t*)rb.buf;
+  for (Py_ssize_t i = 0; i < n; i++) {
+    Rec r;
+    memcpy(&r, base + 32 * i, 32);
+    const int kind = r.kc & 7;
+    if (kind > 5 || r.comm >= ncomms) { PyErr_SetString(PyExc_ValueError, "malformed record"); Py_CLEAR(out); goto done; }
+    PyObject* ev = evt->tp_alloc(evt, 0);
+    if (!ev) { Py_CLEAR(out); goto done; }
+    PyList_SET_ITEM(out, i, ev);
+    for (int f = 0; f < F_INDEX; f++) { Py_INCREF(Py_None); set_slot(ev, se, f, Py_None); }
+    PyObject* tsv = ts_list ? Py_NewRef(PyList_GET_ITEM(tsobj, i)) : PyLong_FromLongLong(((const int64_t*)tb.buf)[i]);
+    PyObject* cm = PyList_GET_ITEM(comms, r.comm);
+    if (set_slot(ev, se, F_SEQ, PyLong_FromUnsignedLongLong(r.seq)) || set_slot(ev, se, F_TS, tsv) ||
+        set_slot(ev, se, F_KIND, Py_NewRef(PyTuple_GET_ITEM(kinds, kind))) || set_slot(ev, se, F_COMM, Py_NewRef(cm)) ||
+        set_slot(ev, se, F_NRANKS, PyLong_FromLong(r.nranks)) || set_slot(ev, se, F_RANK, PyLong_FromLong(r.rank)) ||
+        set_slot(ev, se, F_DEV, PyLong_FromLong(r.dev))) { Py_CLEAR(out); goto done; }
+    int bad = 0;
+    if (kind == 0) {
+      const int coll = (r.kc >> 3) & 7, algo = r.ad & 3, dt = (r.ad >> 2) & 15;
+      if (coll > 4 || dt > 9) { bad = 1; }
+      else {
+        bad |= set_slot(ev, se, F_COLL, Py_NewRef(PyTuple_GET_ITEM(colls, coll)));
+        bad |= set_slot(ev, se, F_ALGO, Py_NewRef(PyTuple_GET_ITEM(algos, algo)));
+        if ((r.kc >> 6) & 1) bad |= set_slot(ev, se, F_ROOT, PyLong_FromLong(r.aux));
+        bad |= set_slot(ev, se, F_COUNT, PyLong_FromUnsignedLongLong(r.count));
+        bad |= set_slot(ev, se, F_DTYPE, Py_NewRef(PyTuple_GET_ITEM(dtypes, dt)));
+      }
+    } else if (kind <= 2) {
+      const int dt = (r.ad >> 2) & 15;
+      if (dt > 9) { bad = 1; }
+      else {
+        bad |= set_slot(ev, se, F_PEER, PyLong_FromLong(r.aux));
+        bad |= set_slot(ev, se, F_COUNT, PyLong_FromUnsignedLongLong(r.count));
+        bad |= set_slot(ev, se, F_DTYPE, Py_NewRef(PyTuple_GET_ITEM(dtypes, dt)));
+      }
+    } else {
+      const int ck = (r.ad >> 6) & 3;
+      if (ck > 2) { bad = 1; }
+      else {
+        PyObject* ends[2] = {NULL, NULL};
+        const int is_host[2] = {ck == 0, ck == 1};
+        const uint16_t idx[2] = {r.aux, r.aux2};
+        for (int e = 0; e < 2 && !bad; e++) {
+          if (is_host[e]) { ends[e] = Py_NewRef(host); continue; }
+          PyObject* g = idx[e] < 256 ? gpu_ep[idx[e]] : NULL;
+          if (!g) {
+            g = ept->tp_alloc(ept, 0);
+            if (!g || set_slot(g, sp, F_KIND, Py_NewRef(gpu_kind)) || set_slot(g, sp, F_INDEX, PyLong_FromLong(idx[e]))) {
+              Py_XDECREF(g);
+              bad = 1;
+              break;
+            }
+            if (idx[e] < 256) gpu_ep[idx[e]] = g;  /* the cache holds this reference */
+            else { ends[e] = g; continue; }
+          }
+          ends[e] = Py_NewRef(g);
+        }
+        if (!bad) {
+          bad |= set_slot(ev, se, F_CKIND, Py_NewRef(PyTuple_GET_ITEM(ckinds, ck)));
+          bad |= set_slot(ev, se, F_SRC, ends[0]);
+          bad |= set_slot(ev, se, F_DST, ends[1]);
+          bad |= set_slot(ev, se, F_BYTES, PyLong_FromUnsignedLongLong(r.count));
+        } else {
+          Py_XDECREF(ends[0]);
+          Py_XDECREF(ends[1]);
+        }
+      }
+    }
+    if (bad) {
+      if (!PyErr_Occurred()) PyErr_SetString(PyExc_ValueError, "malformed record");
+      for (int k = 0; k < 256; k++) Py_XDECREF(gpu_ep[k]);
+      Py_CLEAR(out);
+      goto done;
+    }
+  }
+  for (int k = 0; k < 256; k++) Py_XDECREF(gpu_ep[k]);
+done:
+  PyBuffer_Release(&rb);
+  if (have_tb) PyBuffer_Release(&tb);
+  return out;
+}
+
 static PyMethodDef kMethods[] = {
     {"pack", pack, METH_VARARGS, "pack(events, comm_ids, codes) -> (records, ts, bad)"},
+    {"unpack", unpack, METH_VARARGS, "unpack(records, ts, comms, tables) -> list[TraceEvent]"},
     {NULL, NULL, 0, NULL}};
 
 static struct PyModuleDef kModule = {PyModuleDef_HEAD_INIT, "_ctpack", "native TraceEvent packer", -1, kMethods};

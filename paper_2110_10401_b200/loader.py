@@ -175,4 +175,40 @@ def load_trace_file(path, device: int | None = None) -> PackedTrace:
         return load_trace(fh.read(), device=device)
 
 
-__all__ = ["load_trace", "load_trace_file"]
+#: texts at least this large are read by the device loader in ``parse_trace``
+DEVICE_PARSE_MIN_BYTES = 1 << 20
+
+
+def _device_ready() -> bool:
+    try:
+        import torch
+
+        if not torch.cuda.is_available():
+            return False
+        _lib.load()
+        return True
+    except Exception:
+        return False
+
+
+def parse_trace(source) -> list:
+    """``parse_trace`` of the drop-in API (reference events.py:352-384): the same
+    TraceEvent list and the same exceptions.  A text of 1 MB or more goes through the
+    device loader (``load_trace``) and the native unpacker; a smaller one through the
+    reference-mirroring host reader (``events.parse_trace``), whose per-call cost is lower
+    than a device round trip."""
+    from .events import parse_trace as host_parse
+    from .packed import unpack
+
+    data = source if isinstance(source, (str, bytes, bytearray, memoryview)) else source.read()
+    if len(data) >= DEVICE_PARSE_MIN_BYTES and _device_ready():
+        return unpack(load_trace(data))
+    return host_parse(data)
+
+
+def parse_trace_file(path) -> list:
+    with open(path, "rb") as fh:
+        return parse_trace(fh.read())
+
+
+__all__ = ["load_trace", "load_trace_file", "parse_trace", "parse_trace_file"]

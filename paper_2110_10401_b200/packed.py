@@ -252,5 +252,39 @@ def unpack_record(r, comms, ts: int = 0) -> TraceEvent:
     return TraceEvent(**base, copy_kind=ck, copy_src=src, copy_dst=dst, bytes=int(r["count"]))
 
 
+def _unpack_tables():
+    return (TraceEvent, Endpoint, tuple(KINDS[i] for i in range(6)), tuple(COLLS[i] for i in range(5)),
+            tuple(ALGOS[i] for i in range(4)), tuple(DTYPES[i] for i in range(10)), tuple(CKINDS[i] for i in range(3)),
+            HOST, EndpointKind.GPU)
+
+
 def unpack(trace: PackedTrace) -> list[TraceEvent]:
-    return [trace.event(i) for i in range(len(trace))]
+    """The TraceEvent objects of a packed trace (the original objects when it was packed
+    from them).  The native unpacker (``csrc/ct_pack.c``) builds the slotted objects
+    directly; without it, record by record in Python."""
+    if trace.events is not None:
+        return list(trace.events)
+    native = _native()
+    n = len(trace)
+    if native is not None and n:
+        rec = trace.records
+        if not isinstance(rec, np.ndarray):  # device records (a CUDA tensor of rows)
+            rec = rec.cpu().numpy()
+        raw = np.ascontiguousarray(rec).view(np.uint8).reshape(-1)
+        ts = trace.ts
+        if ts is None:
+            ts = np.zeros(n, np.int64)
+        elif not isinstance(ts, np.ndarray):
+            ts = [int(t) for t in ts]
+        else:
+            ts = np.ascontiguousarray(ts, dtype=np.int64)
+        import gc
+
+        was = gc.isenabled()
+        gc.disable()  # millions of new container objects would trigger collections all along
+        try:
+            return native.unpack(raw, ts, list(trace.comms), _unpack_tables())
+        finally:
+            if was:
+                gc.enable()
+    return [trace.event(i) for i in range(n)]

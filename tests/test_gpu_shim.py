@@ -51,7 +51,8 @@ def test_real_nccl_trace_loads_and_analyses(tmp_path):
     main = [o for o in objs if o["comm"] == objs[0]["comm"]]
     assert [o["seq"] for o in main] == list(range(len(main)))
 
-    from paper_2110_10401_b200 import analyze_packed, load_trace, parse_trace, pack_events
+    from paper_2110_10401_b200 import analyze_packed, load_trace, pack_events
+    from paper_2110_10401_b200.events import parse_trace
     tr = load_trace(text.encode())
     assert tr.load_info["deferred"] == 0
     ref = pack_events(parse_trace(text))

@@ -118,3 +118,27 @@ def test_native_packer_speed():
     tr = PK.pack_events(evs)
     dt = time.perf_counter() - t0
     assert len(tr) == len(evs) and len(evs) / dt > 1_000_000, len(evs) / dt
+
+
+def test_native_unpack_round_trip(golden_traces):
+    """unpack (csrc/ct_pack.c) rebuilds exactly the events the records came from: every
+    golden trace (all kinds, copies to / from the host, GPU endpoints, rooted and
+    unrooted collectives), big timestamps (list ts), GPUs beyond the endpoint cache."""
+    for case in golden_traces:
+        evs = parse_trace(case["jsonl"])
+        if not evs:
+            continue
+        tr = PK.pack_events(evs)
+        back = PK.unpack(PK.PackedTrace(tr.records, tr.comms, tr.ts, None))
+        assert back == evs
+    evs = [
+        TraceEvent(seq=1, ts_ns=1 << 70, kind=EventKind.MEMCPY, comm="c", n_ranks=1, rank=0, device=3,
+                   copy_kind=CopyKind.D2D, copy_src=gpu(300), copy_dst=gpu(7), bytes=1 << 63),
+        TraceEvent(seq=(1 << 64) - 1, ts_ns=-5, kind=EventKind.COLLECTIVE, comm="d", n_ranks=4, rank=3,
+                   device=65535, collective=CollectiveKind.REDUCE, algorithm=Algorithm.RING, root=2,
+                   count=0, dtype=DataType.BFLOAT16),
+        TraceEvent(seq=0, ts_ns=0, kind=EventKind.UNIFIED_MEMORY, comm="c", n_ranks=1, rank=0, device=0,
+                   copy_kind=CopyKind.D2H, copy_src=gpu(0), copy_dst=HOST, bytes=0),
+    ]
+    tr = PK.pack_events(evs)
+    assert PK.unpack(PK.PackedTrace(tr.records, tr.comms, tr.ts, None)) == evs
