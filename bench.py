@@ -556,6 +556,29 @@ def object_api_measure(ctx, n=1_000_000, ref_sample=100_000):
             out[name] = {"events": len(evs), "records_per_s": len(evs) / dt, "ms": dt * 1e3,
                          "ref_port_records_per_s": k / rdt, "ref_port_sample": k, "ref_port_cores": 1,
                          "instances": res.stats.instances, "ref_instances_in_sample": want["result"]["instances"]}
+        # the literal drop-in path on a JSONL text: parse_trace (device loader + native
+        # unpack) then analyze_events, against the reference's own CPU path restated
+        # (oracle parse_jsonl + analyze_flat, one process) on a sample of the same text
+        import paper_2110_10401_b200 as P
+        from paper_2110_10401_b200.events import write_trace
+
+        text = write_trace(big)
+        lines = text.splitlines(keepends=True)
+        P.analyze_events(P.parse_trace(b"".join(lines[:20_000])))  # warm-up
+        ts = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            res = P.analyze_events(P.parse_trace(text))
+            ts.append(time.perf_counter() - t0)
+        dt = statistics.median(ts)
+        sample = b"".join(lines[:ref_sample])
+        t0 = time.perf_counter()
+        O.analyze_flat(O.parse_jsonl(sample))
+        rdt = time.perf_counter() - t0
+        out["parse_analyze_C3_1M"] = {"lines": n, "bytes": len(text), "lines_per_s": n / dt, "ms": dt * 1e3,
+                                      "ref_port_lines_per_s": ref_sample / rdt, "ref_port_sample": ref_sample,
+                                      "instances": res.stats.instances,
+                                      "api": "parse_trace(jsonl) + analyze_events (drop-in top-level API)"}
         out["api"] = ("analyze_events(list[TraceEvent]) end to end (native packer, pinned-less H2D, device "
                       "analysis, result objects); ref_port = reference algorithm CPU port on the same events")
         return out
