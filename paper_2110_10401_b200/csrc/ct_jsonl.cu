@@ -1152,7 +1152,8 @@ constexpr int kFThreads = CT_FTHREADS;
 constexpr uint32_t kFT = kFThreads * 128;  // terminator bytes per tile: 8 groups of 16 per thread
 constexpr uint32_t kFM = 4 * 1024;    // look-behind: a line may start this far before its tile
 constexpr uint32_t kFStage = kFM + kFT + 128;  // + zero padding (template reads overrun)
-static_assert(kFM + kFT < 65536, "line ends are 16-bit stage offsets");
+// stage offsets of line ends / tail starts: 16 bits while the stage allows it
+using StOff = std::conditional_t<(kFM + kFT < 65536), uint16_t, uint32_t>;
 constexpr int kFMaxLines = (int)kFT / 16;
 constexpr int kFMaxRecs = (int)kFT / 64;  // records per tile (non-blank lines averaging >= 64 bytes)
 constexpr int kFCache = 64;           // per-CTA name cache entries
@@ -1555,7 +1556,7 @@ __device__ bool fast_suffix(const uint8_t* st, uint32_t p, uint32_t e, int kind,
 __global__ void __launch_bounds__(kFThreads) k_fused(FArgs A) {
   extern __shared__ __align__(16) uint8_t st[];  // the stage: [st0, t1) and 32 zero-padded bytes
   __shared__ uint16_t msk[(kFM + kFT) / 16];
-  __shared__ uint16_t tp[kFMaxLines + 1];          // line ends (stage offsets < 2^16)
+  __shared__ StOff tp[kFMaxLines + 1];             // line ends (stage offsets)
   __shared__ uint16_t rl[kFMaxLines];              // record index within the tile (0xFFFF: blank)
   __shared__ unsigned long long ckey[kFCache];
   __shared__ unsigned long long cref[kFCache];
@@ -1671,7 +1672,7 @@ __global__ void __launch_bounds__(kFThreads) k_fused(FArgs A) {
       while (m) {
         const int j = __ffs(m) - 1;
         m &= m - 1;
-        tp[off++] = (uint16_t)(16 * (g0 + k) + j);
+        tp[off++] = (StOff)(16 * (g0 + k) + j);
       }
     }
   }
@@ -1680,7 +1681,7 @@ __global__ void __launch_bounds__(kFThreads) k_fused(FArgs A) {
     uint32_t L = min(tot, (uint32_t)kFMaxLines);
     if (t1 == A.size && !s_abort) {  // the final line when the text does not end with a terminator
       const uint32_t le = L ? tp[L - 1] + blen_s(st, tp[L - 1], nst) : s_prev;
-      if (le < nst && L < (uint32_t)kFMaxLines) tp[L++] = (uint16_t)nst;
+      if (le < nst && L < (uint32_t)kFMaxLines) tp[L++] = (StOff)nst;
       else if (le < nst) s_abort = 1;
     }
     s_nl = L;
@@ -1721,15 +1722,15 @@ __global__ void __launch_bounds__(kFThreads) k_fused(FArgs A) {
   // kFThreads lines: the common head (thread = line), the name through the cache, then
   // the kind-specific tail with the lines regrouped by kind so that warps stay uniform.
   // The mask array is free now: per-line state between the two halves lives there.
-  uint16_t* s_p = reinterpret_cast<uint16_t*>(msk);   // tail start
-  uint16_t* s_n = s_p + kFThreads;                     // nranks, rank, dev, comm slot
+  StOff* s_p = reinterpret_cast<StOff*>(msk);         // tail start
+  uint16_t* s_n = reinterpret_cast<uint16_t*>(s_p + kFThreads);  // nranks, rank, dev, comm slot
   uint16_t* s_rank = s_n + kFThreads;
   uint16_t* s_dev = s_rank + kFThreads;
   uint16_t* s_cs = s_dev + kFThreads;
   uint8_t* s_kind = reinterpret_cast<uint8_t*>(s_cs + kFThreads);
   uint8_t* s_ce = s_kind + kFThreads;
-  uint8_t* s_ord = s_ce + kFThreads;                   // regrouped position -> line of the round
-  static_assert(kFThreads * 13 <= (int)sizeof(msk), "per-line state must fit the mask array");
+  uint16_t* s_ord = reinterpret_cast<uint16_t*>(s_ce + kFThreads);  // regrouped position -> line of the round
+  static_assert(kFThreads * (12 + (int)sizeof(StOff)) <= (int)sizeof(msk), "per-line state must fit the mask array");
   __shared__ uint32_t s_wcnt[3][kFThreads / 32];
   const int warp = tid >> 5, lane = tid & 31;
   for (uint32_t r0 = 0; r0 < L; r0 += kFThreads) {
@@ -1788,7 +1789,7 @@ __global__ void __launch_bounds__(kFThreads) k_fused(FArgs A) {
         const uint64_t slot = t * kFMaxRecs + rl[k];
         reinterpret_cast<unsigned long long*>(A.trec + slot)[1] = o.r.seq;
         A.tts[slot] = o.ts;
-        s_p[tid] = (uint16_t)p;
+        s_p[tid] = (StOff)p;
         s_n[tid] = o.r.nranks;
         s_rank[tid] = o.r.rank;
         s_dev[tid] = o.r.dev;
@@ -1816,7 +1817,7 @@ __global__ void __launch_bounds__(kFThreads) k_fused(FArgs A) {
         if (c < cls || (c == cls && w < warp)) pos += v;
         nsorted += v;
       }
-    if (cls < 3) s_ord[pos + __popc(bm[cls] & ((1u << lane) - 1))] = (uint8_t)tid;
+    if (cls < 3) s_ord[pos + __popc(bm[cls] & ((1u << lane) - 1))] = (uint16_t)tid;
     __syncthreads();
     if ((uint32_t)tid < nsorted) {
       const uint32_t i = s_ord[tid], kk = r0 + i;
