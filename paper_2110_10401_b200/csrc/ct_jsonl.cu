@@ -2189,21 +2189,24 @@ int run_fused(ct_jsonl* j, const uint8_t* s, uint64_t size, Pool& pool, cudaEven
 constexpr uint64_t kStageChunk = 16ull << 20;
 
 int upload_text(ct_jsonl* j, uint8_t* d, const uint8_t* text, uint64_t size) {
-  static uint8_t* pinned = nullptr;  // per process, reused across calls
-  static cudaEvent_t ev[2];
-  static std::mutex mu;
-  if (size < 4 * kStageChunk || getenv("CT_JSONL_PAGEABLE")) {
+  constexpr int kDevs = 64;
+  static uint8_t* pinned_of[kDevs] = {};  // per device, reused across calls
+  static cudaEvent_t ev_of[kDevs][2];
+  static std::mutex mu_of[kDevs];
+  if (size < 4 * kStageChunk || getenv("CT_JSONL_PAGEABLE") || j->device < 0 || j->device >= kDevs) {
     JL_TRY(cudaMemcpyAsync(d, text, size, cudaMemcpyHostToDevice, j->st));
     return 0;
   }
-  std::lock_guard<std::mutex> lock(mu);
+  std::lock_guard<std::mutex> lock(mu_of[j->device]);
+  uint8_t*& pinned = pinned_of[j->device];
+  cudaEvent_t* ev = ev_of[j->device];
   if (!pinned) {
     if (cudaHostAlloc(&pinned, 2 * kStageChunk, cudaHostAllocPortable) != cudaSuccess) {
       pinned = nullptr;
       JL_TRY(cudaMemcpyAsync(d, text, size, cudaMemcpyHostToDevice, j->st));
       return 0;
     }
-    JL_TRY(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+    JL_TRY(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));  // on j->device (set by the caller)
     JL_TRY(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
   }
   static const int nthr_env = getenv("CT_JSONL_UPLOAD_THREADS") ? atoi(getenv("CT_JSONL_UPLOAD_THREADS")) : 4;
