@@ -67,6 +67,15 @@ struct ct_context {
   ShardState shard;  // multi-GPU canonicalise-then-shard state (ct_shard_*)
   unsigned char* exp_tab = nullptr;  // ct_partial_export: global comm / channel hash tables
   size_t exp_tab_cap = 0;
+  // pinned host copies of the last fast run's state / cells / first-occurrence keys:
+  // read back with one synchronisation, then used by summarize_state
+  GlobalState* h_state = nullptr;  // [0] initial state uploaded, [1] result
+  unsigned long long* h_cells = nullptr;
+  size_t h_cells_cap = 0;
+  unsigned long long* h_tcf = nullptr;
+  size_t h_tcf_cap = 0;
+  int h_g2 = 0;             // layout the host copies hold (0: none)
+  uint32_t h_comms = 0;
 };
 
 namespace {
@@ -94,6 +103,18 @@ int ensure(ct_context* c, T*& p, size_t& cap, size_t need) {
   size_t n = std::max(need, (size_t)1);
   cudaError_t e = cudaMalloc(&p, n * sizeof(T));
   if (e != cudaSuccess) { cap = 0; return cuda_fail(c, e, "cudaMalloc"); }
+  cap = n;
+  return 0;
+}
+
+template <typename T>
+int ensure_host(ct_context* c, T*& p, size_t& cap, size_t need) {
+  if (need <= cap && p) return 0;
+  if (p) cudaFreeHost(p);
+  p = nullptr;
+  size_t n = std::max(need, (size_t)1);
+  cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&p), n * sizeof(T), cudaHostAllocDefault);
+  if (e != cudaSuccess) { cap = 0; p = nullptr; return cuda_fail(c, e, "cudaHostAlloc"); }
   cap = n;
   return 0;
 }
@@ -128,7 +149,13 @@ int run_fast(ct_context* c, const ct_record* recs, uint64_t n, int gcap, bool ex
   CTX_TRY(c, cudaMemsetAsync(c->cells, 0, 2 * ncell * sizeof(unsigned long long), st));
   CTX_TRY(c, cudaMemsetAsync(c->tcf, 0xFF, tcf_need * sizeof(unsigned long long), st));
   {
-    GlobalState init{};
+    size_t hs_cap = c->h_state ? 2 : 0;
+    if (ensure_host(c, c->h_state, hs_cap, 2)) return CT_ERR_CUDA;
+    if (ensure_host(c, c->h_cells, c->h_cells_cap, 2 * ncell)) return CT_ERR_CUDA;
+    if (ensure_host(c, c->h_tcf, c->h_tcf_cap, tcf_need)) return CT_ERR_CUDA;
+    c->h_g2 = 0;  // invalid until this run's read-back
+    GlobalState& init = c->h_state[0];
+    init = GlobalState{};
     init.max_dev = -1;
     for (int k = 0; k < 3; k++) init.copy_first[k] = ~0ull;
     init.oor_key = ~0ull;
@@ -173,8 +200,14 @@ int run_fast(ct_context* c, const ct_record* recs, uint64_t n, int gcap, bool ex
     CTX_TRY(c, cudaGetLastError());
     launches += 2;
   }
-  CTX_TRY(c, cudaMemcpyAsync(&out->gs, c->st, sizeof(GlobalState), cudaMemcpyDeviceToHost, st));
+  // state, cells and first-occurrence keys in one round trip (summarize_state reuses them)
+  CTX_TRY(c, cudaMemcpyAsync(&c->h_state[1], c->st, sizeof(GlobalState), cudaMemcpyDeviceToHost, st));
+  CTX_TRY(c, cudaMemcpyAsync(c->h_cells, c->cells, 2 * ncell * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+  CTX_TRY(c, cudaMemcpyAsync(c->h_tcf, c->tcf, tcf_need * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
   CTX_TRY(c, cudaStreamSynchronize(st));
+  out->gs = c->h_state[1];
+  c->h_g2 = g2;
+  c->h_comms = n_comms;
   if (n) CTX_TRY(c, cudaEventElapsedTime(&out->ms_kernel, c->ev[0], c->ev[1]));
   out->launches = launches;
   return 0;
@@ -369,6 +402,9 @@ int ct_context_destroy(ct_context* c) {
   cudaFree(c->slots);
   cudaFree(c->chans);
   cudaFree(c->exp_tab);
+  cudaFreeHost(c->h_state);
+  cudaFreeHost(c->h_cells);
+  cudaFreeHost(c->h_tcf);
   cudaFree(c->ring);
   if (c->canon_keep) cudaFree(c->canon_keep);
   for (int k = 0; k < 4; k++) cudaEventDestroy(c->ev[k]);
@@ -541,7 +577,10 @@ int ct_analyze(ct_context* c, const ct_record* recs, uint64_t n, int on_device, 
   {
     const uint64_t extra[3] = {ran_exact ? ex_res.n_incomplete : 0, ran_exact ? ex_res.n_unmatched_send : 0,
                                ran_exact ? ex_res.n_unmatched_recv : 0};
-    if (int e = summarize_state(c, ro.gs, gcap, d, path, extra, arr, n_comms, st, out)) return e;
+    const bool pre = c->h_g2 == gcap + 2 && c->h_comms == n_comms;  // the final run's read-back
+    if (int e = summarize_state(c, ro.gs, gcap, d, path, extra, arr, n_comms, st, out, pre ? c->h_tcf : nullptr,
+                                pre ? c->h_cells : nullptr))
+      return e;
   }
   CTX_TRY(c, cudaEventRecord(c->ev[3], st));
   CTX_TRY(c, cudaEventSynchronize(c->ev[3]));
