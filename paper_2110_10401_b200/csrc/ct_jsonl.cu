@@ -2119,10 +2119,10 @@ int run_fused(ct_jsonl* j, const uint8_t* s, uint64_t size, Pool& pool, cudaEven
   }
   A.side = Side{side, side_used, side_cap};
   k_finit<<<16, 256, 0, j->st>>>(A);
-  static bool attr_set = false;
-  if (!attr_set) {
+  static bool attr_set[64] = {};  // the attribute lives in each device's context
+  if (j->device < 0 || j->device >= 64 || !attr_set[j->device]) {
     JL_TRY(cudaFuncSetAttribute(k_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFStage));
-    attr_set = true;
+    if (j->device >= 0 && j->device < 64) attr_set[j->device] = true;
   }
   const bool dbg = getenv("CT_JSONL_DEBUG") != nullptr;
   cudaEvent_t ev[6];
