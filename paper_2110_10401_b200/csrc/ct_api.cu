@@ -922,8 +922,7 @@ __global__ void __launch_bounds__(256) k_export_write(const ExpTab* g, const War
 __global__ void k_merge_partials(const uint64_t* parts, int world, uint64_t words, int g2, uint32_t n_comms,
                                  unsigned long long* cells, unsigned long long* tcf, GlobalState* gs,
                                  unsigned long long* info) {
-  const uint64_t ncell = (uint64_t)kTypes * g2 * g2;
-  const uint64_t o_tcf = kHdr + kStats, o_cells = o_tcf + 6ull * n_comms;
+  const uint64_t o_tcf = kHdr + kStats;
   const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t j = tid; j < 6ull * n_comms; j += stride) {
     uint64_t best = ~0ull, base = 0;

@@ -573,13 +573,6 @@ struct SAReq {
   bool act;
 };
 
-__device__ __forceinline__ void limb_add(uint32_t* L, unsigned long long v) {  // v < 2^63, no wrap
-  const uint32_t a = (uint32_t)v;
-  const uint32_t o = atomicAdd(L, a);
-  const uint32_t h = (uint32_t)(v >> 32) + (o + a < o ? 1u : 0u);
-  if (h) atomicAdd(L + 1, h);
-}
-
 // Edge-by-edge expansion of one VALID instance (the accumulators did not take it):
 // statistics, then every transfer through one emission site.  Out of line to keep the
 // accumulator fast path compact in the instruction cache.

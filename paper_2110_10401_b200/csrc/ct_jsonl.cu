@@ -2182,52 +2182,103 @@ int run_fused(ct_jsonl* j, const uint8_t* s, uint64_t size, Pool& pool, cudaEven
   return 0;
 }
 
-// Host text -> device.  A pageable cudaMemcpy goes through the driver's bounce buffers at
-// a fraction of the link rate; large texts instead stream through two pinned 16 MB
-// staging slots: host threads copy chunk k + 1 into one slot while the DMA engine moves
-// chunk k out of the other.
+// Host <-> device through pinned staging.  A pageable cudaMemcpy goes through the
+// driver's bounce buffers at a fraction of the link rate; large transfers instead stream
+// through two pinned 16 MB slots per device: host threads copy chunk k + 1 into (or out
+// of) one slot while the DMA engine moves chunk k through the other.
 constexpr uint64_t kStageChunk = 16ull << 20;
 
-int upload_text(ct_jsonl* j, uint8_t* d, const uint8_t* text, uint64_t size) {
+struct Staging {  // per device, created on first use and reused across calls
+  uint8_t* pinned = nullptr;
+  cudaEvent_t ev[2];
+  std::mutex mu;
+};
+
+Staging* staging_for(int device) {
   constexpr int kDevs = 64;
-  static uint8_t* pinned_of[kDevs] = {};  // per device, reused across calls
-  static cudaEvent_t ev_of[kDevs][2];
-  static std::mutex mu_of[kDevs];
-  if (size < 4 * kStageChunk || getenv("CT_JSONL_PAGEABLE") || j->device < 0 || j->device >= kDevs) {
+  static Staging st_of[kDevs];
+  static std::mutex init_mu;
+  if (device < 0 || device >= kDevs) return nullptr;
+  Staging& S = st_of[device];
+  std::lock_guard<std::mutex> lock(init_mu);
+  if (!S.pinned) {
+    uint8_t* p = nullptr;
+    if (cudaHostAlloc(&p, 2 * kStageChunk, cudaHostAllocPortable) != cudaSuccess) return nullptr;
+    if (cudaEventCreateWithFlags(&S.ev[0], cudaEventDisableTiming) != cudaSuccess ||  // on `device` (the caller's)
+        cudaEventCreateWithFlags(&S.ev[1], cudaEventDisableTiming) != cudaSuccess) {
+      cudaFreeHost(p);
+      return nullptr;
+    }
+    S.pinned = p;
+  }
+  return &S;
+}
+
+int stage_threads() {
+  static const int env = getenv("CT_JSONL_UPLOAD_THREADS") ? atoi(getenv("CT_JSONL_UPLOAD_THREADS")) : 8;
+  return std::max(1, std::min(env, omp_get_max_threads()));
+}
+
+void par_copy(uint8_t* dst, const uint8_t* src, uint64_t len, int nthr) {
+  const uint64_t part = (len + nthr - 1) / nthr;
+#pragma omp parallel for num_threads(nthr) schedule(static)
+  for (int q = 0; q < nthr; q++) {
+    const uint64_t a = (uint64_t)q * part;
+    if (a < len) memcpy(dst + a, src + a, std::min(part, len - a));
+  }
+}
+
+bool staged(uint64_t size, uint64_t min_size) {
+  return size >= min_size && !getenv("CT_JSONL_PAGEABLE");
+}
+
+int upload_text(ct_jsonl* j, uint8_t* d, const uint8_t* text, uint64_t size) {
+  Staging* S = staged(size, 4 * kStageChunk) ? staging_for(j->device) : nullptr;
+  if (!S) {
     JL_TRY(cudaMemcpyAsync(d, text, size, cudaMemcpyHostToDevice, j->st));
     return 0;
   }
-  std::lock_guard<std::mutex> lock(mu_of[j->device]);
-  uint8_t*& pinned = pinned_of[j->device];
-  cudaEvent_t* ev = ev_of[j->device];
-  if (!pinned) {
-    if (cudaHostAlloc(&pinned, 2 * kStageChunk, cudaHostAllocPortable) != cudaSuccess) {
-      pinned = nullptr;
-      JL_TRY(cudaMemcpyAsync(d, text, size, cudaMemcpyHostToDevice, j->st));
-      return 0;
-    }
-    JL_TRY(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));  // on j->device (set by the caller)
-    JL_TRY(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
-  }
-  static const int nthr_env = getenv("CT_JSONL_UPLOAD_THREADS") ? atoi(getenv("CT_JSONL_UPLOAD_THREADS")) : 4;
-  const int nthr = std::max(1, std::min(nthr_env, omp_get_max_threads()));
+  std::lock_guard<std::mutex> lock(S->mu);
+  const int nthr = stage_threads();
   uint64_t k = 0;
   for (uint64_t off = 0; off < size; off += kStageChunk, k++) {
     const int slot = (int)(k & 1);
-    if (k >= 2) JL_TRY(cudaEventSynchronize(ev[slot]));  // the slot's previous DMA is done
+    if (k >= 2) JL_TRY(cudaEventSynchronize(S->ev[slot]));  // the slot's previous DMA is done
     const uint64_t len = std::min(kStageChunk, size - off);
-    uint8_t* dst = pinned + slot * kStageChunk;
-    const uint64_t part = (len + nthr - 1) / nthr;
-#pragma omp parallel for num_threads(nthr) schedule(static)
-    for (int q = 0; q < nthr; q++) {
-      const uint64_t a = (uint64_t)q * part;
-      if (a < len) memcpy(dst + a, text + off + a, std::min(part, len - a));
-    }
-    JL_TRY(cudaMemcpyAsync(d + off, dst, len, cudaMemcpyHostToDevice, j->st));
-    JL_TRY(cudaEventRecord(ev[slot], j->st));
+    uint8_t* stg = S->pinned + slot * kStageChunk;
+    par_copy(stg, text + off, len, nthr);
+    JL_TRY(cudaMemcpyAsync(d + off, stg, len, cudaMemcpyHostToDevice, j->st));
+    JL_TRY(cudaEventRecord(S->ev[slot], j->st));
   }
   // the staging slots are reused by the next call: their last DMAs must finish first
-  JL_TRY(cudaEventSynchronize(ev[(k - 1) & 1]));
+  JL_TRY(cudaEventSynchronize(S->ev[(k - 1) & 1]));
+  return 0;
+}
+
+// Device -> pageable host (the timestamps): DMA chunk k + 1 into one slot while host
+// threads copy chunk k out of the other.
+int download(ct_jsonl* j, uint8_t* host, const uint8_t* d, uint64_t size) {
+  Staging* S = staged(size, kStageChunk) ? staging_for(j->device) : nullptr;
+  if (!S) {
+    JL_TRY(cudaMemcpyAsync(host, d, size, cudaMemcpyDeviceToHost, j->st));
+    JL_TRY(cudaStreamSynchronize(j->st));
+    return 0;
+  }
+  std::lock_guard<std::mutex> lock(S->mu);
+  const int nthr = stage_threads();
+  const uint64_t nk = (size + kStageChunk - 1) / kStageChunk;
+  auto issue = [&](uint64_t k) -> cudaError_t {
+    const uint64_t off = k * kStageChunk, len = std::min(kStageChunk, size - off);
+    cudaError_t e = cudaMemcpyAsync(S->pinned + (k & 1) * kStageChunk, d + off, len, cudaMemcpyDeviceToHost, j->st);
+    return e == cudaSuccess ? cudaEventRecord(S->ev[k & 1], j->st) : e;
+  };
+  JL_TRY(issue(0));
+  for (uint64_t k = 0; k < nk; k++) {
+    if (k + 1 < nk) JL_TRY(issue(k + 1));  // the other slot: its copy-out (chunk k - 1) is done
+    JL_TRY(cudaEventSynchronize(S->ev[k & 1]));
+    const uint64_t off = k * kStageChunk;
+    par_copy(host + off, S->pinned + (k & 1) * kStageChunk, std::min(kStageChunk, size - off), nthr);
+  }
   return 0;
 }
 
@@ -2498,11 +2549,15 @@ int ct_jsonl_parse(int device, const char* text, uint64_t size, int on_device, c
 int ct_jsonl_records(ct_jsonl* j, ct_record* dev_out, int64_t* host_ts) {
   if (!j) return CT_ERR_ARGUMENT;
   const uint64_t n = j->info.n_records;
-  cudaError_t e = cudaSuccess;
-  if (n && dev_out) e = cudaMemcpyAsync(dev_out, j->recs, n * sizeof(ct_record), cudaMemcpyDeviceToDevice, j->st);
-  if (e == cudaSuccess && n && host_ts)
-    e = cudaMemcpyAsync(host_ts, j->ts, n * sizeof(int64_t), cudaMemcpyDeviceToHost, j->st);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(j->st);
+  cudaError_t e = cudaSetDevice(j->device);  // the staging events belong to the device
+  if (e == cudaSuccess && n && dev_out) e = cudaMemcpyAsync(dev_out, j->recs, n * sizeof(ct_record), cudaMemcpyDeviceToDevice, j->st);
+  if (e != cudaSuccess) { j->err = cudaGetErrorString(e); return CT_ERR_CUDA; }
+  if (n && host_ts) {
+    if (download(j, reinterpret_cast<uint8_t*>(host_ts), reinterpret_cast<const uint8_t*>(j->ts),
+                 n * sizeof(int64_t)))
+      return CT_ERR_CUDA;
+  }
+  e = cudaStreamSynchronize(j->st);
   if (e != cudaSuccess) { j->err = cudaGetErrorString(e); return CT_ERR_CUDA; }
   return CT_OK;
 }
