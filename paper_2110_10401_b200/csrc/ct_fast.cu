@@ -891,8 +891,7 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
           const bool isHB = (kindB == CT_KIND_COLLECTIVE && (bB.y >> 16) == 0) || kindB == CT_KIND_SEND;
           const bool isCpA = (uint32_t)(kindA - CT_KIND_MEMCPY) < 3u, isCpB = (uint32_t)(kindB - CT_KIND_MEMCPY) < 3u;
           const unsigned hmA = __ballot_sync(kFull, isHA), hmB = __ballot_sync(kFull, isHB);
-          const unsigned cpm = __popc(__ballot_sync(kFull, isCpA)) + __popc(__ballot_sync(kFull, isCpB));
-          cover += lane == 0 ? (int)cpm : 0;
+          cover += (int)isCpA + (int)isCpB;  // copies tile the range too (summed over lanes at the end)
           const uint32_t nA = __popc(hmA);
           if (isHA) W.q[(qt + __popc(hmA & lt)) & kQM] = relA;
           if (isHB) W.q[(qt + nA + __popc(hmB & lt)) & kQM] = relB;
