@@ -129,6 +129,13 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t pari
   }
 }
 
+// one ring record (two 128-bit words) at a shared-window address; volatile keeps it
+// after the mbarrier waits that publish the ring slot
+__device__ __forceinline__ void lds256(uint32_t a, uint4& x, uint4& y) {
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(x.x), "=r"(x.y), "=r"(x.z), "=r"(x.w) : "r"(a));
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4+16];" : "=r"(y.x), "=r"(y.y), "=r"(y.z), "=r"(y.w) : "r"(a));
+}
+
 __device__ __forceinline__ Rec ring_rec(const ct_record* R, uint32_t pos) { return load_shared(R + (pos & kRM)); }
 
 __device__ __forceinline__ bool is_start(int kind, uint32_t rank) {
@@ -740,6 +747,15 @@ __device__ __forceinline__ void expand_block(const FastParams& P, Sink<SH>& sk, 
   sk.flags |= expand_direct<SH>(P, R, h, p, gidx, j0, fastdev, packed, devs, algo);
 }
 
+// nibble r of the result = nibble r ^ x of d (x < 8): the device word of a walk that
+// visited rank k ^ x at step k, back in rank order
+__device__ __forceinline__ uint32_t nibble_xor(uint32_t d, uint32_t x) {
+  if (x & 1u) d = ((d >> 4) & 0x0F0F0F0Fu) | ((d << 4) & 0xF0F0F0F0u);
+  if (x & 2u) d = __byte_perm(d, 0, 0x2301);
+  if (x & 4u) d = __byte_perm(d, 0, 0x1032);
+  return d;
+}
+
 __device__ __noinline__ void count_diag(uint32_t st) {
   if (st == ST_INCOMPAT) atomicAdd(&cta_mem().diag[CT_DIAG_INCOMPATIBLE], 1u);
   else if (st == ST_DUPDEV) atomicAdd(&cta_mem().diag[CT_DIAG_DUPLICATE_DEVICE], 1u);
@@ -1002,10 +1018,33 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
 #ifndef CT_N8
 #define CT_N8 1
 #endif
+            bool walked = false;
             if (CT_N8 && all8) {  // every block of the batch has 8 ranks: fully unrolled
+              // The common case first: every member record is the head's record with its
+              // own rank and device (same count, seq, comm, aux, aux2, kind byte and flags
+              // byte).  One OR of XORs per word proves it; lane l visits rank k ^ (l & 7)
+              // (bank spread) and keeps device nibbles in visit order.  Any difference, a
+              // device >= 32 or a block across the ring's end takes the field-by-field walk,
+              // which decides the same flags exactly.
+              const uint32_t jx = (uint32_t)lane & 7u;
+              const uint32_t Bs = ring_a + 32u * (p & kRM), jx32 = jx << 5;
+              const uint32_t nj = n | (jx << 16);
+              uint32_t E = (p & kRM) > (uint32_t)kRM - 7u ? 1u : 0u, zor = 0, D = 0;
 #pragma unroll
-              for (uint32_t k = 0; k < 8; k++) vrec((j0 + k) & 7u);
-            } else {
+              for (uint32_t k = 0; k < 8; k++) {
+                uint4 wa, wb;
+                lds256(Bs + (jx32 ^ (k << 5)), wa, wb);
+                E |= (wa.x ^ hc0) | (wa.y ^ hc1) | (wa.z ^ hq0) | (wa.w ^ hq1);
+                E |= (wb.x ^ h.comm) | (wb.y ^ nj ^ (k << 16)) | ((wb.z ^ hw6) & 0xFFFF0000u) | (wb.w ^ hw7);
+                zor |= wb.z;
+                m32 |= 1u << (wb.z & 31u);
+                D |= (wb.z & 15u) << (4 * k);
+              }
+              walked = E == 0 && (zor & 0xFFE0u) == 0;
+              if (CT_LIKELY(walked)) devs = nibble_xor(D, jx);  // nibble r = device of rank r
+              else m32 = 0;
+            }
+            if (!walked) {
               uint32_t j = j0;
               uint32_t i = 0;
               for (; i + 1 < n; i += 2) {
