@@ -470,12 +470,14 @@ __device__ __noinline__ bool seq_order_ranks(const ct_record* R, uint32_t p, uin
 // bit 0 = two records share a device, bit 1 = every device is < gcap
 __device__ __noinline__ uint32_t block_devices(const ct_record* R, uint32_t p, uint32_t n, uint32_t gcap) {
   bool dup = false, below = true;
+  uint32_t top = 0;
   for (uint32_t m = 0; m < n; m++) {
     const uint32_t d = R[(p + m) & kRM].dev;
+    top = max(top, d);
     below = below && d < gcap;
     for (uint32_t m2 = 0; m2 < m; m2++) dup = dup || R[(p + m2) & kRM].dev == d;
   }
-  return (dup ? 1u : 0u) | (below ? 2u : 0u);
+  return (dup ? 1u : 0u) | (below ? 2u : 0u) | (top << 16);
 }
 
 // p2p order: per (comm, src, dst) channel, send seqs and recv seqs non-decreasing in file
@@ -880,6 +882,7 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
               if (ck != CT_CKIND_H2D) my_max_dev = max(my_max_dev, (int)aux);
               if (ck != CT_CKIND_D2H) my_max_dev = max(my_max_dev, (int)aux2);
             }
+            my_max_dev = max(my_max_dev, (int)(b.z & 0xFFFF));  // the record's own device (d, matrix.py:250-258)
             const int t = kind - CT_KIND_MEMCPY;  // statistics: the host sums the type's cells
             if (!no_expand) {
               const int src = ck == CT_CKIND_H2D ? -1 : (int)aux, dst = ck == CT_CKIND_D2H ? -1 : (int)aux2;
@@ -902,7 +905,6 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
           const uint4 bA = reinterpret_cast<const uint4*>(R + (relA & kRM))[1];  // any ring slot is readable
           const uint4 bB = reinterpret_cast<const uint4*>(R + (relB & kRM))[1];
           const int kindA = actA ? (int)((bA.w >> 16) & 7) : 7, kindB = actB ? (int)((bB.w >> 16) & 7) : 7;
-          my_max_dev = max(my_max_dev, max(actA ? (int)(bA.z & 0xFFFF) : -1, actB ? (int)(bB.z & 0xFFFF) : -1));
           const bool isHA = (kindA == CT_KIND_COLLECTIVE && (bA.y >> 16) == 0) || kindA == CT_KIND_SEND;
           const bool isHB = (kindB == CT_KIND_COLLECTIVE && (bB.y >> 16) == 0) || kindB == CT_KIND_SEND;
           const bool isCpA = (uint32_t)(kindA - CT_KIND_MEMCPY) < 3u, isCpB = (uint32_t)(kindB - CT_KIND_MEMCPY) < 3u;
@@ -1060,10 +1062,12 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
             if (CT_LIKELY(!big)) {  // devices < 32: the mask holds them all
               dup = __popc(m32) != (int)n;  // pairwise distinct devices
               fastdev = P.gcap >= 32 || (m32 >> P.gcap) == 0;
+              my_max_dev = max(my_max_dev, 31 - __clz(m32));  // the block's devices (d)
             } else {
               const uint32_t info = block_devices(R, p, n, (uint32_t)P.gcap);
               dup = (info & 1u) != 0;
               fastdev = (info & 2u) != 0;
+              my_max_dev = max(my_max_dev, (int)(info >> 16));
             }
             packed = !big && n <= 8 && (m32 >> 16) == 0;
             st = incw ? ST_INCOMPAT : (dup ? ST_DUPDEV : ST_VALID);
@@ -1073,6 +1077,7 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
             st = (r.count != h.count || r.dtype() != h.dtype()) ? ST_MISMATCH : ST_VALID;  // decompose.py:362-372
             rseq = r.seq;
             rdev = r.dev;
+            my_max_dev = max(my_max_dev, (int)max(h.dev, rdev));
           }
           {  // per (comm, rank) seq strictly increasing from the comm's previous block
             const bool pu = __shfl_sync(kFull, uniform, pl < 0 ? lane : pl);
