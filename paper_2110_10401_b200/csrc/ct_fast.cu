@@ -994,7 +994,9 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
           uint64_t rseq = 0;
           uint32_t rdev = 0;
           const uint32_t j0 = n == 0 ? 0u : ((n & (n - 1)) == 0 ? (uint32_t)lane & (n - 1) : (uint32_t)lane % n);
-          const bool all8 = __all_sync(kFull, !isC || bad || h.nranks == 8);  // warp-uniform choice
+          // warp-uniform choice: every block of the batch has 8 ranks and none crosses the
+          // ring's end (else one lane's fallback walk would run next to everyone's fast walk)
+          const bool all8 = __all_sync(kFull, !isC || bad || (h.nranks == 8 && (p & kRM) <= (uint32_t)kRM - 7u));
           if (isC && !bad) {
             // compare raw words against the head: w4 comm, w5 nranks | rank << 16, w6 dev |
             // aux << 16 (aux = root when rooted), w7 aux2 | kc << 16 | ad << 24
@@ -1025,13 +1027,13 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
               // The common case first: every member record is the head's record with its
               // own rank and device (same count, seq, comm, aux, aux2, kind byte and flags
               // byte).  One OR of XORs per word proves it; lane l visits rank k ^ (l & 7)
-              // (bank spread) and keeps device nibbles in visit order.  Any difference, a
-              // device >= 32 or a block across the ring's end takes the field-by-field walk,
-              // which decides the same flags exactly.
+              // (bank spread) and keeps device nibbles in visit order.  Any difference or a
+              // device >= 32 takes the field-by-field walk, which decides the same flags
+              // exactly.
               const uint32_t jx = (uint32_t)lane & 7u;
               const uint32_t Bs = ring_a + 32u * (p & kRM), jx32 = jx << 5;
               const uint32_t nj = n | (jx << 16);
-              uint32_t E = (p & kRM) > (uint32_t)kRM - 7u ? 1u : 0u, zor = 0, D = 0;
+              uint32_t E = (p & kRM) > (uint32_t)kRM - 7u ? 1u : 0u, zor = 0, D = 0;  // (excluded by all8)
 #pragma unroll
               for (uint32_t k = 0; k < 8; k++) {
                 uint4 wa, wb;
