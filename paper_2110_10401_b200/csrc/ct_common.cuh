@@ -160,6 +160,10 @@ __device__ __forceinline__ uint64_t udiv_small(uint64_t s, uint32_t n) {
 }
 
 __device__ __forceinline__ uint64_t ceil_div(uint64_t s, uint32_t n) {
+  if ((n & (n - 1)) == 0) {  // power-of-two communicators (the common 2 / 4 / 8): a shift
+    const uint32_t k = 31 - __clz(n);
+    return (s >> k) + ((s & (n - 1)) != 0 ? 1 : 0);
+  }
   const uint64_t q = udiv_small(s, n);
   return q + (q * n != s ? 1 : 0);
 }
