@@ -886,9 +886,10 @@ __global__ void __launch_bounds__(kThreads, 1) fast_kernel(FastParams P) {
             const int t = kind - CT_KIND_MEMCPY;  // statistics: the host sums the type's cells
             if (!no_expand) {
               const int src = ck == CT_CKIND_H2D ? -1 : (int)aux, dst = ck == CT_CKIND_D2H ? -1 : (int)aux2;
-              if (src < P.gcap && dst < P.gcap && (cnt >> 63) == 0) {
-                const int a = src < 0 ? kHost : src + 2, bb = dst < 0 ? kHost : dst + 2;
-                sk.add((uint32_t)(((CT_T_EXPLICIT + t) * P.g2 + a) * P.g2 + bb), cnt);
+              // table rows: host 0, gpu g at g + 2 (an in-table endpoint is a row < g2)
+              const uint32_t a = (uint32_t)(src + 2) & (src < 0 ? 0u : ~0u), bb = (uint32_t)(dst + 2) & (dst < 0 ? 0u : ~0u);
+              if (max(a, bb) < (uint32_t)P.g2 && (cnt >> 63) == 0) {
+                sk.add((uint32_t)((CT_T_EXPLICIT + t) * P.g2 * P.g2) + a * (uint32_t)P.g2 + bb, cnt);
               } else {  // an endpoint outside the table or >= 2^63 bytes (out of line)
                 sk.flags |= copy_edge_slow<SH>(P, rb0 + rel, CT_T_EXPLICIT + t, src, dst, cnt);
               }
